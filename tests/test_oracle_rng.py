@@ -1,0 +1,84 @@
+"""Pins of the oracle's random-number contract (R13, R14) against
+things other than the oracle itself: the Random123 known-answer vectors, the
+exact u-grid, libm/numpy log2 over every value the uniform map can produce.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _kat_rows():
+    rows = []
+    with open(os.path.join(GOLDEN, "philox4x32_10_kat.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            v = [int(t, 16) for t in line.split()]
+            rows.append((v[0:4], v[4:6], v[6:10]))
+    return rows
+
+
+@pytest.mark.parametrize("ctr,key,expect", _kat_rows())
+def test_philox_known_answers(ctr, key, expect):
+    assert list(oracle.philox(ctr, key)) == expect
+
+
+def test_uniform_grid_is_exact_and_open():
+    # u = (2*(x>>9)+1) 2^-24: the extremes and a mid value, computed from the definition
+    assert oracle.uniform(0) == 2.0 ** -24
+    assert oracle.uniform(0xFFFFFFFF) == 1.0 - 2.0 ** -24
+    assert oracle.uniform(0x1FF) == 2.0 ** -24          # low 9 bits are dropped
+    assert oracle.uniform(0x80000000) == (2 * (1 << 22) + 1) * 2.0 ** -24
+    rng = np.random.default_rng(1)
+    for x in rng.integers(0, 2 ** 32, size=2000, dtype=np.uint64):
+        u = oracle.uniform(int(x))
+        assert 0.0 < u < 1.0
+        k = u * 2 ** 24
+        assert k == int(k) and int(k) % 2 == 1
+
+
+def test_det_log2_exhaustive_against_libm():
+    """Every u the uniform map can produce (2^23 values): det_log2 within 2 ulp of
+    log2 in double, strictly negative, and non-decreasing in u (A-Res keys,
+    P:1042-1049, must be a monotone transform of r)."""
+    j = np.arange(1 << 23, dtype=np.float64)
+    u64 = (2.0 * j + 1.0) / 2.0 ** 24
+    u = u64.astype(np.float32)
+    assert np.all(u.astype(np.float64) == u64)
+    got = oracle.det_log2_many(u).astype(np.float64)
+    ref = np.log2(u64)
+    ulp = np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
+    err = np.abs(got - ref) / ulp
+    assert err.max() <= 2.0, err.max()
+    assert np.all(got < 0.0)
+    assert np.all(np.diff(got) >= 0.0)
+
+
+def test_det_log2_powers_of_two_exact():
+    for e in range(-24, 0):
+        assert oracle.det_log2(2.0 ** e) == float(e)
+    # SPEC.md S:267-268 (golden/spec_worked_examples.txt wrs_key_w1/w2): key = (1/w) log2 r
+    import ctypes
+    k1 = np.float32(oracle.det_log2(0.5)) * np.float32(1.0 / 1.0)
+    k2 = np.float32(oracle.det_log2(0.5)) * np.float32(1.0 / 2.0)
+    assert k1 == -1.0 and k2 == -0.5
+    # S:269 monotone in w at fixed r = 0.25
+    L = np.float32(oracle.det_log2(0.25))
+    assert L * np.float32(1 / 4) > L * np.float32(1 / 2) > L * np.float32(1 / 1)
+
+
+def test_start_node_uniform():
+    """Alg. 1: u ~ U{0, n-1}; chi-square over (ant, iteration) pairs."""
+    from scipy.stats import chisquare
+    n = 7
+    seed = 42
+    counts = np.zeros(n)
+    for it in range(40):
+        for a in range(1000):
+            counts[oracle.start_node(n, a, it, seed)] += 1
+    assert chisquare(counts).pvalue > 1e-3
