@@ -1,0 +1,305 @@
+"""bench.py -- candidate tours/s of the MMAS hot path on synthetic pr1002-shaped
+instances (BASELINE.json metric), 1..8 B200 (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step = one full MMAS iteration: every ant of
+the colony builds a tour, the iteration/global best is selected (with the
+all-gather exchange for N > 1) and the pheromone update runs.  Weak scaling:
+each GPU builds n_ants (1002 for C2) per step; value = all ranks' tours / the
+max-over-ranks device time.  L2 is flushed (256 MiB write) between timed steps,
+outside the per-step CUDA-event intervals.
+
+--impl reference times the CPU oracle (oracle/) on the host
+cores on a bounded sample of the same workload; it is the slow baseline, not
+the product.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2003_11902_b200.instances import CONFIGS  # noqa: E402
+
+METRIC = "candidate tours/sec (pr1002-shaped, 1/2/4/8 B200) and % L2/HBM roofline"
+UNIT = "tours/s"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6454.0), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv = None
+            self.err = str(e)
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self._t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": sorted(self.reasons)}
+
+
+def algorithmic_bytes_per_tour(w):
+    """Sec. 8(d): bytes of choice_info / candidate rows an ant's construction reads.
+    cl > 0: (n-1) steps x cl candidates x (4 B inv_w + 2 B id);  cl = 0: sum over steps of
+    the unvisited entries of the inv_w row, (n-1) n / 2 x 4 B."""
+    if w.cand_len:
+        return (w.n - 1) * w.cand_len * 6
+    return (w.n - 1) * w.n // 2 * 4
+
+
+def cpu_baseline_leg(w, budget_s=12.0):
+    """The oracle as it stands on this host's cores, bounded to ~budget_s of CPU work."""
+    import oracle
+    cores = os.cpu_count() or 1
+    col = oracle.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, nthreads=cores)
+    t0 = time.perf_counter()
+    iters = 0
+    while True:
+        col.iterate(1)
+        iters += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or iters >= 1000:
+            break
+    return {"value": w.n_ants * iters / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{iters} full oracle iterations of {w.name} (m={w.n_ants}, cl={w.cand_len}) in {el:.1f} s "
+                      f"on {cores} host threads"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w = CONFIGS[args.config]
+    import oracle
+    cores = os.cpu_count() or 1
+    col = oracle.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, nthreads=cores)
+    for _ in range(args.warmup if args.warmup < 3 else 1):
+        col.iterate(1)
+    # bounded: each step is one full oracle iteration; cap the number of timed steps
+    t_probe = time.perf_counter()
+    col.iterate(1)
+    t_iter = time.perf_counter() - t_probe
+    steps = int(max(1, min(args.steps, 90.0 // max(t_iter, 1e-3))))
+    t0 = time.perf_counter()
+    col.iterate(steps)
+    el = time.perf_counter() - t0
+    value = w.n_ants * steps / el
+    sample = f"{steps} of the requested {args.steps} steps (full {w.n_ants}-ant oracle iterations of {w.name})"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": el / steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": w.name, "n": w.n, "n_ants": w.n_ants, "cand_len": w.cand_len},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2003_11902_b200 import mmas
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    w = CONFIGS[args.config]
+    m_total = w.n_ants * world                      # weak scaling: n_ants per GPU
+    coords = w.coords()
+    stream = torch.cuda.current_stream().cuda_stream
+    col = mmas.Colony(coords, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=local_rank,
+                      stream=stream, rank=rank, world=world)
+    rb = col.record_bytes
+    local = torch.zeros(rb, dtype=torch.uint8, device="cuda")
+    gathered = torch.zeros(world * rb, dtype=torch.uint8, device="cuda")
+
+    def step():
+        if world == 1:
+            col.iterate(1)
+        else:
+            col.construct(local.data_ptr())
+            dist.all_gather_into_tensor(gathered, local)
+            col.update(gathered.data_ptr(), world)
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MiB > 126 MB L2
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = col.kernel_launches
+    col.profile(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record()
+            step()
+            ev[k][1].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    gpu_launches = col.kernel_launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(np.sum(step_ms))
+    phases = col.phase_times()
+    col.profile(False)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    tours = m_total * args.steps
+    value = tours / (total_ms * 1e-3)
+
+    # roofline of the dominant kernel (construction), live CUDA-event time on its stream
+    cons_ms = phases["construct_ms"] / max(phases["iterations"], 1)
+    bytes_per_launch = algorithmic_bytes_per_tour(w) * col.shard()[1]
+    hbm_peak, peak_src = measured_peaks()
+    achieved = bytes_per_launch / (cons_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": None, "kernel": "construct_cl_kernel" if w.cand_len else "construct_full_kernel",
+                "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
+                "kernel_ms": cons_ms, "kernel_share_of_step": cons_ms / (total_ms / args.steps),
+                "algorithmic_bytes_per_launch": bytes_per_launch,
+                "note": "bytes = (n-1)*cl*6 per tour (4 B inv_w + 2 B id per candidate), SURVEY 8(d); the kernel "
+                        "is issue/latency-bound (ALU + dependent chain), see DESIGN.md Sec. 6"}
+    update_ms = phases["update_ms"] / max(phases["iterations"], 1)
+    upd_bytes = 16 * w.n * w.n
+    update_roof = {"kernel": "pheromone_update_kernel", "kernel_ms": update_ms,
+                   "achieved_gbs": upd_bytes / (update_ms * 1e-3) / 1e9,
+                   "frac": upd_bytes / (update_ms * 1e-3) / 1e9 / hbm_peak,
+                   "algorithmic_bytes_per_launch": upd_bytes}
+
+    # e2e through the C ABI with host buffers: create from host coords (H2D), then per step
+    # iterate + read the global best back to the host (D2H), all inside the timed region.
+    e2e = None
+    if rank == 0 and world == 1:
+        torch.cuda.synchronize()
+        pinned = torch.from_numpy(coords.copy()).pin_memory().numpy()
+        out_steps = args.steps
+        t0 = time.perf_counter()
+        c2 = mmas.Colony(pinned, w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=local_rank)
+        for _ in range(out_steps):
+            c2.iterate(1)
+            c2.best_tour()
+        el = time.perf_counter() - t0
+        c2.close()
+        e2e = {"value": w.n_ants * out_steps / el, "unit": UNIT,
+               "h2d_bytes_per_step": 16 * w.n / out_steps, "d2h_bytes_per_step": 2 * w.n + 8,
+               "note": "mmas_create from host coords + per step mmas_iterate(1) + mmas_best_tour (sync, D2H)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_leg(w)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{w.name} ({args.config}): n={w.n}, {w.n_ants} ants per GPU, "
+                                       f"cl={w.cand_len}, rho={w.rho}, alpha=1, beta=2",
+                           "n": w.n, "ants_per_gpu": w.n_ants, "global_ants": m_total, "cand_len": w.cand_len,
+                           "parallelism": f"ant-sharded x{world}" if world > 1 else "single GPU",
+                           "l2": "flushed between timed steps (256 MiB write, outside the step events)",
+                           "paper_context": "V100 pr1002 WRS-BT cl=32 construction: 1.08M tours/s (P:1549), "
+                                            "other hardware, construction only"},
+                "roofline": roofline, "update_roofline": update_roof,
+                "phases_ms_per_step": {"construct": cons_ms, "select": phases["select_ms"] / max(phases["iterations"], 1),
+                                       "update": update_ms},
+                "construction_only_tours_per_s": w.n_ants / (cons_ms * 1e-3),
+                "gpu_launches": gpu_launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+                "fallback_steps_per_tour": col.stats()["fallback_steps"] / max(col.stats()["iterations"], 1) / col.shard()[1]}
+        print(json.dumps(line), flush=True)
+    col.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,167 @@
+/*
+ * mmas.h -- C ABI of the B200-native MAX-MIN Ant System hot path.
+ *
+ * Implements the per-iteration colony step of Skinderowicz, "Implementing a
+ * GPU-based parallel MAX-MIN Ant System" (arXiv 2003.11902): tour construction
+ * by weighted reservoir sampling (Sec. 4.2.2, Alg. 3) over
+ * candidate lists (Sec. 4.3) with a bitmask tabu (Sec. 4.1,
+ * P:806-815), then the MMAS pheromone update (Sec. 2.1, Alg. 1,
+ * P:278-325).  The problem statement is the symmetric TSP on a complete graph
+ * with TSPLIB EUC_2D distances.  Every numerical
+ * convention the paper leaves open is fixed in DESIGN.md Sec. 3 (readings R1-R22);
+ * results are bit-identical to the CPU oracle in oracle/.
+ *
+ * Conventions for every call:
+ *  - Plain C types only.  Host pointers unless a parameter says "device".
+ *  - Errors: calls returning int return 0 (MMAS_OK) or a negative mmas_status;
+ *    calls returning a pointer return NULL.  mmas_last_error() then gives a
+ *    thread-local, human-readable message (valid until the next call on this thread).
+ *  - A context is bound to one CUDA device and one stream; it is NOT thread-safe.
+ *    Use one context per device per process.
+ *  - All work is asynchronous with respect to the host unless stated otherwise.
+ */
+#ifndef MMAS_H
+#define MMAS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mmas_ctx mmas_ctx;
+
+typedef enum mmas_status {
+    MMAS_OK = 0,
+    MMAS_EINVAL = -1, /* invalid argument */
+    MMAS_ENOMEM = -2, /* device or host allocation failed */
+    MMAS_ECUDA = -3,  /* a CUDA runtime call or kernel failed */
+    MMAS_ENCCL = -4,  /* reserved: collective failure (exchange is done by the caller) */
+    MMAS_ESTATE = -5  /* call not valid in the current state (e.g. no global best yet) */
+} mmas_status;
+
+enum { MMAS_DEPOSIT_ITERATION_BEST = 0, MMAS_DEPOSIT_GLOBAL_BEST = 1 }; /* Alg.1 l.288 / P:332-333 (R7) */
+enum { MMAS_FALLBACK_WRS = 0, MMAS_FALLBACK_ARGMAX = 1 };               /* R9 */
+
+/* Full configuration (mmas_config_init() fills the defaults). */
+typedef struct mmas_config {
+    const double *coords;  /* 2n interleaved x,y (host).  Copied; caller may free after create. */
+    int32_t n;             /* cities, 3 <= n < 65536 (u16 ids, Tab. 1 caption P:822-824) */
+    double alpha;          /* pheromone exponent (Eq. 1); integer in [0,8] (R17) */
+    double beta;           /* heuristic exponent; >= 0 (R18) */
+    double rho;            /* retention: evaporation tau <- max(rho tau, tau_min) (R1); 0 < rho < 1 */
+    int32_t n_ants;        /* colony size m (global, over all ranks); 1 <= m < 2^24 */
+    int32_t cand_len;      /* candidate-list length cl, 0 <= cl <= min(n-1, 128); 0 = full-row WRS */
+    uint64_t seed;         /* Philox key (R13) */
+    double p_best;         /* trail-limit parameter; default 0.01 */
+    int32_t deposit;       /* MMAS_DEPOSIT_*; default iteration best */
+    int32_t fallback;      /* MMAS_FALLBACK_*; default WRS over all unvisited */
+    int32_t local_search;  /* 2-opt (row a8); must be 0 in this version */
+    int32_t device;        /* CUDA device ordinal; -1 = current device */
+    void *stream;          /* cudaStream_t to run on; NULL = a stream owned by the context */
+    int32_t rank, world;   /* ant shard: this context builds global ants [floor(rank*m/world),
+                              floor((rank+1)*m/world)) (R21); default 0, 1 */
+} mmas_config;
+
+/* Per-context counters (cumulative since create). */
+typedef struct mmas_stats {
+    int64_t iterations;       /* completed iterations (== the global iteration counter, R20) */
+    int64_t fallback_steps;   /* construction steps that fell back to all unvisited cities (R9), this shard */
+    int64_t ant_steps;        /* construction steps taken by this shard's ants */
+    int32_t ants_local;       /* ants built by this context per iteration */
+    int32_t first_ant;        /* global id of the first of them */
+} mmas_stats;
+
+/* Last error message of this thread ("" if none). */
+const char *mmas_last_error(void);
+
+/* Fills cfg with defaults (p_best 0.01, iteration-best deposit, WRS fallback,
+ * no local search, current device, own stream, rank 0 of 1). */
+void mmas_config_init(mmas_config *cfg);
+
+/* Creates a colony and runs setup (row a0): eta^beta, candidate lists, the
+ * nearest-neighbour tour and initial limits (Alg. 1),
+ * tau = tau_max, inv_w = 1/choice_info.  Synchronous.
+ * Returns NULL on error (see mmas_last_error). */
+mmas_ctx *mmas_create(const double *coords, int32_t n, double alpha, double beta, double rho,
+                      int32_t n_ants, int32_t cand_len, uint64_t seed);
+
+/* As mmas_create with every option; *out receives the context.  Returns mmas_status. */
+int mmas_create_ex(const mmas_config *cfg, mmas_ctx **out);
+
+/* Runs `iters` complete MMAS iterations (Alg. 1): construction
+ * of every ant's route (a1-a4), iteration/global best and limits (a5),
+ * evaporation + deposit + clamp and choice_info refresh (a6).  Single-rank
+ * contexts only (world == 1; otherwise MMAS_ESTATE -- use the split calls).
+ * Asynchronous. iters >= 1. */
+int mmas_iterate(mmas_ctx *h, int32_t iters);
+
+/* ---- split iteration for sharded colonies (world > 1; also valid for world == 1) ----
+ * Per iteration:  mmas_construct(h)  ->  caller all-gathers the per-rank records
+ * (e.g. torch.distributed.all_gather_into_tensor / ncclAllGather on the same
+ * stream)  ->  mmas_update(h, gathered, world).  A record is
+ * mmas_record_bytes(h) bytes: uint64 key = (tour_length << 24 | global_ant)
+ * followed by the route as n uint16 city ids. */
+int64_t mmas_record_bytes(const mmas_ctx *h);
+
+/* Builds this shard's routes and writes its best record into `record_dev`
+ * (device pointer, mmas_record_bytes(h) bytes, 8-byte aligned).  Asynchronous. */
+int mmas_construct(mmas_ctx *h, void *record_dev);
+
+/* Reads `count` contiguous records at `records_dev` (device), selects the
+ * iteration best (min key: shortest, ties -> lowest global ant id, R8), updates
+ * the global best and limits, and runs the pheromone update.  Asynchronous. */
+int mmas_update(mmas_ctx *h, const void *records_dev, int32_t count);
+
+/* Synchronises the context's stream and copies the global best route (n city
+ * ids, starting at its route[0]) into tour_out (host, n int32, caller-owned).
+ * Returns its length (>= 0), or MMAS_ESTATE before the first iteration (gb
+ * empty, Alg. 1), or another negative mmas_status. */
+int64_t mmas_best_tour(mmas_ctx *h, int32_t *tour_out);
+
+/* Frees every device and host resource.  NULL is a no-op. */
+void mmas_destroy(mmas_ctx *h);
+
+/* ---- introspection (synchronous; caller-allocated host buffers) ---- */
+int32_t mmas_n(const mmas_ctx *h);
+int32_t mmas_iteration(const mmas_ctx *h);
+/* last iteration's routes of this shard: out has ants_local*n int32 */
+int mmas_get_tours(mmas_ctx *h, int32_t *out, int32_t *first_ant, int32_t *count);
+int mmas_get_lengths(mmas_ctx *h, int64_t *out);             /* ants_local int64 */
+int mmas_get_pheromone(mmas_ctx *h, float *out);             /* n*n float, row-major */
+int mmas_get_inv_w(mmas_ctx *h, float *out);                 /* n*n float: 1/choice_info */
+int mmas_get_heuristic(mmas_ctx *h, float *out);             /* n*n float: eta^beta */
+int mmas_get_candidates(mmas_ctx *h, int32_t *out);          /* n*cl int32 */
+int mmas_get_limits(mmas_ctx *h, float *tau_min, float *tau_max);
+int mmas_get_stats(mmas_ctx *h, mmas_stats *out);
+/* ---- measurement (bench.py) ----
+ * With profiling on, the context brackets each phase of every iteration with
+ * CUDA events on its own stream and accumulates the device time per phase. */
+typedef struct mmas_phase_times {
+    double construct_ms;   /* construction kernels (a1-a5 local) */
+    double select_ms;      /* iteration/global best + limits (a5) */
+    double update_ms;      /* pheromone update kernel (a6) */
+    int64_t iterations;    /* iterations accumulated */
+} mmas_phase_times;
+int mmas_profile(mmas_ctx *h, int32_t enable);                   /* resets the accumulators */
+int mmas_get_phase_times(mmas_ctx *h, mmas_phase_times *out);    /* synchronises */
+/* Number of kernels this context has launched since create (cumulative). */
+int64_t mmas_kernel_launches(const mmas_ctx *h);
+
+/* ---- test hooks for the random-key primitives (R13, R14); synchronous, current device ----
+ * mmas_debug_philox: for i < count, runs the device Philox4x32-10 on counter
+ * ctr_key[6i..6i+3] and key ctr_key[6i+4..6i+5]; writes the 4 output words to
+ * out_words[4i..4i+3] and det_log2(uniform(word)) to out_log2[4i..4i+3] (host).
+ * mmas_debug_log2: out[i] = device det_log2(u[i]) for normal u[i] > 0 (host arrays). */
+int mmas_debug_philox(const uint32_t *ctr_key, int64_t count, uint32_t *out_words, float *out_log2);
+int mmas_debug_log2(const float *u, int64_t count, float *out);
+
+/* Device pointer of the stream the context runs on (cudaStream_t). */
+void *mmas_stream(const mmas_ctx *h);
+/* Synchronises the context's stream. */
+int mmas_sync(mmas_ctx *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMAS_H */

@@ -88,6 +88,8 @@ def lib():
                          ("orc_get_inv_w", ctypes.c_float), ("orc_get_heur", ctypes.c_float),
                          ("orc_get_cand", ctypes.c_int32)):
             getattr(L, name).argtypes = [ctypes.c_void_p, P(ct)]
+        L.orc_construct_ant.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_int32), P(ctypes.c_int64)]
+        L.orc_construct_ant.restype = ctypes.c_int64
         L.orc_best_tour.argtypes = [ctypes.c_void_p, P(ctypes.c_int32)]
         L.orc_best_tour.restype = ctypes.c_int64
         _lib = L
@@ -274,6 +276,13 @@ class Colony:
 
     def cand(self):
         return self._get("orc_get_cand", (self.n, max(self.cl, 0)), np.int32, ctypes.c_int32)
+
+    def construct_ant(self, a):
+        """Route of global ant `a` at the current iteration (colony not advanced)."""
+        out = np.zeros(self.n, dtype=np.int32)
+        fb = ctypes.c_int64()
+        L = lib().orc_construct_ant(self._h, int(a), _ptr(out, ctypes.c_int32), ctypes.byref(fb))
+        return out, int(L), fb.value
 
     def best_tour(self):
         out = np.zeros(self.n, dtype=np.int32)

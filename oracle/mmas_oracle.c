@@ -392,6 +392,29 @@ typedef struct {
     int32_t a0, a1;
 } orc_job;
 
+/* Alg. 1: ant a builds its route for the current iteration.
+ * Returns the number of fallback steps (R9). */
+static int64_t build_route(const orc_t *o, int32_t a, int32_t *route, char *vis)
+{
+    int32_t n = o->p.n;
+    memset(vis, 0, (size_t)n);
+    int64_t fb = 0;
+    int32_t cur = orc_start_node(n, (uint32_t)a, (uint32_t)o->iter, o->key);
+    route[0] = cur;
+    vis[cur] = 1;
+    for (int32_t s = 1; s < n; ++s) {
+        int32_t f;
+        int32_t nxt = orc_select_next(o->inv_w + (size_t)cur * n, o->cand + (size_t)cur * o->p.cl,
+                                      o->p.cl, vis, n, s, (uint32_t)a, (uint32_t)o->iter, o->key,
+                                      o->p.fallback_argmax, &f);
+        fb += f;
+        route[s] = nxt;
+        vis[nxt] = 1;
+        cur = nxt;
+    }
+    return fb;
+}
+
 static void *construct_range(void *arg)
 {
     orc_job *job = arg;
@@ -400,26 +423,22 @@ static void *construct_range(void *arg)
     char *vis = malloc((size_t)n);
     for (int32_t a = job->a0; a < job->a1; ++a) {
         int32_t *route = o->routes + (size_t)a * n;
-        memset(vis, 0, (size_t)n);
-        int64_t fb = 0;
-        int32_t cur = orc_start_node(n, (uint32_t)a, (uint32_t)o->iter, o->key);
-        route[0] = cur;
-        vis[cur] = 1;
-        for (int32_t s = 1; s < n; ++s) {
-            int32_t f;
-            int32_t nxt = orc_select_next(o->inv_w + (size_t)cur * n, o->cand + (size_t)cur * o->p.cl,
-                                          o->p.cl, vis, n, s, (uint32_t)a, (uint32_t)o->iter, o->key,
-                                          o->p.fallback_argmax, &f);
-            fb += f;
-            route[s] = nxt;
-            vis[nxt] = 1;
-            cur = nxt;
-        }
+        o->fallbacks[a] = build_route(o, a, route, vis);
         o->lengths[a] = orc_tour_length(o->xy, n, route);
-        o->fallbacks[a] = fb;
     }
     free(vis);
     return NULL;
+}
+
+/* One ant's route at the current iteration without advancing the colony (for
+ * sampled parity checks at full size).  Returns its length. */
+ORC_EXPORT int64_t orc_construct_ant(const orc_t *o, int32_t a, int32_t *route_out, int64_t *fallbacks)
+{
+    char *vis = malloc((size_t)o->p.n);
+    int64_t fb = build_route(o, a, route_out, vis);
+    free(vis);
+    if (fallbacks) *fallbacks = fb;
+    return orc_tour_length(o->xy, o->p.n, route_out);
 }
 
 /* Pheromone update, Alg. 1, in the paper's order.

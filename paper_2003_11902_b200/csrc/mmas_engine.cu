@@ -1,0 +1,773 @@
+// mmas_engine.cu -- the C ABI (include/mmas.h) and the host-side engine.
+//
+// One context = one colony shard on one CUDA device and one stream.  Setup
+// (row a0) runs once in mmas_create; each iteration is the kernel sequence
+//   construct_{cl,full}  ->  select_best  ->  pheromone_update
+// with no host synchronisation inside the loop (the iteration counter, the
+// limits and the global best live in device memory).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/mmas.h"
+#include "kernels.cuh"
+
+using namespace mmas;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+    g_last_error = msg;
+    return status;
+}
+
+#define CU(call)                                                                                     \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess)                                                                       \
+            return fail(MMAS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));             \
+    } while (0)
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// ---- host side of setup (row a0), written from DESIGN.md R3, R10, R12 ----
+inline int32_t host_dist(const double* xy, int i, int j) {
+    const double dx = xy[2 * i] - xy[2 * j];
+    const double dy = xy[2 * i + 1] - xy[2 * j + 1];
+    const double r = std::sqrt(dx * dx + dy * dy);   // compiled with -ffp-contract=off
+    return (int32_t)(r + 0.5);
+}
+
+// cl nearest neighbours of every city by (d, id), self excluded (R10)
+void candidate_lists(const double* xy, int n, int cl, std::vector<uint16_t>& out) {
+    out.assign((size_t)n * cl, 0);
+    unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    auto work = [&](int r0, int r1) {
+        std::vector<std::pair<int32_t, int32_t>> buf((size_t)n);
+        for (int i = r0; i < r1; ++i) {
+            int k = 0;
+            for (int j = 0; j < n; ++j)
+                if (j != i) buf[k++] = {host_dist(xy, i, j), j};
+            std::partial_sort(buf.begin(), buf.begin() + cl, buf.begin() + k);
+            for (int q = 0; q < cl; ++q) out[(size_t)i * cl + q] = (uint16_t)buf[q].second;
+        }
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < hw; ++t) th.emplace_back(work, (int)((int64_t)n * t / hw), (int)((int64_t)n * (t + 1) / hw));
+    for (auto& t : th) t.join();
+}
+
+// nearest-neighbour tour from city 0, ties -> lowest id; returns its length (R3)
+int64_t nn_tour_length(const double* xy, int n) {
+    std::vector<char> vis((size_t)n, 0);
+    int cur = 0;
+    vis[0] = 1;
+    int64_t len = 0;
+    for (int s = 1; s < n; ++s) {
+        int best = -1;
+        int32_t bd = 0;
+        for (int j = 0; j < n; ++j) {
+            if (vis[j]) continue;
+            const int32_t d = host_dist(xy, cur, j);
+            if (best < 0 || d < bd) { best = j; bd = d; }
+        }
+        vis[best] = 1;
+        len += bd;
+        cur = best;
+    }
+    return len + host_dist(xy, cur, 0);
+}
+
+// R2: limits in double, cast to float
+void host_limits(double rho, int64_t cost, double factor, float* tmin, float* tmax) {
+    const double tx = 1.0 / ((1.0 - rho) * (double)cost);
+    double tn = tx * factor;
+    if (tn > tx) tn = tx;
+    *tmax = (float)tx;
+    *tmin = (float)tn;
+}
+
+bool is_int_in(double x, int lo, int hi) { return x == std::floor(x) && x >= lo && x <= hi; }
+
+}  // namespace
+
+struct mmas_ctx {
+    mmas_config cfg{};
+    int n = 0, ld = 0, cl = 0, ldr = 0;
+    int m = 0, ant_lo = 0, m_local = 0;
+    int alpha = 1;
+    int device = 0, num_sms = 148, smem_optin = 0;
+    double factor = 0.0;
+    int64_t nn_len = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    PhiloxKey key{};
+    int rec_bytes = 0;
+
+    // device buffers
+    double2* xy = nullptr;
+    float *heur = nullptr, *tau = nullptr, *inv_w = nullptr, *cand_inv = nullptr;
+    uint16_t* cand_id = nullptr;
+    uint16_t* routes = nullptr;
+    long long* lengths = nullptr;
+    unsigned long long* best_key = nullptr;
+    unsigned long long* fallback_count = nullptr;
+    uint16_t *ib_route = nullptr, *gb_route = nullptr, *succ = nullptr, *pred = nullptr;
+    long long *gb_len = nullptr, *ib_len = nullptr;
+    int* ib_ant = nullptr;
+    float* scal = nullptr;        // tau_min, tau_max, delta
+    uint32_t* iter_dev = nullptr;
+    unsigned char* local_record = nullptr;  // world == 1 path of mmas_construct/mmas_update
+
+    // launch plan for construction
+    bool smem_table = false;
+    int slots = 1;
+    int cons_warps = 4, cons_grid = 1;
+    size_t cons_smem = 0;
+    uint32_t tb_inv = 0, tb_id = 0;
+
+    // host mirrors
+    int32_t iteration = 0;
+    int64_t launches = 0;
+
+    // profiling
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct Span { cudaEvent_t a, b; int phase; };
+    std::vector<Span> spans;
+    double acc_ms[3] = {0, 0, 0};
+    int64_t acc_iters = 0;
+};
+
+namespace {
+
+cudaEvent_t take_event(mmas_ctx* h) {
+    if (h->ev_used == h->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        h->ev_pool.push_back(e);
+    }
+    return h->ev_pool[h->ev_used++];
+}
+
+// Folds completed spans into the accumulators (synchronises the stream).
+void drain_spans(mmas_ctx* h) {
+    if (h->spans.empty()) return;
+    cudaStreamSynchronize(h->stream);
+    for (auto& s : h->spans) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, s.a, s.b);
+        h->acc_ms[s.phase] += ms;
+    }
+    h->spans.clear();
+    h->ev_used = 0;
+}
+
+struct PhaseScope {
+    mmas_ctx* h;
+    int phase;
+    cudaEvent_t a{};
+    PhaseScope(mmas_ctx* hh, int p) : h(hh), phase(p) {
+        if (h->profiling) {
+            if (h->ev_used + 2 > 4096) drain_spans(h);
+            a = take_event(h);
+            cudaEventRecord(a, h->stream);
+        }
+    }
+    ~PhaseScope() {
+        if (h->profiling) {
+            cudaEvent_t b = take_event(h);
+            cudaEventRecord(b, h->stream);
+            h->spans.push_back({a, b, phase});
+        }
+    }
+};
+
+ConstructArgs construct_args(mmas_ctx* h) {
+    ConstructArgs A{};
+    A.xy = h->xy;
+    A.inv_w = h->inv_w;
+    A.cand_id = h->cand_id;
+    A.cand_inv = h->cand_inv;
+    A.iter_dev = h->iter_dev;
+    A.key = h->key;
+    A.n = h->n;
+    A.ld = h->ld;
+    A.cl = h->cl;
+    A.ldr = h->ldr;
+    A.ant_lo = h->ant_lo;
+    A.m_local = h->m_local;
+    A.fallback_argmax = h->cfg.fallback == MMAS_FALLBACK_ARGMAX;
+    A.warps_per_block = h->cons_warps;
+    A.table_bytes_inv = h->tb_inv;
+    A.table_bytes_id = h->tb_id;
+    A.routes = h->routes;
+    A.lengths = h->lengths;
+    A.best_key = h->best_key;
+    A.fallback_count = h->fallback_count;
+    return A;
+}
+
+template <int S, bool T>
+void set_smem_attr(size_t bytes) {
+    cudaFuncSetAttribute(construct_cl_kernel<S, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int S, bool T>
+void launch_cl(mmas_ctx* h, const ConstructArgs& A) {
+    construct_cl_kernel<S, T><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+}
+
+int launch_construct(mmas_ctx* h) {
+    if (h->m_local == 0) return MMAS_OK;
+    PhaseScope ps(h, 0);
+    ConstructArgs A = construct_args(h);
+    if (h->cl == 0) {
+        construct_full_kernel<<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+    } else if (h->smem_table) {
+        if (h->slots == 1) launch_cl<1, true>(h, A);
+        else if (h->slots == 2) launch_cl<2, true>(h, A);
+        else launch_cl<4, true>(h, A);
+    } else {
+        if (h->slots == 1) launch_cl<1, false>(h, A);
+        else if (h->slots == 2) launch_cl<2, false>(h, A);
+        else launch_cl<4, false>(h, A);
+    }
+    h->launches++;
+    CU(cudaGetLastError());
+    return MMAS_OK;
+}
+
+int launch_select(mmas_ctx* h, const unsigned char* records, int count) {
+    PhaseScope ps(h, 1);
+    SelectArgs S{};
+    S.records = records;
+    S.count = count;
+    S.rec_bytes = h->rec_bytes;
+    S.local_key = h->best_key;
+    S.routes = h->routes;
+    S.ldr = h->ldr;
+    S.ant_lo = h->ant_lo;
+    S.n = h->n;
+    S.rho = h->cfg.rho;
+    S.factor = h->factor;
+    S.deposit_global = h->cfg.deposit == MMAS_DEPOSIT_GLOBAL_BEST;
+    S.ib_route = h->ib_route;
+    S.gb_route = h->gb_route;
+    S.gb_len = h->gb_len;
+    S.ib_len = h->ib_len;
+    S.ib_ant = h->ib_ant;
+    S.scal = h->scal;
+    S.succ = h->succ;
+    S.pred = h->pred;
+    select_best_kernel<<<1, 1024, 0, h->stream>>>(S);
+    h->launches++;
+    CU(cudaGetLastError());
+    return MMAS_OK;
+}
+
+int launch_update(mmas_ctx* h) {
+    PhaseScope ps(h, 2);
+    UpdateArgs U{};
+    U.tau = h->tau;
+    U.inv_w = h->inv_w;
+    U.heur = h->heur;
+    U.n = h->n;
+    U.ld = h->ld;
+    U.alpha = h->alpha;
+    U.rho_f = (float)h->cfg.rho;
+    U.scal = h->scal;
+    U.succ = h->succ;
+    U.pred = h->pred;
+    U.cand_id = h->cand_id;
+    U.cand_inv = h->cand_inv;
+    U.cl = h->cl;
+    U.iter_dev = h->iter_dev;
+    const int threads = h->n >= 1024 ? 256 : 128;
+    pheromone_update_kernel<<<h->n, threads, 0, h->stream>>>(U);
+    h->launches++;
+    CU(cudaGetLastError());
+    return MMAS_OK;
+}
+
+void free_ctx(mmas_ctx* h) {
+    if (!h) return;
+    if (h->device >= 0) cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    void* ptrs[] = {h->xy, h->heur, h->tau, h->inv_w, h->cand_inv, h->cand_id, h->routes, h->lengths,
+                    h->best_key, h->fallback_count, h->ib_route, h->gb_route, h->succ, h->pred, h->gb_len,
+                    h->ib_len, h->ib_ant, h->scal, h->iter_dev, h->local_record};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (auto e : h->ev_pool) cudaEventDestroy(e);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+template <class T>
+int dalloc(T** p, size_t count) {
+    cudaError_t e = cudaMalloc((void**)p, sizeof(T) * std::max<size_t>(count, 1));
+    if (e != cudaSuccess) return fail(MMAS_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return MMAS_OK;
+}
+
+int setup(mmas_ctx* h) {
+    const mmas_config& c = h->cfg;
+    const int n = c.n;
+    if (c.device >= 0) CU(cudaSetDevice(c.device));
+    CU(cudaGetDevice(&h->device));
+    CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
+    CU(cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+    if (c.stream) {
+        h->stream = (cudaStream_t)c.stream;
+    } else {
+        CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->own_stream = true;
+    }
+    h->n = n;
+    h->ld = round_up(n, 32);
+    h->ldr = round_up(n, 32);
+    h->cl = c.cand_len;
+    h->m = c.n_ants;
+    h->alpha = (int)c.alpha;
+    h->ant_lo = (int)((int64_t)c.rank * c.n_ants / c.world);
+    h->m_local = (int)((int64_t)(c.rank + 1) * c.n_ants / c.world) - h->ant_lo;
+    h->key.k0 = (uint32_t)c.seed;
+    h->key.k1 = (uint32_t)(c.seed >> 32);
+    h->rec_bytes = round_up(8 + 2 * n, 16);
+
+    const size_t nn = (size_t)n * h->ld;
+    int st;
+    if ((st = dalloc(&h->xy, n)) || (st = dalloc(&h->heur, nn)) || (st = dalloc(&h->tau, nn)) ||
+        (st = dalloc(&h->inv_w, nn)) || (st = dalloc(&h->cand_inv, (size_t)n * h->cl + 64)) ||
+        (st = dalloc(&h->cand_id, (size_t)n * h->cl + 64)) ||
+        (st = dalloc(&h->routes, (size_t)std::max(h->m_local, 1) * h->ldr)) ||
+        (st = dalloc(&h->lengths, (size_t)std::max(h->m_local, 1))) || (st = dalloc(&h->best_key, 1)) ||
+        (st = dalloc(&h->fallback_count, 1)) || (st = dalloc(&h->ib_route, n)) || (st = dalloc(&h->gb_route, n)) ||
+        (st = dalloc(&h->succ, n)) || (st = dalloc(&h->pred, n)) || (st = dalloc(&h->gb_len, 1)) ||
+        (st = dalloc(&h->ib_len, 1)) || (st = dalloc(&h->ib_ant, 1)) || (st = dalloc(&h->scal, 4)) ||
+        (st = dalloc(&h->iter_dev, 1)) || (st = dalloc(&h->local_record, (size_t)h->rec_bytes)))
+        return st;
+
+    CU(cudaMemcpyAsync(h->xy, c.coords, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemsetAsync(h->routes, 0, sizeof(uint16_t) * (size_t)std::max(h->m_local, 1) * h->ldr, h->stream));
+    CU(cudaMemsetAsync(h->lengths, 0, sizeof(long long) * (size_t)std::max(h->m_local, 1), h->stream));
+    CU(cudaMemsetAsync(h->best_key, 0xFF, sizeof(unsigned long long), h->stream));
+    CU(cudaMemsetAsync(h->fallback_count, 0, sizeof(unsigned long long), h->stream));
+    CU(cudaMemsetAsync(h->gb_len, 0xFF, sizeof(long long), h->stream));   // -1: empty
+    CU(cudaMemsetAsync(h->ib_len, 0xFF, sizeof(long long), h->stream));
+    CU(cudaMemsetAsync(h->iter_dev, 0, sizeof(uint32_t), h->stream));
+    CU(cudaMemsetAsync(h->succ, 0, sizeof(uint16_t) * n, h->stream));
+    CU(cudaMemsetAsync(h->pred, 0, sizeof(uint16_t) * n, h->stream));
+
+    // eta^beta (R11, R18)
+    if (is_int_in(c.beta, 0, 8)) {
+        dim3 g((h->ld + 255) / 256, n);
+        heur_kernel<<<g, 256, 0, h->stream>>>(h->xy, n, h->ld, (int)c.beta, h->heur);
+        h->launches++;
+        CU(cudaGetLastError());
+    } else {
+        std::vector<float> hh(nn, 1.0f);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) {
+                const int32_t d = host_dist(c.coords, i, j);
+                hh[(size_t)i * h->ld + j] = (float)std::pow((double)(d > 1 ? d : 1), -c.beta);
+            }
+        CU(cudaMemcpyAsync(h->heur, hh.data(), sizeof(float) * nn, cudaMemcpyHostToDevice, h->stream));
+        CU(cudaStreamSynchronize(h->stream));
+    }
+
+    // candidate lists (host, parallel over rows)
+    if (h->cl > 0) {
+        std::vector<uint16_t> cand;
+        candidate_lists(c.coords, n, h->cl, cand);
+        CU(cudaMemcpyAsync(h->cand_id, cand.data(), sizeof(uint16_t) * cand.size(), cudaMemcpyHostToDevice,
+                           h->stream));
+        CU(cudaStreamSynchronize(h->stream));
+    }
+
+    // initial limits from the NN tour (Alg. 1); F from libm pow (R2)
+    h->nn_len = nn_tour_length(c.coords, n);
+    const double pn = std::pow(c.p_best, 1.0 / (double)n);
+    h->factor = (1.0 - pn) / (((double)n / 2.0 - 1.0) * pn);
+    float lim[4] = {0, 0, 0, 0};
+    host_limits(c.rho, h->nn_len, h->factor, &lim[0], &lim[1]);
+    CU(cudaMemcpyAsync(h->scal, lim, sizeof(lim), cudaMemcpyHostToDevice, h->stream));
+    {
+        dim3 g((h->ld + 255) / 256, n);
+        init_trails_kernel<<<g, 256, 0, h->stream>>>(h->tau, h->inv_w, h->heur, n, h->ld, h->alpha, h->scal);
+        h->launches++;
+        CU(cudaGetLastError());
+    }
+    if (h->cl > 0) {
+        gather_cand_kernel<<<std::max(1, std::min(4096, (n * h->cl + 255) / 256)), 256, 0, h->stream>>>(
+            h->inv_w, n, h->ld, h->cand_id, h->cand_inv, h->cl);
+        h->launches++;
+        CU(cudaGetLastError());
+    }
+
+    // ---- construction launch plan ----
+    const int nwords = round_up((n + 31) / 32, 4);
+    const size_t tabu_bytes = (size_t)nwords * 4;
+    h->slots = h->cl <= 32 ? 1 : (h->cl <= 64 ? 2 : 4);
+    if (h->cl > 0) {
+        h->tb_inv = (uint32_t)round_up(n * h->cl * 4, 16);
+        h->tb_id = (uint32_t)round_up(n * h->cl * 2, 16);
+        int w = std::max(1, std::min(16, (h->m_local + h->num_sms - 1) / std::max(h->num_sms, 1)));
+        size_t need = 128 + (size_t)h->tb_inv + h->tb_id + (size_t)w * tabu_bytes;
+        h->smem_table = need <= (size_t)h->smem_optin;
+        if (h->smem_table) {
+            h->cons_warps = w;
+            h->cons_grid = std::max(1, (h->m_local + w - 1) / w);
+            h->cons_smem = need;
+        } else {
+            h->cons_warps = 4;
+            h->cons_grid = std::max(1, (h->m_local + 3) / 4);
+            h->cons_smem = 128 + 4 * tabu_bytes;
+        }
+    } else {
+        h->cons_warps = 4;
+        h->cons_grid = std::max(1, (h->m_local + 3) / 4);
+        h->cons_smem = 128 + 4 * tabu_bytes;
+    }
+    if (h->cons_smem > (size_t)h->smem_optin)
+        return fail(MMAS_EINVAL, "n too large for the shared-memory tabu of one block");
+    if (h->cl > 0) {
+        if (h->slots == 1) { set_smem_attr<1, true>(h->cons_smem); set_smem_attr<1, false>(h->cons_smem); }
+        else if (h->slots == 2) { set_smem_attr<2, true>(h->cons_smem); set_smem_attr<2, false>(h->cons_smem); }
+        else { set_smem_attr<4, true>(h->cons_smem); set_smem_attr<4, false>(h->cons_smem); }
+    } else {
+        cudaFuncSetAttribute(construct_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->cons_smem);
+    }
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(h->stream));
+    return MMAS_OK;
+}
+
+int validate(const mmas_config* c) {
+    if (!c) return fail(MMAS_EINVAL, "config is NULL");
+    if (!c->coords) return fail(MMAS_EINVAL, "coords is NULL");
+    if (c->n < 3 || c->n >= 65536) return fail(MMAS_EINVAL, "n must satisfy 3 <= n < 65536");
+    if (c->n_ants < 1 || c->n_ants >= (1 << 24)) return fail(MMAS_EINVAL, "n_ants must satisfy 1 <= m < 2^24");
+    if (c->cand_len < 0 || c->cand_len > c->n - 1 || c->cand_len > 128)
+        return fail(MMAS_EINVAL, "cand_len must satisfy 0 <= cl <= min(n-1, 128)");
+    if (!(c->rho > 0.0 && c->rho < 1.0)) return fail(MMAS_EINVAL, "rho must satisfy 0 < rho < 1");
+    if (!is_int_in(c->alpha, 0, 8)) return fail(MMAS_EINVAL, "alpha must be an integer in [0, 8]");
+    if (!(c->beta >= 0.0) || !std::isfinite(c->beta)) return fail(MMAS_EINVAL, "beta must be finite and >= 0");
+    if (!(c->p_best > 0.0 && c->p_best < 1.0)) return fail(MMAS_EINVAL, "p_best must satisfy 0 < p < 1");
+    if (c->deposit != MMAS_DEPOSIT_ITERATION_BEST && c->deposit != MMAS_DEPOSIT_GLOBAL_BEST)
+        return fail(MMAS_EINVAL, "deposit must be MMAS_DEPOSIT_*");
+    if (c->fallback != MMAS_FALLBACK_WRS && c->fallback != MMAS_FALLBACK_ARGMAX)
+        return fail(MMAS_EINVAL, "fallback must be MMAS_FALLBACK_*");
+    if (c->local_search != 0) return fail(MMAS_EINVAL, "local_search (2-opt) is not available in this version");
+    if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(MMAS_EINVAL, "need 0 <= rank < world");
+    double lo_x = INFINITY, hi_x = -INFINITY, lo_y = INFINITY, hi_y = -INFINITY;
+    for (int i = 0; i < c->n; ++i) {
+        const double x = c->coords[2 * i], y = c->coords[2 * i + 1];
+        if (!std::isfinite(x) || !std::isfinite(y)) return fail(MMAS_EINVAL, "coords must be finite");
+        lo_x = std::min(lo_x, x); hi_x = std::max(hi_x, x);
+        lo_y = std::min(lo_y, y); hi_y = std::max(hi_y, y);
+    }
+    // tour length must fit the 40-bit field of the (len << 24 | ant) key
+    const double diag = std::sqrt((hi_x - lo_x) * (hi_x - lo_x) + (hi_y - lo_y) * (hi_y - lo_y)) + 1.0;
+    if (diag * c->n >= 1099511627776.0 || diag >= 2147483647.0)
+        return fail(MMAS_EINVAL, "coordinate range too large: tour lengths must stay below 2^40");
+    return MMAS_OK;
+}
+
+int check(const mmas_ctx* h) {
+    if (!h) return fail(MMAS_EINVAL, "context is NULL");
+    return MMAS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mmas_last_error(void) { return g_last_error.c_str(); }
+
+void mmas_config_init(mmas_config* cfg) {
+    if (!cfg) return;
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->alpha = 1.0;
+    cfg->beta = 2.0;
+    cfg->rho = 0.5;
+    cfg->p_best = 0.01;
+    cfg->deposit = MMAS_DEPOSIT_ITERATION_BEST;
+    cfg->fallback = MMAS_FALLBACK_WRS;
+    cfg->device = -1;
+    cfg->rank = 0;
+    cfg->world = 1;
+}
+
+int mmas_create_ex(const mmas_config* cfg, mmas_ctx** out) {
+    g_last_error.clear();
+    if (!out) return fail(MMAS_EINVAL, "out is NULL");
+    *out = nullptr;
+    int st = validate(cfg);
+    if (st) return st;
+    mmas_ctx* h = new mmas_ctx();
+    h->cfg = *cfg;
+    h->device = -1;
+    st = setup(h);
+    if (st) {
+        std::string msg = g_last_error;
+        free_ctx(h);
+        g_last_error = msg;
+        return st;
+    }
+    h->cfg.coords = nullptr;  // not retained
+    *out = h;
+    return MMAS_OK;
+}
+
+mmas_ctx* mmas_create(const double* coords, int32_t n, double alpha, double beta, double rho, int32_t n_ants,
+                      int32_t cand_len, uint64_t seed) {
+    mmas_config c;
+    mmas_config_init(&c);
+    c.coords = coords;
+    c.n = n;
+    c.alpha = alpha;
+    c.beta = beta;
+    c.rho = rho;
+    c.n_ants = n_ants;
+    c.cand_len = cand_len;
+    c.seed = seed;
+    mmas_ctx* h = nullptr;
+    return mmas_create_ex(&c, &h) == MMAS_OK ? h : nullptr;
+}
+
+int64_t mmas_record_bytes(const mmas_ctx* h) { return h ? h->rec_bytes : fail(MMAS_EINVAL, "context is NULL"); }
+
+int mmas_construct(mmas_ctx* h, void* record_dev) {
+    int st = check(h);
+    if (st) return st;
+    if (!record_dev) return fail(MMAS_EINVAL, "record_dev is NULL");
+    CU(cudaSetDevice(h->device));
+    if ((st = launch_construct(h))) return st;
+    if (h->m_local > 0) {
+        publish_kernel<<<1, 256, 0, h->stream>>>(h->best_key, h->routes, h->ldr, h->ant_lo, h->n,
+                                                 (unsigned char*)record_dev);
+        h->launches++;
+    } else {
+        // empty shard: a record that never wins
+        CU(cudaMemsetAsync(record_dev, 0xFF, 8, h->stream));
+    }
+    CU(cudaGetLastError());
+    return MMAS_OK;
+}
+
+int mmas_update(mmas_ctx* h, const void* records_dev, int32_t count) {
+    int st = check(h);
+    if (st) return st;
+    if (!records_dev || count < 1) return fail(MMAS_EINVAL, "need records_dev != NULL and count >= 1");
+    CU(cudaSetDevice(h->device));
+    if ((st = launch_select(h, (const unsigned char*)records_dev, count))) return st;
+    if ((st = launch_update(h))) return st;
+    h->iteration++;
+    if (h->profiling) h->acc_iters++;
+    return MMAS_OK;
+}
+
+int mmas_iterate(mmas_ctx* h, int32_t iters) {
+    int st = check(h);
+    if (st) return st;
+    if (iters < 1) return fail(MMAS_EINVAL, "iters must be >= 1");
+    if (h->cfg.world != 1) return fail(MMAS_ESTATE, "mmas_iterate needs world == 1; use mmas_construct/mmas_update");
+    CU(cudaSetDevice(h->device));
+    for (int k = 0; k < iters; ++k) {
+        if ((st = launch_construct(h))) return st;
+        if ((st = launch_select(h, nullptr, 1))) return st;
+        if ((st = launch_update(h))) return st;
+        h->iteration++;
+        if (h->profiling) h->acc_iters++;
+    }
+    return MMAS_OK;
+}
+
+int64_t mmas_best_tour(mmas_ctx* h, int32_t* tour_out) {
+    int st = check(h);
+    if (st) return st;
+    if (!tour_out) return fail(MMAS_EINVAL, "tour_out is NULL");
+    CU(cudaSetDevice(h->device));
+    long long len = -1;
+    std::vector<uint16_t> r((size_t)h->n);
+    CU(cudaMemcpyAsync(&len, h->gb_len, sizeof(len), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(r.data(), h->gb_route, sizeof(uint16_t) * h->n, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    if (len < 0) return fail(MMAS_ESTATE, "no global best yet (run at least one iteration)");
+    for (int i = 0; i < h->n; ++i) tour_out[i] = r[i];
+    return len;
+}
+
+void mmas_destroy(mmas_ctx* h) { free_ctx(h); }
+
+int32_t mmas_n(const mmas_ctx* h) { return h ? h->n : 0; }
+int32_t mmas_iteration(const mmas_ctx* h) { return h ? h->iteration : 0; }
+
+int mmas_get_tours(mmas_ctx* h, int32_t* out, int32_t* first_ant, int32_t* count) {
+    int st = check(h);
+    if (st) return st;
+    if (first_ant) *first_ant = h->ant_lo;
+    if (count) *count = h->m_local;
+    if (!out) return MMAS_OK;
+    CU(cudaSetDevice(h->device));
+    std::vector<uint16_t> r((size_t)std::max(h->m_local, 1) * h->ldr);
+    CU(cudaMemcpyAsync(r.data(), h->routes, sizeof(uint16_t) * r.size(), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    for (int a = 0; a < h->m_local; ++a)
+        for (int k = 0; k < h->n; ++k) out[(size_t)a * h->n + k] = r[(size_t)a * h->ldr + k];
+    return MMAS_OK;
+}
+
+int mmas_get_lengths(mmas_ctx* h, int64_t* out) {
+    int st = check(h);
+    if (st) return st;
+    if (!out) return fail(MMAS_EINVAL, "out is NULL");
+    CU(cudaSetDevice(h->device));
+    CU(cudaMemcpyAsync(out, h->lengths, sizeof(int64_t) * h->m_local, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return MMAS_OK;
+}
+
+static int get_matrix(mmas_ctx* h, const float* src, float* out) {
+    int st = check(h);
+    if (st) return st;
+    if (!out) return fail(MMAS_EINVAL, "out is NULL");
+    CU(cudaSetDevice(h->device));
+    CU(cudaMemcpy2DAsync(out, sizeof(float) * h->n, src, sizeof(float) * h->ld, sizeof(float) * h->n, h->n,
+                         cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return MMAS_OK;
+}
+
+int mmas_get_pheromone(mmas_ctx* h, float* out) { return get_matrix(h, h ? h->tau : nullptr, out); }
+int mmas_get_inv_w(mmas_ctx* h, float* out) { return get_matrix(h, h ? h->inv_w : nullptr, out); }
+int mmas_get_heuristic(mmas_ctx* h, float* out) { return get_matrix(h, h ? h->heur : nullptr, out); }
+
+int mmas_get_candidates(mmas_ctx* h, int32_t* out) {
+    int st = check(h);
+    if (st) return st;
+    if (!out) return fail(MMAS_EINVAL, "out is NULL");
+    if (h->cl == 0) return MMAS_OK;
+    CU(cudaSetDevice(h->device));
+    std::vector<uint16_t> r((size_t)h->n * h->cl);
+    CU(cudaMemcpyAsync(r.data(), h->cand_id, sizeof(uint16_t) * r.size(), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    for (size_t e = 0; e < r.size(); ++e) out[e] = r[e];
+    return MMAS_OK;
+}
+
+int mmas_get_limits(mmas_ctx* h, float* tau_min, float* tau_max) {
+    int st = check(h);
+    if (st) return st;
+    CU(cudaSetDevice(h->device));
+    float s[4];
+    CU(cudaMemcpyAsync(s, h->scal, sizeof(s), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    if (tau_min) *tau_min = s[0];
+    if (tau_max) *tau_max = s[1];
+    return MMAS_OK;
+}
+
+int mmas_get_stats(mmas_ctx* h, mmas_stats* out) {
+    int st = check(h);
+    if (st) return st;
+    if (!out) return fail(MMAS_EINVAL, "out is NULL");
+    CU(cudaSetDevice(h->device));
+    unsigned long long fb = 0;
+    CU(cudaMemcpyAsync(&fb, h->fallback_count, sizeof(fb), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    out->iterations = h->iteration;
+    out->fallback_steps = (int64_t)fb;
+    out->ant_steps = (int64_t)h->iteration * h->m_local * (h->n - 1);
+    out->ants_local = h->m_local;
+    out->first_ant = h->ant_lo;
+    return MMAS_OK;
+}
+
+int mmas_profile(mmas_ctx* h, int32_t enable) {
+    int st = check(h);
+    if (st) return st;
+    drain_spans(h);
+    h->profiling = enable != 0;
+    h->acc_ms[0] = h->acc_ms[1] = h->acc_ms[2] = 0.0;
+    h->acc_iters = 0;
+    return MMAS_OK;
+}
+
+int mmas_get_phase_times(mmas_ctx* h, mmas_phase_times* out) {
+    int st = check(h);
+    if (st) return st;
+    if (!out) return fail(MMAS_EINVAL, "out is NULL");
+    CU(cudaSetDevice(h->device));
+    drain_spans(h);
+    out->construct_ms = h->acc_ms[0];
+    out->select_ms = h->acc_ms[1];
+    out->update_ms = h->acc_ms[2];
+    out->iterations = h->acc_iters;
+    return MMAS_OK;
+}
+
+int mmas_debug_philox(const uint32_t* ctr_key, int64_t count, uint32_t* out_words, float* out_log2) {
+    if (count < 0 || (count > 0 && (!ctr_key || !out_words || !out_log2))) return fail(MMAS_EINVAL, "bad arguments");
+    if (count == 0) return MMAS_OK;
+    uint32_t* d_ck = nullptr;
+    uint32_t* d_w = nullptr;
+    float* d_l = nullptr;
+    int st;
+    if ((st = dalloc(&d_ck, 6 * (size_t)count)) || (st = dalloc(&d_w, 4 * (size_t)count)) ||
+        (st = dalloc(&d_l, 4 * (size_t)count))) {
+        cudaFree(d_ck); cudaFree(d_w); cudaFree(d_l);
+        return st;
+    }
+    cudaMemcpy(d_ck, ctr_key, sizeof(uint32_t) * 6 * count, cudaMemcpyHostToDevice);
+    debug_philox_kernel<<<(unsigned)std::min<int64_t>(4096, (count + 255) / 256), 256>>>(d_ck, count, d_w, d_l);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(out_words, d_w, sizeof(uint32_t) * 4 * count, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(out_log2, d_l, sizeof(float) * 4 * count, cudaMemcpyDeviceToHost);
+    cudaFree(d_ck); cudaFree(d_w); cudaFree(d_l);
+    if (e != cudaSuccess) return fail(MMAS_ECUDA, cudaGetErrorString(e));
+    return MMAS_OK;
+}
+
+int mmas_debug_log2(const float* u, int64_t count, float* out) {
+    if (count < 0 || (count > 0 && (!u || !out))) return fail(MMAS_EINVAL, "bad arguments");
+    if (count == 0) return MMAS_OK;
+    float *d_u = nullptr, *d_o = nullptr;
+    int st;
+    if ((st = dalloc(&d_u, (size_t)count)) || (st = dalloc(&d_o, (size_t)count))) {
+        cudaFree(d_u); cudaFree(d_o);
+        return st;
+    }
+    cudaMemcpy(d_u, u, sizeof(float) * count, cudaMemcpyHostToDevice);
+    debug_log2_kernel<<<(unsigned)std::min<int64_t>(8192, (count + 255) / 256), 256>>>(d_u, count, d_o);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(out, d_o, sizeof(float) * count, cudaMemcpyDeviceToHost);
+    cudaFree(d_u); cudaFree(d_o);
+    if (e != cudaSuccess) return fail(MMAS_ECUDA, cudaGetErrorString(e));
+    return MMAS_OK;
+}
+
+int64_t mmas_kernel_launches(const mmas_ctx* h) { return h ? h->launches : 0; }
+
+void* mmas_stream(const mmas_ctx* h) { return h ? (void*)h->stream : nullptr; }
+
+int mmas_sync(mmas_ctx* h) {
+    int st = check(h);
+    if (st) return st;
+    CU(cudaSetDevice(h->device));
+    CU(cudaStreamSynchronize(h->stream));
+    return MMAS_OK;
+}
+
+}  // extern "C"

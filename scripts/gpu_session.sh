@@ -1,0 +1,54 @@
+#!/bin/bash
+# One GPU session: device facts, parity tests, smoke, bench, ncu launch list + one full capture.
+# Usage (from the repo root, under gpurun): bash scripts/gpu_session.sh [tag] [what...]
+TAG=${1:-r01}
+shift || true
+WHAT=${@:-"facts tests smoke bench ncu"}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+export PYTHONUNBUFFERED=1
+has() { [[ " $WHAT " == *" $1 "* ]]; }
+if has facts; then
+  nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+  nvidia-smi -q -d CLOCK >> $OUT/nvidia-smi.txt 2>&1
+  nproc > $OUT/nproc.txt; lscpu | grep -E "Model name|^CPU\(s\)" >> $OUT/nproc.txt
+  python -c "import torch; p=torch.cuda.get_device_properties(0); print(p); print('sms',p.multi_processor_count,'l2',p.L2_cache_size)" > $OUT/device.txt 2>&1
+fi
+if has build; then
+  timeout 600 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1; echo "build rc=$?" >> $OUT/build.log
+fi
+if has tests; then
+  timeout 1500 python -m pytest tests -x -q -m gpu --durations=15 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+  tail -5 $OUT/pytest_gpu.log
+fi
+if has alltests; then
+  timeout 1800 python -m pytest tests -q -m gpu --durations=15 > $OUT/pytest_gpu_all.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu_all.log
+  tail -5 $OUT/pytest_gpu_all.log
+fi
+if has smoke; then
+  timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+  tail -2 $OUT/smoke.log
+fi
+if has bench; then
+  timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
+  cat $OUT/bench.json | head -c 3000; echo
+fi
+for cfg in C1 C3 C4; do
+  if has bench$cfg; then
+    timeout 900 python bench.py --config $cfg --steps 50 --no-cpu-baseline > $OUT/bench_$cfg.json 2> $OUT/bench_$cfg.err
+    head -c 1500 $OUT/bench_$cfg.json; echo
+  fi
+done
+if has reference; then
+  timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
+  cat $OUT/bench_reference.json
+fi
+if has ncu; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
+     python bench.py --steps 30 --warmup 3 --no-cpu-baseline > $OUT/ncu_launches_bench.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:construct -s 3 -c 1 -o $OUT/prof_construct \
+     python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_construct.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pheromone_update -s 3 -c 1 -o $OUT/prof_update \
+     python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_update.log 2>&1
+  ls -la $OUT
+fi

@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
+by element on the same seeded inputs.  Tours, lengths, candidate lists and
+limits must be bit-exact; pheromone / inv_w are compared bit-exactly too (the
+north_star tolerance is 1e-6 relative; the contract makes them exact)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2003_11902_b200 import mmas
+from paper_2003_11902_b200.instances import CONFIGS, make_coords
+
+pytestmark = pytest.mark.gpu
+RTOL_TAU = 1e-6   # north_star: "to 1e-6 relative for pheromone values"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    assert torch.cuda.is_available(), "-m gpu tests need a CUDA device"
+    mmas.lib()
+
+
+def assert_matrix(g, o, what):
+    if not np.array_equal(g, o):
+        diff = np.abs(g.astype(np.float64) - o.astype(np.float64)) / np.maximum(np.abs(o.astype(np.float64)), 1e-300)
+        i = np.unravel_index(np.argmax(diff), diff.shape)
+        assert diff.max() <= RTOL_TAU, f"{what}: max rel diff {diff.max()} at {i}: gpu {g[i]} oracle {o[i]}"
+        pytest.fail(f"{what}: not bit-exact (max rel diff {diff.max()} within tolerance, but the contract is exact)")
+
+
+def compare_setup(g, o):
+    assert_matrix(g.heur(), o.heur(), "heuristic")
+    assert_matrix(g.inv_w(), o.inv_w(), "inv_w (setup)")
+    assert_matrix(g.tau(), o.tau(), "tau (setup)")
+    assert g.limits() == o.limits()
+    if o.cl > 0:
+        assert np.array_equal(g.cand(), o.cand())
+
+
+def compare_iteration(g, o, it):
+    gt, ot = g.tours(), o.tours()
+    if not np.array_equal(gt, ot):
+        bad = np.where((gt != ot).any(axis=1))[0]
+        a = bad[0]
+        k = int(np.argmax(gt[a] != ot[a]))
+        pytest.fail(f"iteration {it}: {len(bad)} ants differ; ant {a} first at step {k}: gpu {gt[a][k]} oracle {ot[a][k]}")
+    assert np.array_equal(g.lengths(), o.lengths()), f"iteration {it}: lengths"
+    assert g.limits() == o.limits(), f"iteration {it}: limits"
+    gb, gl = g.best_tour()
+    ob, ol = o.best_tour()
+    assert gl == ol and np.array_equal(gb, ob), f"iteration {it}: global best"
+    assert_matrix(g.tau(), o.tau(), f"tau after iteration {it}")
+    assert_matrix(g.inv_w(), o.inv_w(), f"inv_w after iteration {it}")
+
+
+def lockstep(coords, m, cl, iters, seed=42, **kw):
+    g = mmas.Colony(coords, m, cl, seed=seed, **kw)
+    o = oracle.Colony(coords, m, cl, seed=seed, **kw)
+    compare_setup(g, o)
+    for it in range(iters):
+        g.iterate(1)
+        o.iterate(1)
+        compare_iteration(g, o, it)
+    return g, o
+
+
+# ---- primitives -------------------------------------------------------------------
+def test_device_philox_matches_kat_and_oracle():
+    kat = [(0, 0, 0, 0, 0, 0), (0xFFFFFFFF,) * 6, (0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344, 0xA4093822, 0x299F31D0)]
+    expect = [[0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8], [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD],
+              [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]]
+    w, _ = mmas.debug_philox(np.array(kat, dtype=np.uint32))
+    assert w.tolist() == expect
+    rng = np.random.default_rng(3)
+    ck = rng.integers(0, 2 ** 32, size=(4000, 6), dtype=np.uint64).astype(np.uint32)
+    w, logs = mmas.debug_philox(ck)
+    for i in range(0, 4000, 37):
+        ow = oracle.philox(ck[i, :4], ck[i, 4:])
+        assert list(w[i]) == list(ow)
+        for j in range(4):
+            assert logs[i, j] == np.float32(oracle.det_log2(oracle.uniform(int(ow[j]))))
+
+
+def test_device_det_log2_exhaustive_bitwise():
+    j = np.arange(1 << 23, dtype=np.float64)
+    u = ((2.0 * j + 1.0) / 2.0 ** 24).astype(np.float32)
+    assert np.array_equal(mmas.debug_log2(u).view(np.uint32), oracle.det_log2_many(u).view(np.uint32))
+
+
+# ---- whole iterations ---------------------------------------------------------------
+def test_c1_all_50_iterations_bit_exact():
+    w = CONFIGS["C1"]
+    lockstep(w.coords(), w.n_ants, w.cand_len, w.iterations, seed=w.mmas_seed, rho=w.rho)
+
+
+CASES = [
+    # (n, m, cl, iterations, kwargs)   -- ragged sizes, edge cases, every kernel variant
+    (3, 1, 0, 3, {}),
+    (3, 4, 2, 3, {}),
+    (4, 3, 3, 3, {}),                          # n <= 5: tau_min clamped to tau_max
+    (5, 7, 1, 4, {}),
+    (33, 33, 0, 3, {}),                        # full row, ragged tail of a 128-city chunk
+    (67, 40, 5, 4, {}),
+    (130, 70, 16, 4, {}),
+    (130, 70, 32, 4, {}),
+    (129, 31, 1, 3, {}),                       # cl = 1: fallback at most steps
+    (200, 37, 40, 3, {}),                      # 2 slots per lane
+    (150, 20, 100, 3, {}),                     # 4 slots per lane
+    (97, 50, 8, 4, {"fallback_argmax": True}),
+    (97, 50, 8, 4, {"deposit_global": True}),
+    (64, 20, 10, 3, {"alpha": 2.0, "beta": 3.0}),
+    (64, 20, 10, 3, {"alpha": 0.0, "beta": 1.0}),
+    (80, 20, 12, 3, {"beta": 2.5}),            # non-integer beta: host libm pow (R18)
+    (90, 25, 12, 3, {"rho": 0.9, "p_best": 0.05}),
+    (1025, 12, 32, 2, {}),                     # n > 1024: 33 tabu words
+    (1500, 20, 32, 2, {}),                     # candidate table > shared memory: L2 variant
+    (300, 300, 0, 2, {}),                      # full row, many ants
+]
+
+
+@pytest.mark.parametrize("n,m,cl,iters,kw", CASES, ids=[f"n{c[0]}-m{c[1]}-cl{c[2]}-{'-'.join(c[4])}" for c in CASES])
+def test_small_cases_bit_exact(n, m, cl, iters, kw):
+    lockstep(make_coords("uniform", n, 1000 + n), m, cl, iters, seed=7 + n, **kw)
+
+
+def test_clustered_instance_with_fallbacks():
+    c = make_coords("fl3795", 600, 5)
+    g, o = lockstep(c, 60, 8, 3, seed=9)
+    assert g.stats()["fallback_steps"] > 0
+
+
+def test_fallback_counter_matches_oracle():
+    c = make_coords("d198", 198, 198)
+    g = mmas.Colony(c, 120, 4, seed=3)
+    o = oracle.Colony(c, 120, 4, seed=3)
+    tot = 0
+    for _ in range(3):
+        g.iterate(1)
+        o.iterate(1)
+        tot += int(o.fallbacks().sum())
+    assert tot > 0 and g.stats()["fallback_steps"] == tot
+
+
+def test_c2_full_size_iterations_bit_exact():
+    """pr1002-shaped, 1002 ants, cl 32 -- the bench workload, in its launch configuration."""
+    w = CONFIGS["C2"]
+    lockstep(w.coords(), w.n_ants, w.cand_len, 3, seed=w.mmas_seed, rho=w.rho)
+
+
+@pytest.mark.parametrize("cfg,samples", [("C3", 10), ("C4", 4)])
+def test_full_size_sampled_ants(cfg, samples):
+    """C3 (clustered, cl + fallback) and C4 (full row) at full size: iteration 0
+    routes of sampled ants (the oracle computes them one by one), plus properties
+    of every route and of the update that hold at any size."""
+    w = CONFIGS[cfg]
+    c = w.coords()
+    g = mmas.Colony(c, w.n_ants, w.cand_len, seed=w.mmas_seed, rho=w.rho)
+    o = oracle.Colony(c, w.n_ants, w.cand_len, seed=w.mmas_seed, rho=w.rho, nthreads=8)
+    if w.cand_len:
+        assert np.array_equal(g.cand(), o.cand())
+    assert g.limits() == o.limits()
+    g.iterate(1)
+    T, L = g.tours(), g.lengths()
+    rng = np.random.default_rng(0)
+    picks = sorted(set([0, w.n_ants - 1] + list(rng.integers(0, w.n_ants, size=samples))))
+    for a in picks:
+        r, l, _ = o.construct_ant(int(a))
+        assert np.array_equal(T[a], r), f"ant {a}"
+        assert L[a] == l
+    assert np.all(np.sort(T, axis=1) == np.arange(w.n))        # every route a permutation
+    gb, gl = g.best_tour()
+    assert gl == L.min() and oracle.tour_length(c, gb) == gl
+    tmin, tmax = g.limits()
+    assert tmax == np.float32(1.0 / ((1.0 - w.rho) * gl))
+    tau = g.tau()
+    assert tau.min() >= tmin and tau.max() <= tmax
+
+
+# ---- identities of the contract -----------------------------------------------------
+def test_resume_identity():
+    """R20: iterate(2); iterate(3) == iterate(5)."""
+    c = make_coords("uniform", 150, 4)
+    a = mmas.Colony(c, 40, 16, seed=5)
+    b = mmas.Colony(c, 40, 16, seed=5)
+    a.iterate(2)
+    a.iterate(3)
+    b.iterate(5)
+    assert np.array_equal(a.tours(), b.tours()) and np.array_equal(a.tau(), b.tau())
+    assert a.iteration == b.iteration == 5
+
+
+def test_split_calls_equal_iterate():
+    import torch
+    c = make_coords("uniform", 120, 8)
+    a = mmas.Colony(c, 30, 16, seed=2)
+    s = torch.cuda.current_stream().cuda_stream
+    b = mmas.Colony(c, 30, 16, seed=2, stream=s)
+    rec = torch.zeros(b.record_bytes, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        a.iterate(1)
+        b.construct(rec.data_ptr())
+        b.update(rec.data_ptr(), 1)
+    assert np.array_equal(a.tours(), b.tours()) and np.array_equal(a.tau(), b.tau())
+    assert a.best_tour()[1] == b.best_tour()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_sharded_colony_identical_to_single(world):
+    """R21: ants sharded over `world` contexts (one GPU here; one per GPU in
+    production) with their records gathered give bit-identical tours and trails."""
+    import torch
+    c = make_coords("uniform", 140, 12)
+    m, cl = 43, 16
+    s = torch.cuda.current_stream().cuda_stream
+    ref = mmas.Colony(c, m, cl, seed=4)
+    shards = [mmas.Colony(c, m, cl, seed=4, stream=s, rank=r, world=world) for r in range(world)]
+    rb = shards[0].record_bytes
+    recs = torch.zeros(world * rb, dtype=torch.uint8, device="cuda")
+    for _ in range(4):
+        ref.iterate(1)
+        for r, sh in enumerate(shards):
+            sh.construct(recs.data_ptr() + r * rb)
+        for sh in shards:
+            sh.update(recs.data_ptr(), world)
+        T = np.concatenate([sh.tours() for sh in shards])
+        assert np.array_equal(T, ref.tours())
+        for sh in shards:
+            assert np.array_equal(sh.tau(), ref.tau())
+            assert sh.best_tour()[1] == ref.best_tour()[1]
+
+
+def test_best_tour_before_first_iteration_is_estate():
+    g = mmas.Colony(make_coords("uniform", 20, 1), 5, 4)
+    assert g.best_tour() == (None, None)
+    with pytest.raises(mmas.MMASError):
+        g.iterate(0)
+
+
+def test_profiling_accumulates_phase_times():
+    w = CONFIGS["C1"]
+    g = mmas.Colony(w.coords(), w.n_ants, w.cand_len)
+    g.profile(True)
+    n0 = g.kernel_launches
+    g.iterate(5)
+    t = g.phase_times()
+    assert t["iterations"] == 5 and t["construct_ms"] > 0 and t["update_ms"] > 0
+    assert g.kernel_launches - n0 == 15
