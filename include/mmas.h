@@ -58,9 +58,12 @@ typedef struct mmas_config {
     int32_t fallback;      /* MMAS_FALLBACK_*; default WRS over all unvisited */
     int32_t local_search;  /* 2-opt (row a8); must be 0 in this version */
     int32_t device;        /* CUDA device ordinal; -1 = current device */
-    void *stream;          /* cudaStream_t to run on; NULL = a stream owned by the context */
+    void *stream;          /* cudaStream_t to run on (see use_caller_stream) */
     int32_t rank, world;   /* ant shard: this context builds global ants [floor(rank*m/world),
                               floor((rank+1)*m/world)) (R21); default 0, 1 */
+    int32_t use_caller_stream; /* 1: run on `stream` even when it is NULL (the legacy default
+                              stream, e.g. torch's default stream); 0 (default): run on `stream`
+                              if non-NULL, else on a non-blocking stream owned by the context */
 } mmas_config;
 
 /* Per-context counters (cumulative since create). */

@@ -327,7 +327,7 @@ int setup(mmas_ctx* h) {
     CU(cudaGetDevice(&h->device));
     CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
     CU(cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-    if (c.stream) {
+    if (c.stream || c.use_caller_stream) {
         h->stream = (cudaStream_t)c.stream;
     } else {
         CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));

@@ -42,7 +42,7 @@ class Config(ctypes.Structure):
         ("n_ants", ctypes.c_int32), ("cand_len", ctypes.c_int32), ("seed", ctypes.c_uint64),
         ("p_best", ctypes.c_double), ("deposit", ctypes.c_int32), ("fallback", ctypes.c_int32),
         ("local_search", ctypes.c_int32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
-        ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+        ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("use_caller_stream", ctypes.c_int32),
     ]
 
 
@@ -140,7 +140,10 @@ class Colony:
         cfg.fallback = FALLBACK_ARGMAX if fallback_argmax else FALLBACK_WRS
         cfg.local_search = int(bool(local_search))
         cfg.device = int(device)
-        cfg.stream = stream
+        # stream=None: a stream owned by the context; otherwise the given cudaStream_t
+        # (0 = the legacy default stream, which is torch's default current stream)
+        cfg.stream = stream if stream else None
+        cfg.use_caller_stream = 0 if stream is None else 1
         cfg.rank, cfg.world = int(rank), int(world)
         h = ctypes.c_void_p()
         _err(L.mmas_create_ex(ctypes.byref(cfg), ctypes.byref(h)))
