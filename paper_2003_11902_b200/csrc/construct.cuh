@@ -1,0 +1,381 @@
+// construct.cuh -- tour construction kernels.
+//
+// One warp = one ant (the paper's data-parallel mapping at warp granularity,
+// P:1076-1082; one warp per ant at cl = 32).  A construction is
+// n-1 DEPENDENT selections (Alg. 1), so with ~7 ants per SM the
+// kernel is bound by the latency of one step, not by bandwidth or issue.  The
+// step is therefore laid out as a short dependency chain:
+//
+//   cur -> LDS (cand id, 1/w) -> tabu test (SHFL of a register bitmask, or LDS)
+//       -> key = log2(u) * (1/w) -> CREDUX.MIN (largest key) -> CREDUX.MIN (lowest id) -> cur
+//
+// and everything that does not depend on `cur` is moved off it: the random
+// keys of a candidate slot come from Philox counter (slot, s>>2, ant, iter)
+// (R13), so one Philox call per lane covers four steps, and the call
+// for the NEXT four steps is computed in slices interleaved with the current
+// four steps (software pipelining), where it fills the latency bubbles.
+#pragma once
+#include <cstdint>
+#include <type_traits>
+
+#include "rng.cuh"
+
+namespace mmas {
+
+// ---- bitmask tabu (Sec. 4.1) ------------------------------------------
+// n <= 1024: lane j keeps word j in a register; a test is one SHFL, a mark one OR.
+struct RegTabu {
+    uint32_t w;
+    __device__ __forceinline__ void init(uint32_t*, int, int) { w = 0u; }
+    // every lane of the warp must call word()/visited() (warp shuffle)
+    __device__ __forceinline__ uint32_t word(int idx) const { return __shfl_sync(kFull, w, idx & 31); }
+    __device__ __forceinline__ bool visited(uint32_t c) const { return (word((int)(c >> 5)) >> (c & 31)) & 1u; }
+    __device__ __forceinline__ void mark(uint32_t c, int lane) {
+        if (lane == (int)(c >> 5)) w |= 1u << (c & 31);
+    }
+    __device__ __forceinline__ void sync() {}
+};
+// any n: ceil(n/32) words per warp in shared memory.
+struct SmemTabu {
+    uint32_t* t;
+    __device__ __forceinline__ void init(uint32_t* base, int nwords, int lane) {
+        t = base;
+        for (int j = lane; j < nwords; j += 32) t[j] = 0u;
+        __syncwarp();
+    }
+    __device__ __forceinline__ uint32_t word(int idx) const { return t[idx]; }
+    __device__ __forceinline__ bool visited(uint32_t c) const { return (t[c >> 5] >> (c & 31)) & 1u; }
+    __device__ __forceinline__ void mark(uint32_t c, int lane) {
+        if (lane == 0) t[c >> 5] |= 1u << (c & 31);
+    }
+    __device__ __forceinline__ void sync() { __syncwarp(); }
+};
+
+// ---- Philox in slices (rounds [R0, R1)) for software pipelining ----------------------
+template <int R0, int R1>
+__device__ __forceinline__ void philox_rounds(uint4& c, PhiloxKey key) {
+#pragma unroll
+    for (int r = R0; r < R1; ++r) {
+        const uint32_t k0 = key.k0 + (uint32_t)r * 0x9E3779B9u;
+        const uint32_t k1 = key.k1 + (uint32_t)r * 0xBB67AE85u;
+        const uint32_t lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Scan of ALL unvisited cities from `row` (= inv_w[cur]): the full-row WRS step
+// (row a4) and the candidate-list fallback (row a3, R9).  Lane l handles the
+// 4-city groups 128t + 4l (a coalesced float4 of inv_w and one Philox per group
+// whose word j is city 4g+j's uniform, R13); groups whose four cities are all
+// visited are skipped.  Per-lane best with ties to the lower id; the caller
+// reduces across the warp.
+// ---------------------------------------------------------------------------
+template <bool kArgmax, class Tabu>
+__device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, const Tabu& tabu, int n,
+                                               uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
+                                               int lane, uint32_t& best_mag, uint32_t& best_c) {
+    for (int base = 0; base < n; base += 128) {
+        const int c0 = base + 4 * lane;
+        const uint32_t word = tabu.word(min(c0, n - 1) >> 5);   // all lanes (RegTabu shuffles)
+        if (c0 >= n) continue;
+        uint32_t nib = (word >> (c0 & 31)) & 0xFu;
+        if (c0 + 4 > n) nib |= (0xFu << (n - c0)) & 0xFu;     // cities >= n count as visited
+        if (nib == 0xFu) continue;
+        const float4 iv = __ldg(reinterpret_cast<const float4*>(row + c0));
+        const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
+        if (kArgmax) {
+            // R9 flag: the largest weight = the smallest inv_w (positive floats order as uints)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if ((nib >> j) & 1u) continue;
+                const uint32_t mag = __float_as_uint(ivs[j]);
+                if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
+            }
+        } else {
+            const uint4 x = philox4x32_10(ctr_city((uint32_t)c0 >> 2, step, ant, iter), key);
+            const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if ((nib >> j) & 1u) continue;
+                const float k = __fmul_rn(det_log2(uniform_open(xs[j])), ivs[j]);
+                const uint32_t mag = key_magnitude(k);
+                if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
+            }
+        }
+    }
+}
+
+template <bool kArgmax, class Tabu>
+__device__ __noinline__ uint32_t fallback_select(const float* __restrict__ row, const Tabu tabu, int n,
+                                                 uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
+                                                 int lane) {
+    uint32_t bm = kNone, bc = kNone;
+    scan_unvisited<kArgmax>(row, tabu, n, step, ant, iter, key, lane, bm, bc);
+    return warp_select(bm, bc);
+}
+
+// ---- per-ant epilogue: tour length (int64) + local iteration-best key (row a5) ----
+__device__ __forceinline__ void finish_ant(const ConstructArgs& A, const uint16_t* route, int al, uint32_t ant,
+                                           int lane, long long fb) {
+    long long len = 0;
+#pragma unroll 4
+    for (int k = lane; k < A.n; k += 32) {
+        const int i = route[k];
+        const int j = route[(k + 1 < A.n) ? k + 1 : 0];
+        len += euc2d(__ldg(A.xy + i), __ldg(A.xy + j));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(kFull, len, o);
+    if (lane == 0) {
+        A.lengths[al] = len;
+        atomicMin(A.best_key, ((unsigned long long)len << 24) | ant);
+        if (fb) atomicAdd(A.fallback_count, (unsigned long long)fb);
+    }
+}
+
+// Route staging: lane (s & 31) keeps route[s]; every 32 steps the warp writes a
+// coalesced 64-byte segment.
+__device__ __forceinline__ void stage_route(uint16_t* route, int s, uint32_t nxt, int lane, uint32_t& stage) {
+    if (lane == (s & 31)) stage = nxt;
+    if ((s & 31) == 31) route[(s & ~31) + lane] = (uint16_t)stage;
+}
+__device__ __forceinline__ void flush_route(uint16_t* route, int n, int lane, uint32_t stage) {
+    const int last = n - 1;
+    if ((last & 31) != 31) {
+        const int base = last & ~31;
+        if (base + lane <= last) route[base + lane] = (uint16_t)stage;
+    }
+}
+
+// ---- TMA bulk copy helpers (cp.async.bulk global -> shared, mbarrier completion) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+// smem layout of the candidate-list kernel:
+//   [0, 128)                 mbarrier (+ pad)
+//   [128, 128+Tinv)          cand_inv  n x cl f32   (smem-table variant)
+//   [.., +Tid)               cand_id   n x cl u16   (smem-table variant)
+//   [.., + W * 4*nwords)     tabu words (SmemTabu variant)
+extern __shared__ __align__(128) unsigned char g_smem[];
+
+// ---------------------------------------------------------------------------
+// Candidate-list construction (rows a1, a2, a3, a5-local).
+// kSlots = ceil(cl/32) candidate slots per lane; kSmemTable: the n x cl
+// (1/w, id) table is staged once per block into shared memory by TMA bulk
+// copies, else rows are read through L1/L2; kRegTabu: n <= 1024.
+// ---------------------------------------------------------------------------
+template <int kSlots, bool kSmemTable, bool kRegTabu>
+__global__ void __launch_bounds__(512) construct_cl_kernel(ConstructArgs A) {
+    using Tabu = typename std::conditional<kRegTabu, RegTabu, SmemTabu>::type;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int n = A.n, cl = A.cl;
+    const int nwords = (((n + 31) >> 5) + 3) & ~3;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
+    const uint32_t tab_off = kSmemTable ? 128u + A.table_bytes_inv + A.table_bytes_id : 128u;
+
+    if (kSmemTable) {
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            mbar_expect_tx(bar, A.table_bytes_inv + A.table_bytes_id);
+            constexpr uint32_t kChunk = 32768;
+            const uint32_t s_base = smem_u32(g_smem);
+            for (uint32_t off = 0; off < A.table_bytes_inv; off += kChunk)
+                bulk_g2s(s_base + 128u + off, reinterpret_cast<const unsigned char*>(A.cand_inv) + off,
+                         min(kChunk, A.table_bytes_inv - off), bar);
+            for (uint32_t off = 0; off < A.table_bytes_id; off += kChunk)
+                bulk_g2s(s_base + 128u + A.table_bytes_inv + off,
+                         reinterpret_cast<const unsigned char*>(A.cand_id) + off,
+                         min(kChunk, A.table_bytes_id - off), bar);
+        }
+    }
+    // 32-bit shared-window addresses of the two tables (plain LDS with a register address)
+    const uint32_t s_inv = smem_u32(g_smem) + 128u;
+    const uint32_t s_id = s_inv + A.table_bytes_inv;
+    uint32_t* tabu_base = reinterpret_cast<uint32_t*>(g_smem + tab_off) + warp * nwords;
+    const uint32_t iter = *A.iter_dev;
+    if (kSmemTable) {
+        __syncthreads();   // the barrier is initialised before anyone waits on it
+        mbar_wait(bar, 0);
+    }
+
+    for (int al = blockIdx.x * A.warps_per_block + warp; al < A.m_local; al += gridDim.x * A.warps_per_block) {
+        const uint32_t ant = (uint32_t)(A.ant_lo + al);
+        Tabu tabu;
+        tabu.init(tabu_base, nwords, lane);
+        // Alg. 1: start node u ~ U{0, n-1} (R13)
+        const uint32_t start = __umulhi(philox4x32_10(ctr_start(ant, iter), A.key).x, (uint32_t)n);
+        tabu.mark(start, lane);
+        tabu.sync();
+        uint16_t* route = A.routes + (size_t)al * A.ldr;
+        uint32_t stage = (lane == 0) ? start : 0u;
+        uint32_t cur = start;
+        long long fb = 0;
+
+        // slot uniforms of steps 0..3 (R13: counter (k, s>>2, a, iter), word s&3)
+        float L[kSlots][4];
+#pragma unroll
+        for (int q = 0; q < kSlots; ++q) {
+            const uint4 x = philox4x32_10(ctr_slot((uint32_t)(lane + 32 * q), 0u, ant, iter), A.key);
+            L[q][0] = det_log2(uniform_open(x.x));
+            L[q][1] = det_log2(uniform_open(x.y));
+            L[q][2] = det_log2(uniform_open(x.z));
+            L[q][3] = det_log2(uniform_open(x.w));
+        }
+
+        for (int g = 0; 4 * g < n; ++g) {
+            uint4 nx[kSlots];
+            float Ln[kSlots][4];
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q) nx[q] = ctr_slot((uint32_t)(lane + 32 * q), (uint32_t)(g + 1), ant, iter);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                // --- next group's random keys, one slice per step (off the dependency chain) ---
+#pragma unroll
+                for (int q = 0; q < kSlots; ++q) {
+                    if (j == 0) philox_rounds<0, 5>(nx[q], A.key);
+                    if (j == 1) philox_rounds<5, 10>(nx[q], A.key);
+                    if (j == 2) {
+                        Ln[q][0] = det_log2(uniform_open(nx[q].x));
+                        Ln[q][1] = det_log2(uniform_open(nx[q].y));
+                    }
+                    if (j == 3) {
+                        Ln[q][2] = det_log2(uniform_open(nx[q].z));
+                        Ln[q][3] = det_log2(uniform_open(nx[q].w));
+                    }
+                }
+                const int s = 4 * g + j;
+                if (s == 0 || s >= n) continue;
+                // --- step s: WRS over the unvisited candidates of cur (Alg. 3) ---
+                uint32_t bm = kNone, bc = kNone;
+#pragma unroll
+                for (int q = 0; q < kSlots; ++q) {
+                    const int slot = lane + 32 * q;
+                    const bool has = slot < cl;
+                    const int idx = (int)cur * cl + (has ? slot : 0);
+                    uint32_t c;
+                    float iv;
+                    if (kSmemTable) {
+                        c = lds_u16(s_id + 2u * (uint32_t)idx);
+                        iv = lds_f32(s_inv + 4u * (uint32_t)idx);
+                    } else {
+                        c = __ldg(A.cand_id + idx);
+                        iv = __ldg(A.cand_inv + idx);
+                    }
+                    const bool vis = tabu.visited(has ? c : cur);
+                    const uint32_t mag = vis ? kNone : key_magnitude(__fmul_rn(L[q][j], iv));
+                    if (kSlots == 1) {
+                        bm = mag;
+                        bc = c;
+                    } else if (mag < bm || (mag == bm && c < bc)) {
+                        bm = mag;
+                        bc = c;
+                    }
+                }
+                uint32_t nxt = warp_select(bm, bc);
+                if (__builtin_expect(nxt == kNone, 0)) {   // every candidate visited: R9 fallback (row a3)
+                    ++fb;
+                    const float* row = A.inv_w + (size_t)cur * A.ld;
+                    nxt = A.fallback_argmax
+                              ? fallback_select<true>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane)
+                              : fallback_select<false>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane);
+                }
+                tabu.mark(nxt, lane);
+                stage_route(route, s, nxt, lane, stage);
+                tabu.sync();
+                cur = nxt;
+            }
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) L[q][j] = Ln[q][j];
+        }
+        flush_route(route, n, lane, stage);
+        __syncwarp();
+        finish_ant(A, route, al, ant, lane, fb);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Full-row construction (rows a1, a4, a5-local; cl = 0, configuration C4):
+// every step scans all unvisited cities (Alg. 3 over the whole row).
+// ---------------------------------------------------------------------------
+template <bool kRegTabu>
+__global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
+    using Tabu = typename std::conditional<kRegTabu, RegTabu, SmemTabu>::type;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int n = A.n;
+    const int nwords = (((n + 31) >> 5) + 3) & ~3;
+    uint32_t* tabu_base = reinterpret_cast<uint32_t*>(g_smem + 128) + warp * nwords;
+    const uint32_t iter = *A.iter_dev;
+
+    for (int al = blockIdx.x * A.warps_per_block + warp; al < A.m_local; al += gridDim.x * A.warps_per_block) {
+        const uint32_t ant = (uint32_t)(A.ant_lo + al);
+        Tabu tabu;
+        tabu.init(tabu_base, nwords, lane);
+        const uint32_t start = __umulhi(philox4x32_10(ctr_start(ant, iter), A.key).x, (uint32_t)n);
+        tabu.mark(start, lane);
+        tabu.sync();
+        uint16_t* route = A.routes + (size_t)al * A.ldr;
+        uint32_t stage = (lane == 0) ? start : 0u;
+        uint32_t cur = start;
+        for (int s = 1; s < n; ++s) {
+            uint32_t bm = kNone, bc = kNone;
+            scan_unvisited<false>(A.inv_w + (size_t)cur * A.ld, tabu, n, (uint32_t)s, ant, iter, A.key, lane, bm,
+                                  bc);
+            const uint32_t nxt = warp_select(bm, bc);
+            tabu.mark(nxt, lane);
+            stage_route(route, s, nxt, lane, stage);
+            tabu.sync();
+            cur = nxt;
+        }
+        flush_route(route, n, lane, stage);
+        __syncwarp();
+        finish_ant(A, route, al, ant, lane, 0);
+    }
+}
+
+}  // namespace mmas

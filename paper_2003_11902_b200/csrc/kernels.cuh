@@ -73,273 +73,11 @@ struct ConstructArgs {
     unsigned long long* __restrict__ fallback_count;
 };
 
-// ---------------------------------------------------------------------------
-// Scan of ALL unvisited cities from `row` (= inv_w[cur]): the full-row WRS step
-// (row a4) and the candidate-list fallback (row a3, R9).  Lane l handles the
-// 4-city groups 128t + 4l (a coalesced float4 of inv_w and one Philox per group
-// whose word j is city 4g+j's uniform, R13); groups whose four cities are all
-// visited are skipped.  Per-lane best with ties to the lower id; the caller
-// reduces across the warp.
-// ---------------------------------------------------------------------------
-template <bool kArgmax>
-__device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, const uint32_t* tabu, int n,
-                                               uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
-                                               int lane, uint32_t& best_mag, uint32_t& best_c) {
-    for (int base = 0; base < n; base += 128) {
-        const int c0 = base + 4 * lane;
-        if (c0 >= n) continue;
-        uint32_t nib = (tabu[c0 >> 5] >> (c0 & 31)) & 0xFu;
-        if (c0 + 4 > n) nib |= (0xFu << (n - c0)) & 0xFu;   // cities >= n count as visited
-        if (nib == 0xFu) continue;
-        const float4 iv = __ldg(reinterpret_cast<const float4*>(row + c0));
-        const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
-        if (kArgmax) {
-            // R9 flag: largest weight = smallest inv_w (positive floats order as uints)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if ((nib >> j) & 1u) continue;
-                const uint32_t mag = __float_as_uint(ivs[j]);
-                if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
-            }
-        } else {
-            const uint4 x = philox4x32_10(ctr_city((uint32_t)c0 >> 2, step, ant, iter), key);
-            const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if ((nib >> j) & 1u) continue;
-                const float k = __fmul_rn(det_log2(uniform_open(xs[j])), ivs[j]);
-                const uint32_t mag = key_magnitude(k);
-                if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
-            }
-        }
-    }
-}
+}  // namespace mmas
 
-template <bool kArgmax>
-__device__ __noinline__ uint32_t fallback_select(const float* __restrict__ row, const uint32_t* tabu, int n,
-                                                 uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
-                                                 int lane) {
-    uint32_t bm = kNone, bc = kNone;
-    scan_unvisited<kArgmax>(row, tabu, n, step, ant, iter, key, lane, bm, bc);
-    return warp_select(bm, bc);
-}
+#include "construct.cuh"
 
-// ---- per-ant epilogue: tour length (int64) + local iteration-best key (row a5) ----
-__device__ __forceinline__ void finish_ant(const ConstructArgs& A, const uint16_t* route, int al, uint32_t ant,
-                                           int lane, long long fb) {
-    long long len = 0;
-    for (int k = lane; k < A.n; k += 32) {
-        const int i = route[k];
-        const int j = route[(k + 1 < A.n) ? k + 1 : 0];
-        len += euc2d(__ldg(A.xy + i), __ldg(A.xy + j));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(kFull, len, o);
-    if (lane == 0) {
-        A.lengths[al] = len;
-        atomicMin(A.best_key, ((unsigned long long)len << 24) | ant);
-        if (fb) atomicAdd(A.fallback_count, (unsigned long long)fb);
-    }
-}
-
-// Route staging: lane (s & 31) keeps route[s]; every 32 steps the warp writes a
-// coalesced 64-byte segment.
-__device__ __forceinline__ void stage_route(uint16_t* route, int s, uint32_t nxt, int lane, uint32_t& stage) {
-    if (lane == (s & 31)) stage = nxt;
-    if ((s & 31) == 31) route[(s & ~31) + lane] = (uint16_t)stage;
-}
-__device__ __forceinline__ void flush_route(uint16_t* route, int n, int lane, uint32_t stage) {
-    const int last = n - 1;
-    if ((last & 31) != 31) {
-        const int base = last & ~31;
-        if (base + lane <= last) route[base + lane] = (uint16_t)stage;
-    }
-}
-
-// ---- TMA bulk copy helpers (cp.async.bulk global -> shared, mbarrier completion) ----
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(phase)
-            : "memory");
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Candidate-list construction (rows a1, a2, a3, a5-local).  One warp = one ant
-// (the paper's data-parallel mapping at warp granularity, with
-// one warp per ant at cl = 32 as in P:1469-1472).  kSlots = ceil(cl/32)
-// candidate slots per lane.  kSmemTable: the n x cl (inv, id) table is staged
-// once per block into shared memory by TMA bulk copies; otherwise rows are read
-// through L1/L2.  Tabu: bitmask in shared memory, ceil(n/32) words per warp
-// (Sec. 4.1 "bitmask tabu").
-// ---------------------------------------------------------------------------
-template <int kSlots, bool kSmemTable>
-__global__ void __launch_bounds__(512) construct_cl_kernel(ConstructArgs A) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int n = A.n, cl = A.cl;
-    const int nwords = (((n + 31) >> 5) + 3) & ~3;
-
-    const float* cinv = A.cand_inv;
-    const uint16_t* cid = A.cand_id;
-    unsigned char* p = smem;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // smem[0..127]: mbarrier (+ pad)
-    if (kSmemTable) {
-        float* s_inv = reinterpret_cast<float*>(smem + 128);
-        uint16_t* s_id = reinterpret_cast<uint16_t*>(smem + 128 + A.table_bytes_inv);
-        if (threadIdx.x == 0) {
-            mbar_init(bar, 1);
-            mbar_expect_tx(bar, A.table_bytes_inv + A.table_bytes_id);
-            constexpr uint32_t kChunk = 32768;
-            for (uint32_t off = 0; off < A.table_bytes_inv; off += kChunk) {
-                const uint32_t sz = min(kChunk, A.table_bytes_inv - off);
-                bulk_g2s(reinterpret_cast<unsigned char*>(s_inv) + off,
-                         reinterpret_cast<const unsigned char*>(A.cand_inv) + off, sz, bar);
-            }
-            for (uint32_t off = 0; off < A.table_bytes_id; off += kChunk) {
-                const uint32_t sz = min(kChunk, A.table_bytes_id - off);
-                bulk_g2s(reinterpret_cast<unsigned char*>(s_id) + off,
-                         reinterpret_cast<const unsigned char*>(A.cand_id) + off, sz, bar);
-            }
-        }
-        cinv = s_inv;
-        cid = s_id;
-        p = smem + 128 + A.table_bytes_inv + A.table_bytes_id;
-    } else {
-        p = smem + 128;
-    }
-    uint32_t* tabu = reinterpret_cast<uint32_t*>(p) + warp * nwords;
-    const uint32_t iter = *A.iter_dev;
-    if (kSmemTable) {
-        __syncthreads();  // barrier initialised before anyone waits on it
-        mbar_wait(bar, 0);
-    }
-
-    for (int al = blockIdx.x * A.warps_per_block + warp; al < A.m_local; al += gridDim.x * A.warps_per_block) {
-        const uint32_t ant = (uint32_t)(A.ant_lo + al);
-        for (int j = lane; j < nwords; j += 32) tabu[j] = 0u;
-        __syncwarp();
-        // Alg. 1: start node u ~ U{0, n-1} (R13)
-        const uint32_t start = __umulhi(philox4x32_10(ctr_start(ant, iter), A.key).x, (uint32_t)n);
-        if (lane == 0) tabu[start >> 5] |= 1u << (start & 31);
-        uint16_t* route = A.routes + (size_t)al * A.ldr;
-        uint32_t stage = (lane == 0) ? start : 0u;
-        uint32_t cur = start;
-        long long fb = 0;
-        __syncwarp();
-
-        for (int g = 0; 4 * g < n; ++g) {
-            // slot uniforms for steps 4g .. 4g+3 (R13: counter (k, s>>2, a, iter), word s&3)
-            float L[kSlots][4];
-#pragma unroll
-            for (int q = 0; q < kSlots; ++q) {
-                const uint32_t slot = (uint32_t)(lane + 32 * q);
-                const uint4 x = philox4x32_10(ctr_slot(slot, (uint32_t)g, ant, iter), A.key);
-                L[q][0] = det_log2(uniform_open(x.x));
-                L[q][1] = det_log2(uniform_open(x.y));
-                L[q][2] = det_log2(uniform_open(x.z));
-                L[q][3] = det_log2(uniform_open(x.w));
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int s = 4 * g + j;
-                if (s == 0 || s >= n) continue;
-                uint32_t bm = kNone, bc = kNone;
-#pragma unroll
-                for (int q = 0; q < kSlots; ++q) {
-                    const int slot = lane + 32 * q;
-                    if (slot < cl) {
-                        const uint32_t c = cid[cur * cl + slot];
-                        const float iv = cinv[cur * cl + slot];
-                        if (!((tabu[c >> 5] >> (c & 31)) & 1u)) {
-                            const uint32_t mag = key_magnitude(__fmul_rn(L[q][j], iv));
-                            if (mag < bm || (mag == bm && c < bc)) { bm = mag; bc = c; }
-                        }
-                    }
-                }
-                uint32_t nxt = warp_select(bm, bc);
-                if (nxt == kNone) {  // every candidate visited: R9 fallback (row a3)
-                    ++fb;
-                    const float* row = A.inv_w + (size_t)cur * A.ld;
-                    nxt = A.fallback_argmax
-                              ? fallback_select<true>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane)
-                              : fallback_select<false>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane);
-                }
-                if (lane == 0) tabu[nxt >> 5] |= 1u << (nxt & 31);
-                stage_route(route, s, nxt, lane, stage);
-                __syncwarp();
-                cur = nxt;
-            }
-        }
-        flush_route(route, n, lane, stage);
-        __syncwarp();
-        finish_ant(A, route, al, ant, lane, fb);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Full-row construction (rows a1, a4, a5-local; cl = 0, configuration C4):
-// every step scans all unvisited cities (Alg. 3 over the whole row).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int n = A.n;
-    const int nwords = (((n + 31) >> 5) + 3) & ~3;
-    uint32_t* tabu = reinterpret_cast<uint32_t*>(smem + 128) + warp * nwords;
-    const uint32_t iter = *A.iter_dev;
-
-    for (int al = blockIdx.x * A.warps_per_block + warp; al < A.m_local; al += gridDim.x * A.warps_per_block) {
-        const uint32_t ant = (uint32_t)(A.ant_lo + al);
-        for (int j = lane; j < nwords; j += 32) tabu[j] = 0u;
-        __syncwarp();
-        const uint32_t start = __umulhi(philox4x32_10(ctr_start(ant, iter), A.key).x, (uint32_t)n);
-        if (lane == 0) tabu[start >> 5] |= 1u << (start & 31);
-        uint16_t* route = A.routes + (size_t)al * A.ldr;
-        uint32_t stage = (lane == 0) ? start : 0u;
-        uint32_t cur = start;
-        __syncwarp();
-        for (int s = 1; s < n; ++s) {
-            uint32_t bm = kNone, bc = kNone;
-            scan_unvisited<false>(A.inv_w + (size_t)cur * A.ld, tabu, n, (uint32_t)s, ant, iter, A.key, lane, bm,
-                                  bc);
-            const uint32_t nxt = warp_select(bm, bc);
-            if (lane == 0) tabu[nxt >> 5] |= 1u << (nxt & 31);
-            stage_route(route, s, nxt, lane, stage);
-            __syncwarp();
-            cur = nxt;
-        }
-        flush_route(route, n, lane, stage);
-        __syncwarp();
-        finish_ant(A, route, al, ant, lane, 0);
-    }
-}
+namespace mmas {
 
 // ---------------------------------------------------------------------------
 // Iteration best + global best + limits (row a5; Alg. 1).

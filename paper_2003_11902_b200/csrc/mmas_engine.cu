@@ -129,6 +129,7 @@ struct mmas_ctx {
 
     // launch plan for construction
     bool smem_table = false;
+    bool reg_tabu = false;   // n <= 1024: tabu words in registers
     int slots = 1;
     int cons_warps = 4, cons_grid = 1;
     size_t cons_smem = 0;
@@ -217,14 +218,35 @@ ConstructArgs construct_args(mmas_ctx* h) {
     return A;
 }
 
-template <int S, bool T>
+template <int S, bool T, bool R>
 void set_smem_attr(size_t bytes) {
-    cudaFuncSetAttribute(construct_cl_kernel<S, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(construct_cl_kernel<S, T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <int S, bool T>
+template <int S, bool T, bool R>
 void launch_cl(mmas_ctx* h, const ConstructArgs& A) {
-    construct_cl_kernel<S, T><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+    construct_cl_kernel<S, T, R><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+}
+
+// dispatch over the compile-time variants: slots per lane, table placement, tabu placement
+template <bool R>
+void launch_cl_r(mmas_ctx* h, const ConstructArgs& A) {
+    if (h->smem_table) {
+        if (h->slots == 1) launch_cl<1, true, R>(h, A);
+        else if (h->slots == 2) launch_cl<2, true, R>(h, A);
+        else launch_cl<4, true, R>(h, A);
+    } else {
+        if (h->slots == 1) launch_cl<1, false, R>(h, A);
+        else if (h->slots == 2) launch_cl<2, false, R>(h, A);
+        else launch_cl<4, false, R>(h, A);
+    }
+}
+
+template <bool R>
+void set_cl_attrs(size_t bytes) {
+    set_smem_attr<1, true, R>(bytes); set_smem_attr<1, false, R>(bytes);
+    set_smem_attr<2, true, R>(bytes); set_smem_attr<2, false, R>(bytes);
+    set_smem_attr<4, true, R>(bytes); set_smem_attr<4, false, R>(bytes);
 }
 
 int launch_construct(mmas_ctx* h) {
@@ -232,15 +254,14 @@ int launch_construct(mmas_ctx* h) {
     PhaseScope ps(h, 0);
     ConstructArgs A = construct_args(h);
     if (h->cl == 0) {
-        construct_full_kernel<<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
-    } else if (h->smem_table) {
-        if (h->slots == 1) launch_cl<1, true>(h, A);
-        else if (h->slots == 2) launch_cl<2, true>(h, A);
-        else launch_cl<4, true>(h, A);
+        if (h->reg_tabu)
+            construct_full_kernel<true><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+        else
+            construct_full_kernel<false><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+    } else if (h->reg_tabu) {
+        launch_cl_r<true>(h, A);
     } else {
-        if (h->slots == 1) launch_cl<1, false>(h, A);
-        else if (h->slots == 2) launch_cl<2, false>(h, A);
-        else launch_cl<4, false>(h, A);
+        launch_cl_r<false>(h, A);
     }
     h->launches++;
     CU(cudaGetLastError());
@@ -417,11 +438,13 @@ int setup(mmas_ctx* h) {
 
     // ---- construction launch plan ----
     const int nwords = round_up((n + 31) / 32, 4);
-    const size_t tabu_bytes = (size_t)nwords * 4;
+    h->reg_tabu = n <= 1024;
+    const size_t tabu_bytes = h->reg_tabu ? 0 : (size_t)nwords * 4;
     h->slots = h->cl <= 32 ? 1 : (h->cl <= 64 ? 2 : 4);
     if (h->cl > 0) {
         h->tb_inv = (uint32_t)round_up(n * h->cl * 4, 16);
         h->tb_id = (uint32_t)round_up(n * h->cl * 2, 16);
+        // one block per SM holding the whole table; as many warps (ants) as needed
         int w = std::max(1, std::min(16, (h->m_local + h->num_sms - 1) / std::max(h->num_sms, 1)));
         size_t need = 128 + (size_t)h->tb_inv + h->tb_id + (size_t)w * tabu_bytes;
         h->smem_table = need <= (size_t)h->smem_optin;
@@ -442,11 +465,11 @@ int setup(mmas_ctx* h) {
     if (h->cons_smem > (size_t)h->smem_optin)
         return fail(MMAS_EINVAL, "n too large for the shared-memory tabu of one block");
     if (h->cl > 0) {
-        if (h->slots == 1) { set_smem_attr<1, true>(h->cons_smem); set_smem_attr<1, false>(h->cons_smem); }
-        else if (h->slots == 2) { set_smem_attr<2, true>(h->cons_smem); set_smem_attr<2, false>(h->cons_smem); }
-        else { set_smem_attr<4, true>(h->cons_smem); set_smem_attr<4, false>(h->cons_smem); }
+        if (h->reg_tabu) set_cl_attrs<true>(h->cons_smem);
+        else set_cl_attrs<false>(h->cons_smem);
     } else {
-        cudaFuncSetAttribute(construct_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->cons_smem);
+        cudaFuncSetAttribute(construct_full_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->cons_smem);
+        cudaFuncSetAttribute(construct_full_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->cons_smem);
     }
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(h->stream));
