@@ -232,8 +232,11 @@ __global__ void __launch_bounds__(512) construct_cl_kernel(ConstructArgs A) {
         }
     }
     // 32-bit shared-window addresses of the two tables (plain LDS with a register address)
-    const uint32_t s_inv = smem_u32(g_smem) + 128u;
-    const uint32_t s_id = s_inv + A.table_bytes_inv;
+    uint32_t s_inv = smem_u32(g_smem) + 128u;
+    uint32_t s_id = s_inv + A.table_bytes_inv;
+    // opaque: keep the addresses in registers (otherwise ptxas re-derives the shared
+    // window base with a long-latency S2UR SR_CgaCtaId inside every step)
+    asm volatile("" : "+r"(s_inv), "+r"(s_id));
     uint32_t* tabu_base = reinterpret_cast<uint32_t*>(g_smem + tab_off) + warp * nwords;
     const uint32_t iter = *A.iter_dev;
     if (kSmemTable) {
@@ -265,73 +268,116 @@ __global__ void __launch_bounds__(512) construct_cl_kernel(ConstructArgs A) {
             L[q][3] = det_log2(uniform_open(x.w));
         }
 
-        for (int g = 0; 4 * g < n; ++g) {
-            uint4 nx[kSlots];
-            float Ln[kSlots][4];
+        uint4 nx[kSlots];
+        float Ln[kSlots][4];
+        // next group's random keys, one slice per step: Philox rounds 0-4, 5-9, then the
+        // logs of words 0-1 and 2-3 (off the dependency chain; R13)
+        auto slice = [&](auto J) {
+            constexpr int j = decltype(J)::value;
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q) {
+                if (j == 0) philox_rounds<0, 5>(nx[q], A.key);
+                if (j == 1) philox_rounds<5, 10>(nx[q], A.key);
+                if (j == 2) {
+                    Ln[q][0] = det_log2(uniform_open(nx[q].x));
+                    Ln[q][1] = det_log2(uniform_open(nx[q].y));
+                }
+                if (j == 3) {
+                    Ln[q][2] = det_log2(uniform_open(nx[q].z));
+                    Ln[q][3] = det_log2(uniform_open(nx[q].w));
+                }
+            }
+        };
+        // step s (word j = s & 3 of the slot uniforms): WRS over the unvisited candidates of
+        // cur (Alg. 3)
+        auto step = [&](auto J, int s) {
+            constexpr int j = decltype(J)::value;
+            uint32_t bm = kNone, bc = kNone;
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q) {
+                const int slot = lane + 32 * q;
+                const bool has = slot < cl;
+                const int idx = (int)cur * cl + (has ? slot : 0);
+                uint32_t c;
+                float iv;
+                if (kSmemTable) {
+                    c = lds_u16(s_id + 2u * (uint32_t)idx);
+                    iv = lds_f32(s_inv + 4u * (uint32_t)idx);
+                } else {
+                    c = __ldg(A.cand_id + idx);
+                    iv = __ldg(A.cand_inv + idx);
+                }
+                const bool vis = tabu.visited(has ? c : cur);
+                const uint32_t mag = vis ? kNone : key_magnitude(__fmul_rn(L[q][j], iv));
+                if (kSlots == 1) {
+                    bm = mag;
+                    bc = c;
+                } else if (mag < bm || (mag == bm && c < bc)) {
+                    bm = mag;
+                    bc = c;
+                }
+            }
+            // argmax (ties -> lowest city id, R16): both reductions back to back
+            const uint32_t best = __reduce_min_sync(kFull, bm);
+            uint32_t nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
+            if (__builtin_expect(best == kNone, 0)) {   // every candidate visited: R9 fallback (row a3)
+                ++fb;
+                const float* row = A.inv_w + (size_t)cur * A.ld;
+                nxt = A.fallback_argmax
+                          ? fallback_select<true>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane)
+                          : fallback_select<false>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane);
+            }
+            tabu.mark(nxt, lane);
+            stage_route(route, s, nxt, lane, stage);
+            tabu.sync();
+            cur = nxt;
+        };
+        auto next_group = [&](int g) {
 #pragma unroll
             for (int q = 0; q < kSlots; ++q) nx[q] = ctr_slot((uint32_t)(lane + 32 * q), (uint32_t)(g + 1), ant, iter);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                // --- next group's random keys, one slice per step (off the dependency chain) ---
-#pragma unroll
-                for (int q = 0; q < kSlots; ++q) {
-                    if (j == 0) philox_rounds<0, 5>(nx[q], A.key);
-                    if (j == 1) philox_rounds<5, 10>(nx[q], A.key);
-                    if (j == 2) {
-                        Ln[q][0] = det_log2(uniform_open(nx[q].x));
-                        Ln[q][1] = det_log2(uniform_open(nx[q].y));
-                    }
-                    if (j == 3) {
-                        Ln[q][2] = det_log2(uniform_open(nx[q].z));
-                        Ln[q][3] = det_log2(uniform_open(nx[q].w));
-                    }
-                }
-                const int s = 4 * g + j;
-                if (s == 0 || s >= n) continue;
-                // --- step s: WRS over the unvisited candidates of cur (Alg. 3) ---
-                uint32_t bm = kNone, bc = kNone;
-#pragma unroll
-                for (int q = 0; q < kSlots; ++q) {
-                    const int slot = lane + 32 * q;
-                    const bool has = slot < cl;
-                    const int idx = (int)cur * cl + (has ? slot : 0);
-                    uint32_t c;
-                    float iv;
-                    if (kSmemTable) {
-                        c = lds_u16(s_id + 2u * (uint32_t)idx);
-                        iv = lds_f32(s_inv + 4u * (uint32_t)idx);
-                    } else {
-                        c = __ldg(A.cand_id + idx);
-                        iv = __ldg(A.cand_inv + idx);
-                    }
-                    const bool vis = tabu.visited(has ? c : cur);
-                    const uint32_t mag = vis ? kNone : key_magnitude(__fmul_rn(L[q][j], iv));
-                    if (kSlots == 1) {
-                        bm = mag;
-                        bc = c;
-                    } else if (mag < bm || (mag == bm && c < bc)) {
-                        bm = mag;
-                        bc = c;
-                    }
-                }
-                uint32_t nxt = warp_select(bm, bc);
-                if (__builtin_expect(nxt == kNone, 0)) {   // every candidate visited: R9 fallback (row a3)
-                    ++fb;
-                    const float* row = A.inv_w + (size_t)cur * A.ld;
-                    nxt = A.fallback_argmax
-                              ? fallback_select<true>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane)
-                              : fallback_select<false>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane);
-                }
-                tabu.mark(nxt, lane);
-                stage_route(route, s, nxt, lane, stage);
-                tabu.sync();
-                cur = nxt;
-            }
+        };
+        auto rotate = [&]() {
 #pragma unroll
             for (int q = 0; q < kSlots; ++q)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) L[q][j] = Ln[q][j];
+        };
+        using I0 = std::integral_constant<int, 0>;
+        using I1 = std::integral_constant<int, 1>;
+        using I2 = std::integral_constant<int, 2>;
+        using I3 = std::integral_constant<int, 3>;
+        // a group with per-step guards (group 0 holds s = 0, the last group may be ragged)
+        auto guarded_group = [&](int g, bool pipeline) {
+            if (pipeline) next_group(g);
+            if (pipeline) slice(I0{});
+            if (4 * g + 0 > 0 && 4 * g + 0 < n) step(I0{}, 4 * g + 0);
+            if (pipeline) slice(I1{});
+            if (4 * g + 1 < n) step(I1{}, 4 * g + 1);
+            if (pipeline) slice(I2{});
+            if (4 * g + 2 < n) step(I2{}, 4 * g + 2);
+            if (pipeline) slice(I3{});
+            if (4 * g + 3 < n) step(I3{}, 4 * g + 3);
+            if (pipeline) rotate();
+        };
+        const int n_groups = (n + 3) / 4;      // groups holding a step s < n
+        const int n_full = n / 4;              // groups g < n_full have all four steps < n
+        guarded_group(0, n_groups > 1);
+        // full groups: no guard between a Philox slice and the step it overlaps, so each
+        // slice and its step's dependency chain share one basic block for the scheduler
+        int g = 1;
+        for (; g < n_full && g < n_groups - 1; ++g) {
+            next_group(g);
+            slice(I0{});
+            step(I0{}, 4 * g + 0);
+            slice(I1{});
+            step(I1{}, 4 * g + 1);
+            slice(I2{});
+            step(I2{}, 4 * g + 2);
+            slice(I3{});
+            step(I3{}, 4 * g + 3);
+            rotate();
         }
+        for (; g < n_groups; ++g) guarded_group(g, g + 1 < n_groups);
         flush_route(route, n, lane, stage);
         __syncwarp();
         finish_ant(A, route, al, ant, lane, fb);
