@@ -28,8 +28,10 @@ struct RegTabu {
     uint32_t w;
     __device__ __forceinline__ void init(uint32_t*, int, int) { w = 0u; }
     // every lane of the warp must call word()/visited() (warp shuffle)
-    __device__ __forceinline__ uint32_t word(int idx) const { return __shfl_sync(kFull, w, idx & 31); }
+    __device__ __forceinline__ uint32_t word(int idx) const { return __shfl_sync(kFull, w, idx); }
     __device__ __forceinline__ bool visited(uint32_t c) const { return (word((int)(c >> 5)) >> (c & 31)) & 1u; }
+    // bit 31 = "c visited" (other bits garbage); lanes may pass any c < 1024
+    __device__ __forceinline__ uint32_t top_bit(uint32_t c) const { return word((int)(c >> 5)) << (~c & 31u); }
     __device__ __forceinline__ void mark(uint32_t c, int lane) {
         if (lane == (int)(c >> 5)) w |= 1u << (c & 31);
     }
@@ -45,6 +47,7 @@ struct SmemTabu {
     }
     __device__ __forceinline__ uint32_t word(int idx) const { return t[idx]; }
     __device__ __forceinline__ bool visited(uint32_t c) const { return (t[c >> 5] >> (c & 31)) & 1u; }
+    __device__ __forceinline__ uint32_t top_bit(uint32_t c) const { return t[c >> 5] << (~c & 31u); }
     __device__ __forceinline__ void mark(uint32_t c, int lane) {
         if (lane == 0) t[c >> 5] |= 1u << (c & 31);
     }
@@ -206,8 +209,9 @@ extern __shared__ __align__(128) unsigned char g_smem[];
 // (1/w, id) table is staged once per block into shared memory by TMA bulk
 // copies, else rows are read through L1/L2; kRegTabu: n <= 1024.
 // ---------------------------------------------------------------------------
-template <int kSlots, bool kSmemTable, bool kRegTabu>
-__global__ void __launch_bounds__(512) construct_cl_kernel(ConstructArgs A) {
+template <int kSlots, bool kSmemTable, bool kRegTabu, bool kFull32>
+__global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
+    static_assert(!kFull32 || kSlots == 1, "kFull32: cl == 32, one slot per lane");
     using Tabu = typename std::conditional<kRegTabu, RegTabu, SmemTabu>::type;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -237,6 +241,8 @@ __global__ void __launch_bounds__(512) construct_cl_kernel(ConstructArgs A) {
     // opaque: keep the addresses in registers (otherwise ptxas re-derives the shared
     // window base with a long-latency S2UR SR_CgaCtaId inside every step)
     asm volatile("" : "+r"(s_inv), "+r"(s_id));
+    const uint32_t id_lane = s_id + 2u * (uint32_t)lane;     // kFull32: slot = lane
+    const uint32_t inv_lane = s_inv + 4u * (uint32_t)lane;
     uint32_t* tabu_base = reinterpret_cast<uint32_t*>(g_smem + tab_off) + warp * nwords;
     const uint32_t iter = *A.iter_dev;
     if (kSmemTable) {
@@ -293,6 +299,23 @@ __global__ void __launch_bounds__(512) construct_cl_kernel(ConstructArgs A) {
         auto step = [&](auto J, int s) {
             constexpr int j = decltype(J)::value;
             uint32_t bm = kNone, bc = kNone;
+            if constexpr (kFull32) {
+                // cl == 32: lane k owns slot k.  Shortest chain: one IMAD per address, the
+                // tabu bit shifted to bit 31 and merged with the key magnitude by one LOP3
+                // (a visited lane's value has bit 31 set, so it loses to every unvisited one).
+                uint32_t c;
+                float iv;
+                if (kSmemTable) {
+                    c = lds_u16(id_lane + cur * 64u);
+                    iv = lds_f32(inv_lane + cur * 128u);
+                } else {
+                    c = __ldg(A.cand_id + cur * 32u + lane);
+                    iv = __ldg(A.cand_inv + cur * 32u + lane);
+                }
+                const uint32_t t = tabu.top_bit(c);
+                bm = (__float_as_uint(__fmul_rn(L[0][j], iv)) & 0x7FFFFFFFu) | (t & 0x80000000u);
+                bc = c;
+            } else {
 #pragma unroll
             for (int q = 0; q < kSlots; ++q) {
                 const int slot = lane + 32 * q;
@@ -317,10 +340,12 @@ __global__ void __launch_bounds__(512) construct_cl_kernel(ConstructArgs A) {
                     bc = c;
                 }
             }
-            // argmax (ties -> lowest city id, R16): both reductions back to back
+            }
+            // argmax (ties -> lowest city id, R16): both reductions back to back; a best
+            // value with bit 31 set means no unvisited candidate
             const uint32_t best = __reduce_min_sync(kFull, bm);
             uint32_t nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
-            if (__builtin_expect(best == kNone, 0)) {   // every candidate visited: R9 fallback (row a3)
+            if (__builtin_expect(best >= 0x80000000u, 0)) {   // every candidate visited: R9 fallback (row a3)
                 ++fb;
                 const float* row = A.inv_w + (size_t)cur * A.ld;
                 nxt = A.fallback_argmax

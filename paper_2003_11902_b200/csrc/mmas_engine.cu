@@ -218,14 +218,20 @@ ConstructArgs construct_args(mmas_ctx* h) {
     return A;
 }
 
-template <int S, bool T, bool R>
+template <int S, bool T, bool R, bool F = false>
 void set_smem_attr(size_t bytes) {
-    cudaFuncSetAttribute(construct_cl_kernel<S, T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(construct_cl_kernel<S, T, R, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 template <int S, bool T, bool R>
 void launch_cl(mmas_ctx* h, const ConstructArgs& A) {
-    construct_cl_kernel<S, T, R><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+    if constexpr (S == 1) {
+        if (h->cl == 32) {
+            construct_cl_kernel<1, T, R, true><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+            return;
+        }
+    }
+    construct_cl_kernel<S, T, R, false><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
 }
 
 // dispatch over the compile-time variants: slots per lane, table placement, tabu placement
@@ -245,6 +251,7 @@ void launch_cl_r(mmas_ctx* h, const ConstructArgs& A) {
 template <bool R>
 void set_cl_attrs(size_t bytes) {
     set_smem_attr<1, true, R>(bytes); set_smem_attr<1, false, R>(bytes);
+    set_smem_attr<1, true, R, true>(bytes); set_smem_attr<1, false, R, true>(bytes);
     set_smem_attr<2, true, R>(bytes); set_smem_attr<2, false, R>(bytes);
     set_smem_attr<4, true, R>(bytes); set_smem_attr<4, false, R>(bytes);
 }
@@ -445,7 +452,7 @@ int setup(mmas_ctx* h) {
         h->tb_inv = (uint32_t)round_up(n * h->cl * 4, 16);
         h->tb_id = (uint32_t)round_up(n * h->cl * 2, 16);
         // one block per SM holding the whole table; as many warps (ants) as needed
-        int w = std::max(1, std::min(16, (h->m_local + h->num_sms - 1) / std::max(h->num_sms, 1)));
+        int w = std::max(1, std::min(8, (h->m_local + h->num_sms - 1) / std::max(h->num_sms, 1)));
         size_t need = 128 + (size_t)h->tb_inv + h->tb_id + (size_t)w * tabu_bytes;
         h->smem_table = need <= (size_t)h->smem_optin;
         if (h->smem_table) {
