@@ -250,12 +250,14 @@ def run_ours(args):
         c2 = mmas.Colony(pinned, w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=local_rank)
         for _ in range(out_steps):
             c2.iterate(1)
-            c2.best_tour()
+            c2.best_length()
+        tour, _ = c2.best_tour()
         el = time.perf_counter() - t0
         c2.close()
         e2e = {"value": w.n_ants * out_steps / el, "unit": UNIT,
-               "h2d_bytes_per_step": 16 * w.n / out_steps, "d2h_bytes_per_step": 2 * w.n + 8,
-               "note": "mmas_create from host coords + per step mmas_iterate(1) + mmas_best_tour (sync, D2H)"}
+               "h2d_bytes_per_step": 16 * w.n / out_steps, "d2h_bytes_per_step": 8 + 2 * w.n / out_steps,
+               "note": "timed: mmas_create from pinned host coords (H2D), per step mmas_iterate(1) + "
+                       "mmas_best_length (sync + 8-byte D2H), final mmas_best_tour (D2H of the route)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -122,6 +122,10 @@ int mmas_update(mmas_ctx *h, const void *records_dev, int32_t count);
  * empty, Alg. 1), or another negative mmas_status. */
 int64_t mmas_best_tour(mmas_ctx *h, int32_t *tour_out);
 
+/* Synchronises and returns only the global best length (8-byte read-back), or
+ * MMAS_ESTATE before the first iteration. */
+int64_t mmas_best_length(mmas_ctx *h);
+
 /* Frees every device and host resource.  NULL is a no-op. */
 void mmas_destroy(mmas_ctx *h);
 

@@ -55,12 +55,25 @@ struct SmemTabu {
 };
 
 // ---- Philox in slices (rounds [R0, R1)) for software pipelining ----------------------
+// Round keys precomputed once per kernel (warp-uniform: they live in uniform registers).
+struct RoundKeys {
+    uint32_t k0[10], k1[10];
+    __device__ __forceinline__ explicit RoundKeys(PhiloxKey key) {
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            k0[r] = key.k0 + (uint32_t)r * 0x9E3779B9u;
+            k1[r] = key.k1 + (uint32_t)r * 0xBB67AE85u;
+        }
+    }
+};
+
 template <int R0, int R1>
-__device__ __forceinline__ void philox_rounds(uint4& c, PhiloxKey key) {
+__device__ __forceinline__ void philox_rounds(uint4& c, const RoundKeys& rk) {
 #pragma unroll
     for (int r = R0; r < R1; ++r) {
-        const uint32_t k0 = key.k0 + (uint32_t)r * 0x9E3779B9u;
-        const uint32_t k1 = key.k1 + (uint32_t)r * 0xBB67AE85u;
+        // round keys: base key + r * Weyl constant, uniform (UIADD3 on the uniform datapath)
+        const uint32_t k0 = rk.k0[0] + (uint32_t)r * 0x9E3779B9u;
+        const uint32_t k1 = rk.k1[0] + (uint32_t)r * 0xBB67AE85u;
         const uint32_t lo0 = 0xD2511F53u * c.x;
         const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
         const uint32_t lo1 = 0xCD9E8D57u * c.z;
@@ -122,8 +135,8 @@ __device__ __noinline__ uint32_t fallback_select(const float* __restrict__ row, 
 }
 
 // ---- per-ant epilogue: tour length (int64) + local iteration-best key (row a5) ----
-__device__ __forceinline__ void finish_ant(const ConstructArgs& A, const uint16_t* route, int al, uint32_t ant,
-                                           int lane, long long fb) {
+__device__ __forceinline__ unsigned long long finish_ant(const ConstructArgs& A, const uint16_t* route, int al,
+                                                         uint32_t ant, int lane) {
     long long len = 0;
 #pragma unroll 4
     for (int k = lane; k < A.n; k += 32) {
@@ -133,10 +146,44 @@ __device__ __forceinline__ void finish_ant(const ConstructArgs& A, const uint16_
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(kFull, len, o);
+    if (lane == 0) A.lengths[al] = len;
+    return ((unsigned long long)len << 24) | ant;   // iteration-best key (R8)
+}
+
+// Block epilogue: the block's best key and fallback count reach global memory with
+// ONE atomic each (a per-ant global atomic makes ~10^3 same-address atomics queue
+// up at the end of the launch).  world == 1: the last block to finish selects the
+// iteration best with one warp (row a5; all route writes are fenced first).
+__device__ __forceinline__ void block_finish(const ConstructArgs& A, unsigned long long wbest, long long wfb,
+                                             int lane, int warp) {
+    __shared__ unsigned long long s_best, s_fb;
+    __shared__ unsigned s_last;
+    if (threadIdx.x == 0) {
+        s_best = ~0ull;
+        s_fb = 0ull;
+    }
+    __threadfence();
+    __syncthreads();
     if (lane == 0) {
-        A.lengths[al] = len;
-        atomicMin(A.best_key, ((unsigned long long)len << 24) | ant);
-        if (fb) atomicAdd(A.fallback_count, (unsigned long long)fb);
+        atomicMin(&s_best, wbest);
+        if (wfb) atomicAdd(&s_fb, (unsigned long long)wfb);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_best != ~0ull) atomicMin(A.best_key, s_best);
+        if (s_fb) atomicAdd(A.fallback_count, s_fb);
+        unsigned last = 0;
+        if (A.fuse_select) {
+            __threadfence();
+            last = atomicAdd(A.done, 1u) == gridDim.x - 1u;
+        }
+        s_last = last;
+    }
+    __syncthreads();
+    if (s_last && warp == 0) {
+        __threadfence();
+        select_best_warp(A.sel, lane);
+        if (lane == 0) *A.done = 0u;
     }
 }
 
@@ -241,6 +288,7 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
     // opaque: keep the addresses in registers (otherwise ptxas re-derives the shared
     // window base with a long-latency S2UR SR_CgaCtaId inside every step)
     asm volatile("" : "+r"(s_inv), "+r"(s_id));
+    const RoundKeys rk(A.key);
     const uint32_t id_lane = s_id + 2u * (uint32_t)lane;     // kFull32: slot = lane
     const uint32_t inv_lane = s_inv + 4u * (uint32_t)lane;
     uint32_t* tabu_base = reinterpret_cast<uint32_t*>(g_smem + tab_off) + warp * nwords;
@@ -249,6 +297,8 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
         __syncthreads();   // the barrier is initialised before anyone waits on it
         mbar_wait(bar, 0);
     }
+    unsigned long long wbest = ~0ull;
+    long long wfb = 0;
 
     for (int al = blockIdx.x * A.warps_per_block + warp; al < A.m_local; al += gridDim.x * A.warps_per_block) {
         const uint32_t ant = (uint32_t)(A.ant_lo + al);
@@ -282,8 +332,8 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
             constexpr int j = decltype(J)::value;
 #pragma unroll
             for (int q = 0; q < kSlots; ++q) {
-                if (j == 0) philox_rounds<0, 5>(nx[q], A.key);
-                if (j == 1) philox_rounds<5, 10>(nx[q], A.key);
+                if (j == 0) philox_rounds<0, 5>(nx[q], rk);
+                if (j == 1) philox_rounds<5, 10>(nx[q], rk);
                 if (j == 2) {
                     Ln[q][0] = det_log2(uniform_open(nx[q].x));
                     Ln[q][1] = det_log2(uniform_open(nx[q].y));
@@ -405,8 +455,10 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
         for (; g < n_groups; ++g) guarded_group(g, g + 1 < n_groups);
         flush_route(route, n, lane, stage);
         __syncwarp();
-        finish_ant(A, route, al, ant, lane, fb);
+        wbest = min(wbest, finish_ant(A, route, al, ant, lane));
+        wfb += fb;
     }
+    block_finish(A, wbest, wfb, lane, warp);
 }
 
 // ---------------------------------------------------------------------------
@@ -422,6 +474,7 @@ __global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
     const int nwords = (((n + 31) >> 5) + 3) & ~3;
     uint32_t* tabu_base = reinterpret_cast<uint32_t*>(g_smem + 128) + warp * nwords;
     const uint32_t iter = *A.iter_dev;
+    unsigned long long wbest = ~0ull;
 
     for (int al = blockIdx.x * A.warps_per_block + warp; al < A.m_local; al += gridDim.x * A.warps_per_block) {
         const uint32_t ant = (uint32_t)(A.ant_lo + al);
@@ -445,8 +498,9 @@ __global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
         }
         flush_route(route, n, lane, stage);
         __syncwarp();
-        finish_ant(A, route, al, ant, lane, 0);
+        wbest = min(wbest, finish_ant(A, route, al, ant, lane));
     }
+    block_finish(A, wbest, 0, lane, warp);
 }
 
 }  // namespace mmas

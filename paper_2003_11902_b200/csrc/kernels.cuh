@@ -55,34 +55,12 @@ __device__ __forceinline__ uint32_t warp_select(uint32_t mag, uint32_t city) {
     return __reduce_min_sync(kFull, mag == best ? city : kNone);
 }
 
-struct ConstructArgs {
-    const double2* __restrict__ xy;
-    const float* __restrict__ inv_w;        // n x ld
-    const uint16_t* __restrict__ cand_id;   // n x cl
-    const float* __restrict__ cand_inv;     // n x cl, = inv_w[i][cand_id[i][k]]
-    const uint32_t* __restrict__ iter_dev;  // global iteration counter (R20)
-    PhiloxKey key;
-    int n, ld, cl, ldr;
-    int ant_lo, m_local;
-    int fallback_argmax;
-    int warps_per_block;
-    uint32_t table_bytes_inv, table_bytes_id;  // smem-table variant: padded table sizes
-    uint16_t* __restrict__ routes;          // m_local x ldr
-    long long* __restrict__ lengths;        // m_local
-    unsigned long long* __restrict__ best_key;       // local min (len << 24 | ant)
-    unsigned long long* __restrict__ fallback_count;
-};
-
-}  // namespace mmas
-
-#include "construct.cuh"
-
-namespace mmas {
-
 // ---------------------------------------------------------------------------
-// Iteration best + global best + limits (row a5; Alg. 1).
-// Either from this context's local best key (world == 1) or from `count`
-// gathered per-rank records [u64 key][u16 route[n]] (world > 1).
+// Iteration best + global best + limits (row a5; Alg. 1), then the
+// deposit route's successor / predecessor tables for the update.  Either from
+// this context's local best key (world == 1) or from `count` gathered per-rank
+// records [u64 key][u16 route[n]] (world > 1).  Run by ONE warp: either the
+// last construction warp to finish (world == 1, fused) or select_best_kernel.
 // ---------------------------------------------------------------------------
 struct SelectArgs {
     const unsigned char* records;  // nullptr = local mode
@@ -102,27 +80,28 @@ struct SelectArgs {
     uint16_t* pred;
 };
 
-__global__ void __launch_bounds__(1024) select_best_kernel(SelectArgs S) {
-    __shared__ const uint16_t* src;
-    __shared__ int improved;
+__device__ __noinline__ void select_best_warp(const SelectArgs S, int lane) {
     const int n = S.n;
-    if (threadIdx.x == 0) {
-        unsigned long long key;
+    unsigned long long key = 0;
+    const uint16_t* src = nullptr;
+    int improved = 0;
+    long long gbl = 0;
+    if (lane == 0) {
         if (S.records) {
             int bi = 0;
-            key = *reinterpret_cast<const unsigned long long*>(S.records);
+            key = __ldcg(reinterpret_cast<const unsigned long long*>(S.records));
             for (int r = 1; r < S.count; ++r) {
                 const unsigned long long k =
-                    *reinterpret_cast<const unsigned long long*>(S.records + (size_t)r * S.rec_bytes);
+                    __ldcg(reinterpret_cast<const unsigned long long*>(S.records + (size_t)r * S.rec_bytes));
                 if (k < key) { key = k; bi = r; }
             }
             src = reinterpret_cast<const uint16_t*>(S.records + (size_t)bi * S.rec_bytes + 8);
         } else {
-            key = *S.local_key;
+            key = __ldcg(S.local_key);
             src = S.routes + (size_t)((int)(key & 0xFFFFFFu) - S.ant_lo) * S.ldr;
         }
         const long long len = (long long)(key >> 24);
-        const long long gbl = *S.gb_len;
+        gbl = __ldcg(S.gb_len);
         improved = (gbl < 0 || len < gbl);   // strictly shorter (R8)
         if (improved) {
             *S.gb_len = len;
@@ -137,24 +116,80 @@ __global__ void __launch_bounds__(1024) select_best_kernel(SelectArgs S) {
         S.scal[2] = __double2float_rn(__ddiv_rn(1.0, (double)dep));   // R6
         *S.ib_len = len;
         *S.ib_ant = (int)(key & 0xFFFFFFu);
+        if (!S.records) *S.local_key = ~0ull;
     }
-    __syncthreads();
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        const uint16_t v = src[k];
-        S.ib_route[k] = v;
-        if (improved) S.gb_route[k] = v;
+    improved = __shfl_sync(kFull, improved, 0);
+    src = reinterpret_cast<const uint16_t*>(__shfl_sync(kFull, reinterpret_cast<unsigned long long>(src), 0));
+    // deposit route: the iteration best, or the (possibly just replaced) global best (R7)
+    const uint16_t* dep = (!S.deposit_global || improved) ? src : S.gb_route;
+    // 4 cities per 8-byte vector (routes and records are 8-byte aligned); every load of
+    // the warp is issued before any store, so the copy costs ~one L2 round trip
+    constexpr int kVecPerLane = 8;    // n <= 1024 in one pass; larger n loops
+    const int nvec = (n + 3) >> 2;
+    for (int v0 = 0; v0 < nvec; v0 += 32 * kVecPerLane) {
+        uint2 r[kVecPerLane], d[kVecPerLane];
+        uint16_t nx[kVecPerLane];
+#pragma unroll
+        for (int u = 0; u < kVecPerLane; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nvec) {
+                r[u] = __ldcg(reinterpret_cast<const uint2*>(src) + v);
+                d[u] = (dep == src) ? r[u] : __ldcg(reinterpret_cast<const uint2*>(dep) + v);
+                const int k = 4 * v + 4;
+                nx[u] = __ldcg(dep + (k < n ? k : 0));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kVecPerLane; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v >= nvec) break;
+            if (improved) reinterpret_cast<uint2*>(S.gb_route)[v] = r[u];   // gb <- ib (padding ok: ld >= 4*nvec)
+            const uint16_t c[5] = {(uint16_t)(d[u].x & 0xFFFFu), (uint16_t)(d[u].x >> 16),
+                                   (uint16_t)(d[u].y & 0xFFFFu), (uint16_t)(d[u].y >> 16), nx[u]};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k = 4 * v + e;
+                if (k >= n) break;
+                const uint16_t i = c[e];
+                const uint16_t j = (k + 1 < n) ? ((e < 3) ? c[e + 1] : c[4]) : nx[u];
+                S.succ[i] = j;
+                S.pred[j] = i;
+            }
+        }
     }
-    __syncthreads();
-    const uint16_t* dep = S.deposit_global ? S.gb_route : S.ib_route;
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        const uint16_t i = dep[k];
-        const uint16_t j = dep[(k + 1 < n) ? k + 1 : 0];
-        S.succ[i] = j;
-        S.pred[j] = i;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && !S.records) *S.local_key = ~0ull;
 }
+
+__global__ void select_best_kernel(SelectArgs S) {
+    if (threadIdx.x < 32) select_best_warp(S, threadIdx.x);
+}
+
+struct ConstructArgs {
+    const double2* __restrict__ xy;
+    const float* __restrict__ inv_w;        // n x ld
+    const uint16_t* __restrict__ cand_id;   // n x cl
+    const float* __restrict__ cand_inv;     // n x cl, = inv_w[i][cand_id[i][k]]
+    const uint32_t* __restrict__ iter_dev;  // global iteration counter (R20)
+    PhiloxKey key;
+    int n, ld, cl, ldr;
+    int ant_lo, m_local;
+    int fallback_argmax;
+    int warps_per_block;
+    uint32_t table_bytes_inv, table_bytes_id;  // smem-table variant: padded table sizes
+    uint16_t* __restrict__ routes;          // m_local x ldr
+    long long* __restrict__ lengths;        // m_local
+    unsigned long long* __restrict__ best_key;       // local min (len << 24 | ant)
+    unsigned long long* __restrict__ fallback_count;
+    // world == 1: the last warp to finish runs the iteration-best selection (row a5)
+    int fuse_select;
+    unsigned int* done;          // ants finished this launch (reset by the last warp)
+    SelectArgs sel;
+};
+
+}  // namespace mmas
+
+#include "construct.cuh"
+
+namespace mmas {
 
 // world > 1: copy this shard's best route into its exchange record.
 __global__ void publish_kernel(unsigned long long* local_key, const uint16_t* routes, int ldr, int ant_lo, int n,
@@ -196,35 +231,51 @@ struct UpdateArgs {
 };
 
 __global__ void __launch_bounds__(256) pheromone_update_kernel(UpdateArgs U) {
+    extern __shared__ __align__(16) float s_row[];   // new inv_w row (cl > 0: for the gather)
     const float tmin = U.scal[0], tmax = U.scal[1], delta = U.scal[2];
+    const int n4 = (U.n + 3) >> 2;
     for (int i = blockIdx.x; i < U.n; i += gridDim.x) {
         const int si = U.succ[i], pi = U.pred[i];
         float4* trow = reinterpret_cast<float4*>(U.tau + (size_t)i * U.ld);
         float4* wrow = reinterpret_cast<float4*>(U.inv_w + (size_t)i * U.ld);
         const float4* hrow = reinterpret_cast<const float4*>(U.heur + (size_t)i * U.ld);
-        const int n4 = (U.n + 3) >> 2;
-        for (int q = threadIdx.x; q < n4; q += blockDim.x) {
-            const float4 t = trow[q];
-            const float4 h = __ldg(hrow + q);
-            float tv[4] = {t.x, t.y, t.z, t.w};
-            const float hv[4] = {h.x, h.y, h.z, h.w};
-            float wv[4];
+        // up to 4 float4 per thread in flight: all loads first, then compute + store
+        for (int q0 = threadIdx.x; q0 < n4; q0 += 4 * blockDim.x) {
+            float4 t[4], h[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int c = 4 * q + j;
-                float v = fmaxf(__fmul_rn(U.rho_f, tv[j]), tmin);
-                if (c == si || c == pi) v = __fadd_rn(v, delta);
-                v = fminf(v, tmax);
-                tv[j] = v;
-                wv[j] = inv_weight(v, hv[j], U.alpha);
+            for (int u = 0; u < 4; ++u) {
+                const int q = q0 + u * blockDim.x;
+                if (q < n4) {
+                    t[u] = trow[q];
+                    h[u] = __ldg(hrow + q);
+                }
             }
-            trow[q] = make_float4(tv[0], tv[1], tv[2], tv[3]);
-            wrow[q] = make_float4(wv[0], wv[1], wv[2], wv[3]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = q0 + u * blockDim.x;
+                if (q >= n4) break;
+                float tv[4] = {t[u].x, t[u].y, t[u].z, t[u].w};
+                const float hv[4] = {h[u].x, h[u].y, h[u].z, h[u].w};
+                float wv[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int c = 4 * q + j;
+                    float v = fmaxf(__fmul_rn(U.rho_f, tv[j]), tmin);
+                    if (c == si || c == pi) v = __fadd_rn(v, delta);
+                    v = fminf(v, tmax);
+                    tv[j] = v;
+                    wv[j] = inv_weight(v, hv[j], U.alpha);
+                }
+                trow[q] = make_float4(tv[0], tv[1], tv[2], tv[3]);
+                const float4 w4 = make_float4(wv[0], wv[1], wv[2], wv[3]);
+                wrow[q] = w4;
+                if (U.cl > 0) reinterpret_cast<float4*>(s_row)[q] = w4;
+            }
         }
         if (U.cl > 0) {
             __syncthreads();
             for (int k = threadIdx.x; k < U.cl; k += blockDim.x)
-                U.cand_inv[(size_t)i * U.cl + k] = U.inv_w[(size_t)i * U.ld + U.cand_id[(size_t)i * U.cl + k]];
+                U.cand_inv[(size_t)i * U.cl + k] = s_row[U.cand_id[(size_t)i * U.cl + k]];
             __syncthreads();
         }
     }

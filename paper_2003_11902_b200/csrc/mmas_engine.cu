@@ -126,6 +126,7 @@ struct mmas_ctx {
     float* scal = nullptr;        // tau_min, tau_max, delta
     uint32_t* iter_dev = nullptr;
     unsigned char* local_record = nullptr;  // world == 1 path of mmas_construct/mmas_update
+    unsigned int* done = nullptr;           // fused select: ants finished in the running launch
 
     // launch plan for construction
     bool smem_table = false;
@@ -193,8 +194,35 @@ struct PhaseScope {
     }
 };
 
-ConstructArgs construct_args(mmas_ctx* h) {
+SelectArgs select_args(mmas_ctx* h, const unsigned char* records, int count) {
+    SelectArgs S{};
+    S.records = records;
+    S.count = count;
+    S.rec_bytes = h->rec_bytes;
+    S.local_key = h->best_key;
+    S.routes = h->routes;
+    S.ldr = h->ldr;
+    S.ant_lo = h->ant_lo;
+    S.n = h->n;
+    S.rho = h->cfg.rho;
+    S.factor = h->factor;
+    S.deposit_global = h->cfg.deposit == MMAS_DEPOSIT_GLOBAL_BEST;
+    S.ib_route = h->ib_route;
+    S.gb_route = h->gb_route;
+    S.gb_len = h->gb_len;
+    S.ib_len = h->ib_len;
+    S.ib_ant = h->ib_ant;
+    S.scal = h->scal;
+    S.succ = h->succ;
+    S.pred = h->pred;
+    return S;
+}
+
+ConstructArgs construct_args(mmas_ctx* h, bool fuse_select) {
     ConstructArgs A{};
+    A.fuse_select = fuse_select ? 1 : 0;
+    A.done = h->done;
+    A.sel = select_args(h, nullptr, 1);
     A.xy = h->xy;
     A.inv_w = h->inv_w;
     A.cand_id = h->cand_id;
@@ -256,10 +284,10 @@ void set_cl_attrs(size_t bytes) {
     set_smem_attr<4, true, R>(bytes); set_smem_attr<4, false, R>(bytes);
 }
 
-int launch_construct(mmas_ctx* h) {
+int launch_construct(mmas_ctx* h, bool fuse_select) {
     if (h->m_local == 0) return MMAS_OK;
     PhaseScope ps(h, 0);
-    ConstructArgs A = construct_args(h);
+    ConstructArgs A = construct_args(h, fuse_select);
     if (h->cl == 0) {
         if (h->reg_tabu)
             construct_full_kernel<true><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
@@ -277,27 +305,7 @@ int launch_construct(mmas_ctx* h) {
 
 int launch_select(mmas_ctx* h, const unsigned char* records, int count) {
     PhaseScope ps(h, 1);
-    SelectArgs S{};
-    S.records = records;
-    S.count = count;
-    S.rec_bytes = h->rec_bytes;
-    S.local_key = h->best_key;
-    S.routes = h->routes;
-    S.ldr = h->ldr;
-    S.ant_lo = h->ant_lo;
-    S.n = h->n;
-    S.rho = h->cfg.rho;
-    S.factor = h->factor;
-    S.deposit_global = h->cfg.deposit == MMAS_DEPOSIT_GLOBAL_BEST;
-    S.ib_route = h->ib_route;
-    S.gb_route = h->gb_route;
-    S.gb_len = h->gb_len;
-    S.ib_len = h->ib_len;
-    S.ib_ant = h->ib_ant;
-    S.scal = h->scal;
-    S.succ = h->succ;
-    S.pred = h->pred;
-    select_best_kernel<<<1, 1024, 0, h->stream>>>(S);
+    select_best_kernel<<<1, 32, 0, h->stream>>>(select_args(h, records, count));
     h->launches++;
     CU(cudaGetLastError());
     return MMAS_OK;
@@ -320,8 +328,9 @@ int launch_update(mmas_ctx* h) {
     U.cand_inv = h->cand_inv;
     U.cl = h->cl;
     U.iter_dev = h->iter_dev;
-    const int threads = h->n >= 1024 ? 256 : 128;
-    pheromone_update_kernel<<<h->n, threads, 0, h->stream>>>(U);
+    const int threads = 256;
+    const size_t smem = h->cl > 0 ? sizeof(float) * (size_t)h->ld : 0;
+    pheromone_update_kernel<<<h->n, threads, smem, h->stream>>>(U);
     h->launches++;
     CU(cudaGetLastError());
     return MMAS_OK;
@@ -333,7 +342,7 @@ void free_ctx(mmas_ctx* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     void* ptrs[] = {h->xy, h->heur, h->tau, h->inv_w, h->cand_inv, h->cand_id, h->routes, h->lengths,
                     h->best_key, h->fallback_count, h->ib_route, h->gb_route, h->succ, h->pred, h->gb_len,
-                    h->ib_len, h->ib_ant, h->scal, h->iter_dev, h->local_record};
+                    h->ib_len, h->ib_ant, h->scal, h->iter_dev, h->local_record, h->done};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
@@ -380,10 +389,11 @@ int setup(mmas_ctx* h) {
         (st = dalloc(&h->cand_id, (size_t)n * h->cl + 64)) ||
         (st = dalloc(&h->routes, (size_t)std::max(h->m_local, 1) * h->ldr)) ||
         (st = dalloc(&h->lengths, (size_t)std::max(h->m_local, 1))) || (st = dalloc(&h->best_key, 1)) ||
-        (st = dalloc(&h->fallback_count, 1)) || (st = dalloc(&h->ib_route, n)) || (st = dalloc(&h->gb_route, n)) ||
+        (st = dalloc(&h->fallback_count, 1)) || (st = dalloc(&h->ib_route, n)) || (st = dalloc(&h->gb_route, (size_t)h->ldr)) ||
         (st = dalloc(&h->succ, n)) || (st = dalloc(&h->pred, n)) || (st = dalloc(&h->gb_len, 1)) ||
         (st = dalloc(&h->ib_len, 1)) || (st = dalloc(&h->ib_ant, 1)) || (st = dalloc(&h->scal, 4)) ||
-        (st = dalloc(&h->iter_dev, 1)) || (st = dalloc(&h->local_record, (size_t)h->rec_bytes)))
+        (st = dalloc(&h->iter_dev, 1)) || (st = dalloc(&h->local_record, (size_t)h->rec_bytes)) ||
+        (st = dalloc(&h->done, 1)))
         return st;
 
     CU(cudaMemcpyAsync(h->xy, c.coords, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, h->stream));
@@ -394,6 +404,7 @@ int setup(mmas_ctx* h) {
     CU(cudaMemsetAsync(h->gb_len, 0xFF, sizeof(long long), h->stream));   // -1: empty
     CU(cudaMemsetAsync(h->ib_len, 0xFF, sizeof(long long), h->stream));
     CU(cudaMemsetAsync(h->iter_dev, 0, sizeof(uint32_t), h->stream));
+    CU(cudaMemsetAsync(h->done, 0, sizeof(unsigned int), h->stream));
     CU(cudaMemsetAsync(h->succ, 0, sizeof(uint16_t) * n, h->stream));
     CU(cudaMemsetAsync(h->pred, 0, sizeof(uint16_t) * n, h->stream));
 
@@ -478,6 +489,8 @@ int setup(mmas_ctx* h) {
         cudaFuncSetAttribute(construct_full_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->cons_smem);
         cudaFuncSetAttribute(construct_full_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->cons_smem);
     }
+    cudaFuncSetAttribute(pheromone_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(float) * (size_t)h->ld));
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(h->stream));
     return MMAS_OK;
@@ -583,7 +596,7 @@ int mmas_construct(mmas_ctx* h, void* record_dev) {
     if (st) return st;
     if (!record_dev) return fail(MMAS_EINVAL, "record_dev is NULL");
     CU(cudaSetDevice(h->device));
-    if ((st = launch_construct(h))) return st;
+    if ((st = launch_construct(h, false))) return st;
     if (h->m_local > 0) {
         publish_kernel<<<1, 256, 0, h->stream>>>(h->best_key, h->routes, h->ldr, h->ant_lo, h->n,
                                                  (unsigned char*)record_dev);
@@ -615,8 +628,7 @@ int mmas_iterate(mmas_ctx* h, int32_t iters) {
     if (h->cfg.world != 1) return fail(MMAS_ESTATE, "mmas_iterate needs world == 1; use mmas_construct/mmas_update");
     CU(cudaSetDevice(h->device));
     for (int k = 0; k < iters; ++k) {
-        if ((st = launch_construct(h))) return st;
-        if ((st = launch_select(h, nullptr, 1))) return st;
+        if ((st = launch_construct(h, true))) return st;   // + fused iteration-best selection
         if ((st = launch_update(h))) return st;
         h->iteration++;
         if (h->profiling) h->acc_iters++;
@@ -636,6 +648,17 @@ int64_t mmas_best_tour(mmas_ctx* h, int32_t* tour_out) {
     CU(cudaStreamSynchronize(h->stream));
     if (len < 0) return fail(MMAS_ESTATE, "no global best yet (run at least one iteration)");
     for (int i = 0; i < h->n; ++i) tour_out[i] = r[i];
+    return len;
+}
+
+int64_t mmas_best_length(mmas_ctx* h) {
+    int st = check(h);
+    if (st) return st;
+    CU(cudaSetDevice(h->device));
+    long long len = -1;
+    CU(cudaMemcpyAsync(&len, h->gb_len, sizeof(len), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    if (len < 0) return fail(MMAS_ESTATE, "no global best yet (run at least one iteration)");
     return len;
 }
 

@@ -21,7 +21,7 @@ FALLBACK_WRS, FALLBACK_ARGMAX = 0, 1
 # every symbol include/mmas.h declares (checked by tests/test_capi.py)
 EXPORTED = (
     "mmas_last_error", "mmas_config_init", "mmas_create", "mmas_create_ex", "mmas_iterate",
-    "mmas_record_bytes", "mmas_construct", "mmas_update", "mmas_best_tour", "mmas_destroy",
+    "mmas_record_bytes", "mmas_construct", "mmas_update", "mmas_best_tour", "mmas_best_length", "mmas_destroy",
     "mmas_n", "mmas_iteration", "mmas_get_tours", "mmas_get_lengths", "mmas_get_pheromone",
     "mmas_get_inv_w", "mmas_get_heuristic", "mmas_get_candidates", "mmas_get_limits",
     "mmas_get_stats", "mmas_profile", "mmas_get_phase_times", "mmas_kernel_launches",
@@ -82,6 +82,8 @@ def lib():
     L.mmas_update.argtypes = [V, V, ctypes.c_int32]
     L.mmas_best_tour.argtypes = [V, P(ctypes.c_int32)]
     L.mmas_best_tour.restype = ctypes.c_int64
+    L.mmas_best_length.argtypes = [V]
+    L.mmas_best_length.restype = ctypes.c_int64
     L.mmas_destroy.argtypes = [V]
     L.mmas_destroy.restype = None
     L.mmas_n.argtypes = [V]
@@ -189,6 +191,13 @@ class Colony:
             return None, None
         _err(L)
         return out, int(L)
+
+    def best_length(self):
+        """Global best length only (synchronises; 8-byte read-back), None before iteration 1."""
+        L = lib().mmas_best_length(self._h)
+        if L == MMAS_ESTATE:
+            return None
+        return int(_err(L))
 
     # -- introspection --
     @property
