@@ -328,31 +328,43 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
         float Ln[kSlots][4];
         // next group's random keys, one slice per step: Philox rounds 0-4, 5-9, then the
         // logs of words 0-1 and 2-3 (off the dependency chain; R13)
-        auto slice = [&](auto J) {
+        // Each slice is split in two halves (A, B): the step places A behind its table loads
+        // and B behind its tabu shuffle, so the in-order issue fills both latency bubbles.
+        auto slice_half = [&](auto J, auto H) {
             constexpr int j = decltype(J)::value;
+            constexpr int h = decltype(H)::value;
 #pragma unroll
             for (int q = 0; q < kSlots; ++q) {
-                if (j == 0) philox_rounds<0, 5>(nx[q], rk);
-                if (j == 1) philox_rounds<5, 10>(nx[q], rk);
-                if (j == 2) {
-                    Ln[q][0] = det_log2(uniform_open(nx[q].x));
-                    Ln[q][1] = det_log2(uniform_open(nx[q].y));
-                }
-                if (j == 3) {
-                    Ln[q][2] = det_log2(uniform_open(nx[q].z));
-                    Ln[q][3] = det_log2(uniform_open(nx[q].w));
-                }
+                if (j == 0 && h == 0) philox_rounds<0, 3>(nx[q], rk);
+                if (j == 0 && h == 1) philox_rounds<3, 5>(nx[q], rk);
+                if (j == 1 && h == 0) philox_rounds<5, 8>(nx[q], rk);
+                if (j == 1 && h == 1) philox_rounds<8, 10>(nx[q], rk);
+                if (j == 2 && h == 0) Ln[q][0] = det_log2(uniform_open(nx[q].x));
+                if (j == 2 && h == 1) Ln[q][1] = det_log2(uniform_open(nx[q].y));
+                if (j == 3 && h == 0) Ln[q][2] = det_log2(uniform_open(nx[q].z));
+                if (j == 3 && h == 1) Ln[q][3] = det_log2(uniform_open(nx[q].w));
             }
         };
-        // step s (word j = s & 3 of the slot uniforms): WRS over the unvisited candidates of
-        // cur (Alg. 3)
-        auto step = [&](auto J, int s) {
-            constexpr int j = decltype(J)::value;
-            uint32_t bm = kNone, bc = kNone;
+        using H0 = std::integral_constant<int, 0>;
+        using H1 = std::integral_constant<int, 1>;
+        using I0 = std::integral_constant<int, 0>;
+        using I1 = std::integral_constant<int, 1>;
+        using I2 = std::integral_constant<int, 2>;
+        using I3 = std::integral_constant<int, 3>;
+        auto slice = [&](auto J) {
+            slice_half(J, H0{});
+            slice_half(J, H1{});
+        };
+        // Candidate evaluation of the current step (Alg. 3) with the slot key
+        // factors Lv: per-lane (value, city) for the warp argmax.  hook_a / hook_b run
+        // independent work behind the table loads / the tabu shuffle.
+        auto evaluate = [&](const float (&Lv)[kSlots], auto hook_a, auto hook_b, uint32_t& bm, uint32_t& bc) {
+            bm = kNone;
+            bc = kNone;
             if constexpr (kFull32) {
-                // cl == 32: lane k owns slot k.  Shortest chain: one IMAD per address, the
-                // tabu bit shifted to bit 31 and merged with the key magnitude by one LOP3
-                // (a visited lane's value has bit 31 set, so it loses to every unvisited one).
+                // cl == 32: lane k owns slot k.  One IMAD per address; the tabu bit is shifted
+                // to bit 31 and merged with the key magnitude (a visited lane's value has bit 31
+                // set, so it loses to every unvisited one).
                 uint32_t c;
                 float iv;
                 if (kSmemTable) {
@@ -362,50 +374,86 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
                     c = __ldg(A.cand_id + cur * 32u + lane);
                     iv = __ldg(A.cand_inv + cur * 32u + lane);
                 }
+                hook_a();
                 const uint32_t t = tabu.top_bit(c);
-                bm = (__float_as_uint(__fmul_rn(L[0][j], iv)) & 0x7FFFFFFFu) | (t & 0x80000000u);
+                hook_b();
+                bm = (__float_as_uint(__fmul_rn(Lv[0], iv)) & 0x7FFFFFFFu) | (t & 0x80000000u);
                 bc = c;
             } else {
+                hook_a();
+                hook_b();
 #pragma unroll
-            for (int q = 0; q < kSlots; ++q) {
-                const int slot = lane + 32 * q;
-                const bool has = slot < cl;
-                const int idx = (int)cur * cl + (has ? slot : 0);
-                uint32_t c;
-                float iv;
-                if (kSmemTable) {
-                    c = lds_u16(s_id + 2u * (uint32_t)idx);
-                    iv = lds_f32(s_inv + 4u * (uint32_t)idx);
-                } else {
-                    c = __ldg(A.cand_id + idx);
-                    iv = __ldg(A.cand_inv + idx);
-                }
-                const bool vis = tabu.visited(has ? c : cur);
-                const uint32_t mag = vis ? kNone : key_magnitude(__fmul_rn(L[q][j], iv));
-                if (kSlots == 1) {
-                    bm = mag;
-                    bc = c;
-                } else if (mag < bm || (mag == bm && c < bc)) {
-                    bm = mag;
-                    bc = c;
+                for (int q = 0; q < kSlots; ++q) {
+                    const int slot = lane + 32 * q;
+                    const bool has = slot < cl;
+                    const int idx = (int)cur * cl + (has ? slot : 0);
+                    uint32_t c;
+                    float iv;
+                    if (kSmemTable) {
+                        c = lds_u16(s_id + 2u * (uint32_t)idx);
+                        iv = lds_f32(s_inv + 4u * (uint32_t)idx);
+                    } else {
+                        c = __ldg(A.cand_id + idx);
+                        iv = __ldg(A.cand_inv + idx);
+                    }
+                    const bool vis = tabu.visited(has ? c : cur);
+                    const uint32_t mag = vis ? 0x80000000u : key_magnitude(__fmul_rn(Lv[q], iv));
+                    if (mag < bm || (mag == bm && c < bc)) {
+                        bm = mag;
+                        bc = c;
+                    }
                 }
             }
-            }
-            // argmax (ties -> lowest city id, R16): both reductions back to back; a best
-            // value with bit 31 set means no unvisited candidate
-            const uint32_t best = __reduce_min_sync(kFull, bm);
-            uint32_t nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
-            if (__builtin_expect(best >= 0x80000000u, 0)) {   // every candidate visited: R9 fallback (row a3)
-                ++fb;
-                const float* row = A.inv_w + (size_t)cur * A.ld;
-                nxt = A.fallback_argmax
-                          ? fallback_select<true>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane)
-                          : fallback_select<false>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane);
-            }
+        };
+        auto commit = [&](uint32_t nxt, int s) {
             tabu.mark(nxt, lane);
             stage_route(route, s, nxt, lane, stage);
             tabu.sync();
             cur = nxt;
+        };
+        // FAST step (compile-time j): returns true, without choosing, when every candidate is
+        // visited; the generic path below then redoes the step with the fallback scan
+        auto fast_step = [&](auto J, int s) -> bool {
+            constexpr int j = decltype(J)::value;
+            float Lv[kSlots];
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q) Lv[q] = L[q][j];
+            uint32_t bm, bc;
+            evaluate(Lv, [&] { slice_half(J, H0{}); }, [&] { slice_half(J, H1{}); }, bm, bc);
+            // argmax (ties -> lowest city id, R16): both reductions back to back
+            const uint32_t best = __reduce_min_sync(kFull, bm);
+            const uint32_t nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
+            if (__builtin_expect(best >= 0x80000000u, 0)) return true;
+            commit(nxt, s);
+            return false;
+        };
+        // GENERIC step (runtime j): guards, and the R9 fallback (row a3) inlined ONCE
+        auto generic_step = [&](int j, int s) {
+            float Lv[kSlots];
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q)
+                Lv[q] = j == 0 ? L[q][0] : j == 1 ? L[q][1] : j == 2 ? L[q][2] : L[q][3];
+            uint32_t bm, bc;
+            evaluate(Lv, [] {}, [] {}, bm, bc);
+            const uint32_t best = __reduce_min_sync(kFull, bm);
+            uint32_t nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
+            if (best >= 0x80000000u) {   // every candidate visited: R9 fallback
+                ++fb;
+                const float* row = A.inv_w + (size_t)cur * A.ld;
+                uint32_t fm = kNone, fc = kNone;
+                if (A.fallback_argmax)
+                    scan_unvisited<true>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm, fc);
+                else
+                    scan_unvisited<false>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm, fc);
+                nxt = warp_select(fm, fc);
+            }
+            commit(nxt, s);
+        };
+        auto slice_rt = [&](int j) {
+            if (j == 0) slice(I0{});
+            else if (j == 1) slice(I1{});
+            else if (j == 2) slice(I2{});
+            else slice(I3{});
         };
         auto next_group = [&](int g) {
 #pragma unroll
@@ -417,42 +465,41 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) L[q][j] = Ln[q][j];
         };
-        using I0 = std::integral_constant<int, 0>;
-        using I1 = std::integral_constant<int, 1>;
-        using I2 = std::integral_constant<int, 2>;
-        using I3 = std::integral_constant<int, 3>;
-        // a group with per-step guards (group 0 holds s = 0, the last group may be ragged)
-        auto guarded_group = [&](int g, bool pipeline) {
-            if (pipeline) next_group(g);
-            if (pipeline) slice(I0{});
-            if (4 * g + 0 > 0 && 4 * g + 0 < n) step(I0{}, 4 * g + 0);
-            if (pipeline) slice(I1{});
-            if (4 * g + 1 < n) step(I1{}, 4 * g + 1);
-            if (pipeline) slice(I2{});
-            if (4 * g + 2 < n) step(I2{}, 4 * g + 2);
-            if (pipeline) slice(I3{});
-            if (4 * g + 3 < n) step(I3{}, 4 * g + 3);
-            if (pipeline) rotate();
-        };
         const int n_groups = (n + 3) / 4;      // groups holding a step s < n
         const int n_full = n / 4;              // groups g < n_full have all four steps < n
-        guarded_group(0, n_groups > 1);
-        // full groups: no guard between a Philox slice and the step it overlaps, so each
-        // slice and its step's dependency chain share one basic block for the scheduler
-        int g = 1;
-        for (; g < n_full && g < n_groups - 1; ++g) {
-            next_group(g);
-            slice(I0{});
-            step(I0{}, 4 * g + 0);
-            slice(I1{});
-            step(I1{}, 4 * g + 1);
-            slice(I2{});
-            step(I2{}, 4 * g + 2);
-            slice(I3{});
-            step(I3{}, 4 * g + 3);
-            rotate();
+        // Groups 1 .. n_full-1 (all four steps real, a next group to prepare) run the FAST
+        // path: four straight-line steps with no branch but the fallback exit.  Group 0
+        // (s = 0), the ragged tail, and the rest of a group whose fast path hit a fallback
+        // run the GENERIC path, which appears once in the loop body.
+        int g = 0;
+        while (g < n_groups) {
+            const bool pipeline = g + 1 < n_groups;
+            int j0 = 0;
+            bool sliced_j0 = false;
+            if (pipeline) next_group(g);
+            if (g >= 1 && g < n_full && pipeline) {
+                int jf = -1;
+                if (fast_step(I0{}, 4 * g + 0)) jf = 0;
+                else if (fast_step(I1{}, 4 * g + 1)) jf = 1;
+                else if (fast_step(I2{}, 4 * g + 2)) jf = 2;
+                else if (fast_step(I3{}, 4 * g + 3)) jf = 3;
+                if (jf < 0) {
+                    rotate();
+                    ++g;
+                    continue;
+                }
+                j0 = jf;
+                sliced_j0 = true;   // that step's slices ran inside its fast attempt
+            }
+#pragma unroll 1
+            for (int j = j0; j < 4; ++j) {
+                if (pipeline && !(j == j0 && sliced_j0)) slice_rt(j);
+                const int s = 4 * g + j;
+                if (s > 0 && s < n) generic_step(j, s);
+            }
+            if (pipeline) rotate();
+            ++g;
         }
-        for (; g < n_groups; ++g) guarded_group(g, g + 1 < n_groups);
         flush_route(route, n, lane, stage);
         __syncwarp();
         wbest = min(wbest, finish_ant(A, route, al, ant, lane));

@@ -188,6 +188,7 @@ struct ConstructArgs {
 }  // namespace mmas
 
 #include "construct.cuh"
+#include "construct_ws.cuh"
 
 namespace mmas {
 
