@@ -88,6 +88,10 @@ def lib():
                          ("orc_get_inv_w", ctypes.c_float), ("orc_get_heur", ctypes.c_float),
                          ("orc_get_cand", ctypes.c_int32)):
             getattr(L, name).argtypes = [ctypes.c_void_p, P(ct)]
+        L.orc_reverse.argtypes = [P(ctypes.c_int32), P(ctypes.c_int32), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+        L.orc_two_opt.argtypes = [P(ctypes.c_double), ctypes.c_int32, P(ctypes.c_int32), ctypes.c_int32,
+                                  P(ctypes.c_int32), P(ctypes.c_int64)]
+        L.orc_two_opt.restype = ctypes.c_int64
         L.orc_construct_ant.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_int32), P(ctypes.c_int64)]
         L.orc_construct_ant.restype = ctypes.c_int64
         L.orc_best_tour.argtypes = [ctypes.c_void_p, P(ctypes.c_int32)]
@@ -175,6 +179,29 @@ def inv_w(tau: float, heur: float, alpha: int = 1) -> float:
 
 def heur(d: int, beta: float = 2.0) -> float:
     return lib().orc_heur(d, beta)
+
+
+def reverse(route, i, j):
+    """The 2-opt segment reversal (R25) on a copy of `route`."""
+    r = np.array(route, dtype=np.int32, copy=True)
+    pos = np.zeros(len(r), dtype=np.int32)
+    pos[r] = np.arange(len(r), dtype=np.int32)
+    lib().orc_reverse(_ptr(r, ctypes.c_int32), _ptr(pos, ctypes.c_int32), len(r), i, j)
+    return r, pos
+
+
+def two_opt(coords, route, K=32):
+    """2-opt with neighbour lists and a FIFO of active nodes (row a8, R25).
+    Returns (new_route, length_delta, moves)."""
+    c = np.ascontiguousarray(coords, dtype=np.float64).ravel()
+    n = len(c) // 2
+    K = min(K, n - 1)
+    nn = cand_lists(coords, K)
+    r = np.array(route, dtype=np.int32, copy=True)
+    moves = ctypes.c_int64()
+    d = lib().orc_two_opt(_ptr(c, ctypes.c_double), n, _ptr(nn, ctypes.c_int32), K, _ptr(r, ctypes.c_int32),
+                          ctypes.byref(moves))
+    return r, int(d), moves.value
 
 
 def select_next(inv_w_row, cand_row, visited, s, a, it, seed, fallback_argmax=0):

@@ -196,7 +196,7 @@ typedef struct {
     uint64_t seed;
     int32_t deposit_global;   /* R7: 0 = iteration best (Alg. 1), 1 = global best */
     int32_t fallback_argmax;  /* R9: 0 = WRS over all unvisited (default), 1 = argmax weight */
-    int32_t local_search;     /* a8: 2-opt (not built in this oracle yet: must be 0) */
+    int32_t local_search;     /* a8: 2-opt on every route (R25) */
     int32_t nthreads;
 } orc_params;
 
@@ -205,6 +205,8 @@ typedef struct {
     double *xy;
     float *heur, *tau, *inv_w;          /* n x n row-major */
     int32_t *cand;                      /* n x cl */
+    int32_t *ls_nn;                     /* n x ls_k: 2-opt neighbour lists (R25) */
+    int32_t ls_k;
     int32_t *routes;                    /* m x n, last iteration */
     int64_t *lengths;                   /* m */
     int64_t *fallbacks;                 /* m: fallback steps of each ant, last iteration */
@@ -265,7 +267,7 @@ static void recompute_inv_w(orc_t *o)
 ORC_EXPORT void orc_destroy(orc_t *o)
 {
     if (!o) return;
-    free(o->xy); free(o->heur); free(o->tau); free(o->inv_w); free(o->cand);
+    free(o->xy); free(o->heur); free(o->tau); free(o->inv_w); free(o->cand); free(o->ls_nn);
     free(o->routes); free(o->lengths); free(o->fallbacks);
     free(o->gb_route); free(o->ib_route);
     free(o);
@@ -277,7 +279,6 @@ ORC_EXPORT orc_t *orc_create(const orc_params *p, const double *coords)
     if (!(p->rho > 0.0 && p->rho < 1.0)) return NULL;
     if (!is_int_in(p->alpha, 0, 8) || p->beta < 0.0) return NULL;
     if (!(p->p_best > 0.0 && p->p_best < 1.0)) return NULL;
-    if (p->local_search) return NULL;
     for (int32_t i = 0; i < 2 * p->n; ++i)
         if (!isfinite(coords[i])) return NULL;
 
@@ -308,6 +309,12 @@ ORC_EXPORT orc_t *orc_create(const orc_params *p, const double *coords)
         for (int32_t j = 0; j < n; ++j)
             o->heur[(size_t)i * n + j] = orc_heur(orc_dist(o->xy, i, j), p->beta);
     if (p->cl > 0) orc_cand_lists(o->xy, n, p->cl, o->cand);
+    if (p->local_search) {
+        /* the 2-opt search is limited to the 32 nearest neighbours */
+        o->ls_k = n - 1 < 32 ? n - 1 : 32;
+        o->ls_nn = malloc(sizeof(int32_t) * (size_t)n * o->ls_k);
+        orc_cand_lists(o->xy, n, o->ls_k, o->ls_nn);
+    }
 
     /* Alg. 1: limits from the NN solution, tau := tau_max. */
     int32_t *nn_route = malloc(sizeof(int32_t) * n);
@@ -392,6 +399,109 @@ typedef struct {
     int32_t a0, a1;
 } orc_job;
 
+/* ------------------------------------------------------------------------- */
+/* Row a8: 2-opt local search (Sec. 5.7; Bentley 1992), R25:      */
+/*  - neighbour lists: the K = min(32, n-1) nearest nodes by (d, id);          */
+/*  - active nodes in a FIFO queue, initially the route in order; a node is in */
+/*    the queue at most once ("don't-look bit" clear <=> queued);              */
+/*  - for the popped node a: dir = successor, then predecessor; b = dir(a);    */
+/*    for k = 0..K-1: c = nn[a][k]; stop at the first d(a,c) >= d(a,b)        */
+/*    (Bentley's pruning); d = dir(c); skip c == b or d == a;                  */
+/*    gain test  d(a,c) + d(b,d) - d(a,b) - d(c,d) < 0 -> apply the FIRST      */
+/*    improving move, enqueue a, b, c, d (in that order, if not queued), and   */
+/*    go to the next pop;                                                       */
+/*  - a move replaces two edges by (a,c), (b,d): the forward segment between   */
+/*    them is reversed, or its complement when that is strictly shorter;       */
+/*  - "the search is restarted until no further improvements can be found"     */
+/*    (P:1731-1732): when the queue runs empty it is re-seeded with the whole  */
+/*    route (in route order) until a full sweep applies no move, so the result */
+/*    is a local optimum of the neighbour-restricted move set.                 */
+/* ------------------------------------------------------------------------- */
+
+/* Reverse the forward cyclic segment of positions i..j (inclusive); if the
+ * complement is strictly shorter, reverse the complement instead. */
+ORC_EXPORT void orc_reverse(int32_t *route, int32_t *pos, int32_t n, int32_t i, int32_t j)
+{
+    int32_t len = (j - i + n) % n + 1;
+    if (2 * len > n) {                  /* complement (j+1 .. i-1) is strictly shorter */
+        int32_t ni = (j + 1) % n, nj = (i - 1 + n) % n;
+        i = ni;
+        j = nj;
+        len = n - len;
+    }
+    for (int32_t k = 0; k < len / 2; ++k) {
+        int32_t p = (i + k) % n, q = (j - k + n) % n;
+        int32_t t = route[p];
+        route[p] = route[q];
+        route[q] = t;
+        pos[route[p]] = p;
+        pos[route[q]] = q;
+    }
+}
+
+ORC_EXPORT int64_t orc_two_opt(const double *xy, int32_t n, const int32_t *nn, int32_t K, int32_t *route,
+                               int64_t *moves_out)
+{
+    int32_t *pos = malloc(sizeof(int32_t) * (size_t)n);
+    int32_t *queue = malloc(sizeof(int32_t) * (size_t)n);
+    char *inq = malloc((size_t)n);
+    for (int32_t i = 0; i < n; ++i) pos[route[i]] = i;
+    int64_t delta_total = 0, moves = 0, sweep_moves;
+    do {
+        for (int32_t i = 0; i < n; ++i) {     /* (re-)seed: every node, in route order */
+            queue[i] = route[i];
+            inq[route[i]] = 1;
+        }
+        int32_t head = 0, count = n;
+        sweep_moves = 0;
+        while (count > 0) {
+            int32_t a = queue[head];
+            head = (head + 1) % n;
+            --count;
+            inq[a] = 0;
+            int improved = 0;
+            for (int dir = 0; dir < 2 && !improved; ++dir) {       /* 0: successor, 1: predecessor */
+                int32_t pa = pos[a];
+                int32_t b = dir == 0 ? route[(pa + 1) % n] : route[(pa - 1 + n) % n];
+                int64_t dab = orc_dist(xy, a, b);
+                for (int32_t k = 0; k < K; ++k) {
+                    int32_t c = nn[(size_t)a * K + k];
+                    int64_t dac = orc_dist(xy, a, c);
+                    if (dac >= dab) break;
+                    int32_t pc = pos[c];
+                    int32_t d = dir == 0 ? route[(pc + 1) % n] : route[(pc - 1 + n) % n];
+                    if (c == b || d == a) continue;
+                    int64_t delta = dac + orc_dist(xy, b, d) - dab - orc_dist(xy, c, d);
+                    if (delta < 0) {
+                        if (dir == 0)   /* edges (a,b),(c,d) -> (a,c),(b,d): reverse b .. c */
+                            orc_reverse(route, pos, n, pos[b], pos[c]);
+                        else            /* edges (b,a),(d,c) -> (b,d),(a,c): reverse a .. d */
+                            orc_reverse(route, pos, n, pos[a], pos[d]);
+                        int32_t ends[4] = {a, b, c, d};
+                        for (int e = 0; e < 4; ++e) {
+                            if (!inq[ends[e]]) {
+                                queue[(head + count) % n] = ends[e];
+                                ++count;
+                                inq[ends[e]] = 1;
+                            }
+                        }
+                        delta_total += delta;
+                        ++sweep_moves;
+                        improved = 1;
+                        break;
+                    }
+                }
+            }
+        }
+        moves += sweep_moves;
+    } while (sweep_moves > 0);
+    free(pos);
+    free(queue);
+    free(inq);
+    if (moves_out) *moves_out = moves;
+    return delta_total;
+}
+
 /* Alg. 1: ant a builds its route for the current iteration.
  * Returns the number of fallback steps (R9). */
 static int64_t build_route(const orc_t *o, int32_t a, int32_t *route, char *vis)
@@ -412,6 +522,7 @@ static int64_t build_route(const orc_t *o, int32_t a, int32_t *route, char *vis)
         vis[nxt] = 1;
         cur = nxt;
     }
+    if (o->p.local_search) orc_two_opt(o->xy, n, o->ls_nn, o->ls_k, route, NULL);   /* row a8, R26 */
     return fb;
 }
 
