@@ -56,7 +56,7 @@ typedef struct mmas_config {
     double p_best;         /* trail-limit parameter; default 0.01 */
     int32_t deposit;       /* MMAS_DEPOSIT_*; default iteration best */
     int32_t fallback;      /* MMAS_FALLBACK_*; default WRS over all unvisited */
-    int32_t local_search;  /* 2-opt (row a8); must be 0 in this version */
+    int32_t local_search;  /* 1: 2-opt on every route (row a8, Sec. 5.7, R25/R26); default 0 */
     int32_t device;        /* CUDA device ordinal; -1 = current device */
     void *stream;          /* cudaStream_t to run on (see use_caller_stream) */
     int32_t rank, world;   /* ant shard: this context builds global ants [floor(rank*m/world),
@@ -73,6 +73,7 @@ typedef struct mmas_stats {
     int64_t ant_steps;        /* construction steps taken by this shard's ants */
     int32_t ants_local;       /* ants built by this context per iteration */
     int32_t first_ant;        /* global id of the first of them */
+    int64_t local_search_moves; /* improving 2-opt moves applied (row a8), this shard */
 } mmas_stats;
 
 /* Last error message of this thread ("" if none). */
@@ -148,6 +149,7 @@ typedef struct mmas_phase_times {
     double construct_ms;   /* construction kernels (a1-a5 local) */
     double select_ms;      /* iteration/global best + limits (a5) */
     double update_ms;      /* pheromone update kernel (a6) */
+    double local_search_ms; /* 2-opt kernel incl. lengths + best (a8 + a5), local_search only */
     int64_t iterations;    /* iterations accumulated */
 } mmas_phase_times;
 int mmas_profile(mmas_ctx *h, int32_t enable);                   /* resets the accumulators */

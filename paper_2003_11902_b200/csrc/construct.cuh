@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
         }
         flush_route(route, n, lane, stage);
         __syncwarp();
-        wbest = min(wbest, finish_ant(A, route, al, ant, lane));
+        if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane));
         wfb += fb;
     }
     block_finish(A, wbest, wfb, lane, warp);
@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
         }
         flush_route(route, n, lane, stage);
         __syncwarp();
-        wbest = min(wbest, finish_ant(A, route, al, ant, lane));
+        if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane));
     }
     block_finish(A, wbest, 0, lane, warp);
 }

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(512, 1) construct_ws_kernel(ConstructArgs A) {
             if (lane == 0) st_volatile_s32(consumed, vbase + NS);   // the whole ant is consumed
             flush_route(route, n, lane, stage);
             __syncwarp();
-            wbest = min(wbest, finish_ant(A, route, al, ant, lane));
+            if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane));
             wfb += fb;
         }
     }

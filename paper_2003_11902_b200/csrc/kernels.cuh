@@ -181,6 +181,7 @@ struct ConstructArgs {
     unsigned long long* __restrict__ fallback_count;
     // world == 1: the last warp to finish runs the iteration-best selection (row a5)
     int fuse_select;
+    int skip_finish;             // local search follows: lengths / best keys come from two_opt_kernel
     unsigned int* done;          // ants finished this launch (reset by the last warp)
     SelectArgs sel;
 };
@@ -189,6 +190,7 @@ struct ConstructArgs {
 
 #include "construct.cuh"
 #include "construct_ws.cuh"
+#include "two_opt.cuh"
 
 namespace mmas {
 

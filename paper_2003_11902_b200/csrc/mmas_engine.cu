@@ -142,13 +142,20 @@ struct mmas_ctx {
     int32_t iteration = 0;
     int64_t launches = 0;
 
+    // row a8: 2-opt local search (local_search != 0)
+    int ls_k = 0, ls_nwords = 0;
+    uint16_t* ls_nn = nullptr;         // n x ls_k neighbour lists
+    uint16_t *ls_pos = nullptr, *ls_queue = nullptr;
+    uint32_t* ls_inq = nullptr;
+    unsigned long long* ls_moves = nullptr;
+
     // profiling
     bool profiling = false;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     struct Span { cudaEvent_t a, b; int phase; };
     std::vector<Span> spans;
-    double acc_ms[3] = {0, 0, 0};
+    double acc_ms[4] = {0, 0, 0, 0};
     int64_t acc_iters = 0;
 };
 
@@ -220,9 +227,10 @@ SelectArgs select_args(mmas_ctx* h, const unsigned char* records, int count) {
     return S;
 }
 
-ConstructArgs construct_args(mmas_ctx* h, bool fuse_select) {
+ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = false) {
     ConstructArgs A{};
     A.fuse_select = fuse_select ? 1 : 0;
+    A.skip_finish = skip_finish ? 1 : 0;
     A.done = h->done;
     A.sel = select_args(h, nullptr, 1);
     A.xy = h->xy;
@@ -295,8 +303,31 @@ void set_cl_attrs(size_t bytes) {
     set_smem_attr<4, true, R>(bytes); set_smem_attr<4, false, R>(bytes);
 }
 
+int launch_two_opt(mmas_ctx* h, bool fuse_select);
+
+// Construction (rows a1-a4) -- and, with local search on, the 2-opt pass (row a8) that
+// then owns the tour lengths and the iteration-best bookkeeping (row a5).
 int launch_construct(mmas_ctx* h, bool fuse_select) {
     if (h->m_local == 0) return MMAS_OK;
+    if (h->cfg.local_search) {
+        {
+            PhaseScope ps(h, 0);
+            ConstructArgs A = construct_args(h, false, true);
+            if (h->cl == 0) {
+                if (h->reg_tabu)
+                    construct_full_kernel<true><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+                else
+                    construct_full_kernel<false><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+            } else if (h->reg_tabu) {
+                launch_cl_r<true>(h, A);
+            } else {
+                launch_cl_r<false>(h, A);
+            }
+            h->launches++;
+            CU(cudaGetLastError());
+        }
+        return launch_two_opt(h, fuse_select);
+    }
     PhaseScope ps(h, 0);
     ConstructArgs A = construct_args(h, fuse_select);
     if (h->cl == 0) {
@@ -317,6 +348,29 @@ int launch_construct(mmas_ctx* h, bool fuse_select) {
 int launch_select(mmas_ctx* h, const unsigned char* records, int count) {
     PhaseScope ps(h, 1);
     select_best_kernel<<<1, 32, 0, h->stream>>>(select_args(h, records, count));
+    h->launches++;
+    CU(cudaGetLastError());
+    return MMAS_OK;
+}
+
+int launch_two_opt(mmas_ctx* h, bool fuse_select) {
+    PhaseScope ps(h, 3);
+    TwoOptArgs T{};
+    T.xy = h->xy;
+    T.nn = h->ls_nn;
+    T.n = h->n;
+    T.K = h->ls_k;
+    T.ldr = h->ldr;
+    T.m_local = h->m_local;
+    T.warps_per_block = 4;
+    T.nwords = h->ls_nwords;
+    T.routes = h->routes;
+    T.pos = h->ls_pos;
+    T.queue = h->ls_queue;
+    T.inq = h->ls_inq;
+    T.moves = h->ls_moves;
+    const int grid = std::max(1, (h->m_local + 3) / 4);
+    two_opt_kernel<<<grid, 128, 0, h->stream>>>(T, construct_args(h, fuse_select));
     h->launches++;
     CU(cudaGetLastError());
     return MMAS_OK;
@@ -353,7 +407,8 @@ void free_ctx(mmas_ctx* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     void* ptrs[] = {h->xy, h->heur, h->tau, h->inv_w, h->cand_inv, h->cand_id, h->routes, h->lengths,
                     h->best_key, h->fallback_count, h->ib_route, h->gb_route, h->succ, h->pred, h->gb_len,
-                    h->ib_len, h->ib_ant, h->scal, h->iter_dev, h->local_record, h->done};
+                    h->ib_len, h->ib_ant, h->scal, h->iter_dev, h->local_record, h->done,
+                    h->ls_nn, h->ls_pos, h->ls_queue, h->ls_inq, h->ls_moves};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
@@ -445,6 +500,22 @@ int setup(mmas_ctx* h) {
         CU(cudaStreamSynchronize(h->stream));
     }
 
+    // row a8: 2-opt neighbour lists (the 32 nearest) and per-ant scratch
+    if (c.local_search) {
+        h->ls_k = std::min(32, n - 1);
+        h->ls_nwords = (n + 31) / 32;
+        std::vector<uint16_t> nnl;
+        candidate_lists(c.coords, n, h->ls_k, nnl);
+        const size_t ma = (size_t)std::max(h->m_local, 1);
+        if ((st = dalloc(&h->ls_nn, nnl.size())) || (st = dalloc(&h->ls_pos, ma * h->ldr)) ||
+            (st = dalloc(&h->ls_queue, ma * h->ldr)) || (st = dalloc(&h->ls_inq, ma * h->ls_nwords)) ||
+            (st = dalloc(&h->ls_moves, 1)))
+            return st;
+        CU(cudaMemcpyAsync(h->ls_nn, nnl.data(), sizeof(uint16_t) * nnl.size(), cudaMemcpyHostToDevice, h->stream));
+        CU(cudaMemsetAsync(h->ls_moves, 0, sizeof(unsigned long long), h->stream));
+        CU(cudaStreamSynchronize(h->stream));
+    }
+
     // initial limits from the NN tour (Alg. 1); F from libm pow (R2)
     h->nn_len = nn_tour_length(c.coords, n);
     const double pn = std::pow(c.p_best, 1.0 / (double)n);
@@ -526,7 +597,7 @@ int validate(const mmas_config* c) {
         return fail(MMAS_EINVAL, "deposit must be MMAS_DEPOSIT_*");
     if (c->fallback != MMAS_FALLBACK_WRS && c->fallback != MMAS_FALLBACK_ARGMAX)
         return fail(MMAS_EINVAL, "fallback must be MMAS_FALLBACK_*");
-    if (c->local_search != 0) return fail(MMAS_EINVAL, "local_search (2-opt) is not available in this version");
+    if (c->local_search != 0 && c->local_search != 1) return fail(MMAS_EINVAL, "local_search must be 0 or 1");
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(MMAS_EINVAL, "need 0 <= rank < world");
     double lo_x = INFINITY, hi_x = -INFINITY, lo_y = INFINITY, hi_y = -INFINITY;
     for (int i = 0; i < c->n; ++i) {
@@ -760,6 +831,12 @@ int mmas_get_stats(mmas_ctx* h, mmas_stats* out) {
     out->ant_steps = (int64_t)h->iteration * h->m_local * (h->n - 1);
     out->ants_local = h->m_local;
     out->first_ant = h->ant_lo;
+    out->local_search_moves = 0;
+    if (h->ls_moves) {
+        unsigned long long mv = 0;
+        CU(cudaMemcpy(&mv, h->ls_moves, sizeof(mv), cudaMemcpyDeviceToHost));
+        out->local_search_moves = (int64_t)mv;
+    }
     return MMAS_OK;
 }
 
@@ -768,7 +845,7 @@ int mmas_profile(mmas_ctx* h, int32_t enable) {
     if (st) return st;
     drain_spans(h);
     h->profiling = enable != 0;
-    h->acc_ms[0] = h->acc_ms[1] = h->acc_ms[2] = 0.0;
+    h->acc_ms[0] = h->acc_ms[1] = h->acc_ms[2] = h->acc_ms[3] = 0.0;
     h->acc_iters = 0;
     return MMAS_OK;
 }
@@ -782,6 +859,7 @@ int mmas_get_phase_times(mmas_ctx* h, mmas_phase_times* out) {
     out->construct_ms = h->acc_ms[0];
     out->select_ms = h->acc_ms[1];
     out->update_ms = h->acc_ms[2];
+    out->local_search_ms = h->acc_ms[3];
     out->iterations = h->acc_iters;
     return MMAS_OK;
 }

@@ -1,0 +1,161 @@
+// two_opt.cuh -- row a8: 2-opt local search on every ant's route (Sec. 5.7,
+// PAPER.md P:1727-1744; Bentley 1992), written from DESIGN.md R25.
+//
+// One warp per ant.  The paper lets several warps search for an improving pair
+// of edges and "any" that succeeds applies its move; which one wins depends on
+// the schedule, so here the search order is fixed instead (R25): the active
+// nodes form a FIFO queue, and for the popped node a the warp evaluates all of
+// a's neighbour-list moves in both tour directions AT ONCE (lane k = the k-th
+// nearest neighbour c of a), then takes the first improving one in the
+// sequential (direction, k) order with a ballot + find-first-set.  The move is
+// applied by all 32 lanes reversing disjoint position pairs of the shorter side.
+#pragma once
+#include <cstdint>
+
+namespace mmas {
+
+struct TwoOptArgs {
+    const double2* __restrict__ xy;
+    const uint16_t* __restrict__ nn;   // n x K neighbour lists (R10 order)
+    int n, K, ldr, m_local, warps_per_block, nwords;
+    uint16_t* routes;                  // m_local x ldr (in: constructed routes; out: improved)
+    uint16_t* pos;                     // m_local x ldr scratch
+    uint16_t* queue;                   // m_local x ldr scratch
+    uint32_t* inq;                     // m_local x nwords scratch ("don't-look bit" clear <=> queued)
+    unsigned long long* moves;         // total applied moves (stats)
+};
+
+__device__ __forceinline__ int wrap_inc(int i, int n) { return i + 1 == n ? 0 : i + 1; }
+__device__ __forceinline__ int wrap_dec(int i, int n) { return i == 0 ? n - 1 : i - 1; }
+
+// Reverse the forward cyclic segment i..j of the route, or its complement when that is
+// strictly shorter (R25).  Lanes swap disjoint position pairs.
+__device__ __forceinline__ void warp_reverse(uint16_t* route, uint16_t* pos, int n, int i, int j, int lane) {
+    int len = j - i;
+    if (len < 0) len += n;
+    len += 1;
+    if (2 * len > n) {
+        const int ni = wrap_inc(j, n), nj = wrap_dec(i, n);
+        i = ni;
+        j = nj;
+        len = n - len;
+    }
+    for (int k = lane; k < len / 2; k += 32) {
+        int p = i + k;
+        if (p >= n) p -= n;
+        int q = j - k;
+        if (q < 0) q += n;
+        const uint16_t vp = route[p], vq = route[q];
+        route[p] = vq;
+        route[q] = vp;
+        pos[vq] = (uint16_t)p;
+        pos[vp] = (uint16_t)q;
+    }
+    __syncwarp();
+}
+
+// Local search of one route (the whole warp).  Returns the number of applied moves.
+__device__ __forceinline__ long long two_opt_route(const TwoOptArgs& T, uint16_t* route, uint16_t* pos,
+                                                   uint16_t* queue, uint32_t* inq, int lane) {
+    const int n = T.n, K = T.K;
+    for (int i = lane; i < n; i += 32) pos[route[i]] = (uint16_t)i;
+    long long moves = 0, sweep_moves;
+    do {
+        // (re-)seed the queue with every node in route order
+        for (int i = lane; i < n; i += 32) queue[i] = route[i];
+        for (int w = lane; w < T.nwords; w += 32) inq[w] = 0xFFFFFFFFu;
+        __syncwarp();
+        int head = 0, count = n;
+        sweep_moves = 0;
+        while (count > 0) {
+            const int a = queue[head];
+            head = wrap_inc(head, n);
+            --count;
+            if (lane == 0) inq[a >> 5] &= ~(1u << (a & 31));
+            const int pa = pos[a];
+            const int sa = route[wrap_inc(pa, n)];      // successor of a
+            const int pr = route[wrap_dec(pa, n)];      // predecessor of a
+            const double2 xa = __ldg(T.xy + a);
+            const int64_t d_as = euc2d(xa, __ldg(T.xy + sa));
+            const int64_t d_ap = euc2d(xa, __ldg(T.xy + pr));
+            // lane k: the k-th nearest neighbour c of a, in both directions
+            bool imp_s = false, imp_p = false;
+            int c = 0, sc = 0, pc = 0;
+            if (lane < K) {
+                c = T.nn[(size_t)a * K + lane];
+                const double2 xc = __ldg(T.xy + c);
+                const int64_t d_ac = euc2d(xa, xc);
+                const int qc = pos[c];
+                sc = route[wrap_inc(qc, n)];
+                pc = route[wrap_dec(qc, n)];
+                if (d_ac < d_as && c != sa && sc != a)   // Bentley pruning + degenerate moves
+                    imp_s = d_ac + euc2d(__ldg(T.xy + sa), __ldg(T.xy + sc)) - d_as - euc2d(xc, __ldg(T.xy + sc)) < 0;
+                if (d_ac < d_ap && c != pr && pc != a)
+                    imp_p = d_ac + euc2d(__ldg(T.xy + pr), __ldg(T.xy + pc)) - d_ap - euc2d(xc, __ldg(T.xy + pc)) < 0;
+            }
+            // the pruning is a prefix of k (lists are sorted by d(a, .)), so "first improving
+            // in (direction, k) order" is the lowest improving lane of the successor direction,
+            // else of the predecessor direction
+            const uint32_t ms = __ballot_sync(kFull, imp_s);
+            const uint32_t mp = __ballot_sync(kFull, imp_p);
+            if (ms | mp) {
+                const int dir = ms ? 0 : 1;
+                const int kk = __ffs(ms ? ms : mp) - 1;
+                const int cc = __shfl_sync(kFull, c, kk);
+                const int dd = __shfl_sync(kFull, dir == 0 ? sc : pc, kk);
+                const int b = dir == 0 ? sa : pr;
+                if (dir == 0)   // edges (a,b),(c,d) -> (a,c),(b,d): reverse b .. c
+                    warp_reverse(route, pos, n, pos[b], pos[cc], lane);
+                else            // edges (b,a),(d,c) -> (b,d),(a,c): reverse a .. d
+                    warp_reverse(route, pos, n, pos[a], pos[dd], lane);
+                const int ends[4] = {a, b, cc, dd};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int v = ends[e];
+                    const uint32_t bit = 1u << (v & 31);
+                    const bool queued = (inq[v >> 5] & bit) != 0u;
+                    __syncwarp();
+                    if (!queued) {
+                        int t = head + count;
+                        if (t >= n) t -= n;
+                        if (lane == 0) {
+                            queue[t] = (uint16_t)v;
+                            inq[v >> 5] |= bit;
+                        }
+                        ++count;
+                    }
+                    __syncwarp();
+                }
+                ++sweep_moves;
+            }
+            __syncwarp();
+        }
+        moves += sweep_moves;
+    } while (sweep_moves > 0);
+    return moves;
+}
+
+}  // namespace mmas
+
+namespace mmas {
+
+// Row a8 over every ant of the shard, then the per-ant length and the block-level
+// iteration-best bookkeeping (row a5) on the IMPROVED routes (R26: the local-search
+// output replaces the ant's tour).
+__global__ void __launch_bounds__(128) two_opt_kernel(TwoOptArgs T, ConstructArgs A) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    unsigned long long wbest = ~0ull;
+    long long moves = 0;
+    for (int al = blockIdx.x * T.warps_per_block + warp; al < T.m_local; al += gridDim.x * T.warps_per_block) {
+        uint16_t* route = T.routes + (size_t)al * T.ldr;
+        moves += two_opt_route(T, route, T.pos + (size_t)al * T.ldr, T.queue + (size_t)al * T.ldr,
+                               T.inq + (size_t)al * T.nwords, lane);
+        __syncwarp();
+        wbest = min(wbest, finish_ant(A, route, al, (uint32_t)(A.ant_lo + al), lane));
+    }
+    if (lane == 0 && moves) atomicAdd(T.moves, (unsigned long long)moves);
+    block_finish(A, wbest, 0, lane, warp);
+}
+
+}  // namespace mmas

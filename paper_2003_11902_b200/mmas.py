@@ -48,12 +48,13 @@ class Config(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int64), ("fallback_steps", ctypes.c_int64),
-                ("ant_steps", ctypes.c_int64), ("ants_local", ctypes.c_int32), ("first_ant", ctypes.c_int32)]
+                ("ant_steps", ctypes.c_int64), ("ants_local", ctypes.c_int32), ("first_ant", ctypes.c_int32),
+                ("local_search_moves", ctypes.c_int64)]
 
 
 class PhaseTimes(ctypes.Structure):
     _fields_ = [("construct_ms", ctypes.c_double), ("select_ms", ctypes.c_double),
-                ("update_ms", ctypes.c_double), ("iterations", ctypes.c_int64)]
+                ("update_ms", ctypes.c_double), ("local_search_ms", ctypes.c_double), ("iterations", ctypes.c_int64)]
 
 
 _lib = None

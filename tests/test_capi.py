@@ -46,7 +46,7 @@ def test_built_for_sm100a():
     (dict(cand_len=10), "cand_len"),
     (dict(n_ants=0), "n_ants"),
     (dict(beta=-1.0), "beta"),
-    (dict(local_search=1), "local_search"),
+    (dict(local_search=2), "local_search"),
     (dict(world=2, rank=2), "rank"),
 ])
 def test_invalid_arguments_rejected_without_gpu(L, kw, frag):

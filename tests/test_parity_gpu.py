@@ -245,3 +245,37 @@ def test_profiling_accumulates_phase_times():
     t = g.phase_times()
     assert t["iterations"] == 5 and t["construct_ms"] > 0 and t["update_ms"] > 0
     assert g.kernel_launches - n0 == 10   # construct (+ fused select) and update per iteration
+
+
+# ---- row a8: 2-opt local search ------------------------------------------------------
+LS_CASES = [
+    (12, 5, 4, 3),
+    (60, 20, 8, 3),
+    (150, 37, 16, 3),
+    (300, 40, 32, 2),
+    (130, 25, 0, 2),      # full-row construction + 2-opt
+    (1100, 12, 32, 2),    # n > 1024 (shared-memory tabu), ragged n
+]
+
+
+@pytest.mark.parametrize("n,m,cl,iters", LS_CASES, ids=[f"n{c[0]}-m{c[1]}-cl{c[2]}" for c in LS_CASES])
+def test_two_opt_bit_exact(n, m, cl, iters):
+    lockstep(make_coords("uniform", n, 3000 + n), m, cl, iters, seed=11 + n, local_search=True, rho=0.7)
+
+
+def test_c5_sampled_ants_with_two_opt():
+    """d18512-shaped with cl 32 + 2-opt (C5) at full size: iteration-0 routes of sampled
+    ants after local search, computed one by one by the oracle."""
+    w = CONFIGS["C5"]
+    c = w.coords()
+    g = mmas.Colony(c, w.n_ants, w.cand_len, seed=w.mmas_seed, rho=w.rho, local_search=True)
+    o = oracle.Colony(c, w.n_ants, w.cand_len, seed=w.mmas_seed, rho=w.rho, local_search=True, nthreads=8)
+    assert g.limits() == o.limits()
+    g.iterate(1)
+    T, L = g.tours(), g.lengths()
+    for a in (0, 417, w.n_ants - 1):
+        r, l, _ = o.construct_ant(a)
+        assert np.array_equal(T[a], r), f"ant {a}"
+        assert L[a] == l
+    assert np.all(np.sort(T, axis=1) == np.arange(w.n))
+    assert g.stats()["local_search_moves"] > 0
