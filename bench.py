@@ -112,7 +112,8 @@ def cpu_baseline_leg(w, budget_s=12.0):
     """The oracle as it stands on this host's cores, bounded to ~budget_s of CPU work."""
     import oracle
     cores = os.cpu_count() or 1
-    col = oracle.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, nthreads=cores)
+    col = oracle.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, nthreads=cores,
+                        local_search=bool(w.local_search))
     t0 = time.perf_counter()
     iters = 0
     while True:
@@ -133,7 +134,8 @@ def run_reference(args):
     w = CONFIGS[args.config]
     import oracle
     cores = os.cpu_count() or 1
-    col = oracle.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, nthreads=cores)
+    col = oracle.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, nthreads=cores,
+                        local_search=bool(w.local_search))
     for _ in range(args.warmup if args.warmup < 3 else 1):
         col.iterate(1)
     # bounded: each step is one full oracle iteration; cap the number of timed steps
@@ -175,6 +177,7 @@ def run_ours(args):
     coords = w.coords()
     stream = torch.cuda.current_stream().cuda_stream
     col = mmas.Colony(coords, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=local_rank,
+                      local_search=bool(w.local_search),
                       stream=stream, rank=rank, world=world)
     rb = col.record_bytes
     local = torch.zeros(rb, dtype=torch.uint8, device="cuda")
@@ -247,7 +250,8 @@ def run_ours(args):
         pinned = torch.from_numpy(coords.copy()).pin_memory().numpy()
         out_steps = args.steps
         t0 = time.perf_counter()
-        c2 = mmas.Colony(pinned, w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=local_rank)
+        c2 = mmas.Colony(pinned, w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=local_rank,
+                         local_search=bool(w.local_search))
         for _ in range(out_steps):
             c2.iterate(1)
             c2.best_length()
@@ -276,10 +280,12 @@ def run_ours(args):
                                             "other hardware, construction only"},
                 "roofline": roofline, "update_roofline": update_roof,
                 "phases_ms_per_step": {"construct": cons_ms, "select": phases["select_ms"] / max(phases["iterations"], 1),
-                                       "update": update_ms},
+                                       "update": update_ms,
+                                       "local_search": phases["local_search_ms"] / max(phases["iterations"], 1)},
                 "construction_only_tours_per_s": w.n_ants / (cons_ms * 1e-3),
                 "gpu_launches": gpu_launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
-                "fallback_steps_per_tour": col.stats()["fallback_steps"] / max(col.stats()["iterations"], 1) / col.shard()[1]}
+                "fallback_steps_per_tour": col.stats()["fallback_steps"] / max(col.stats()["iterations"], 1) / col.shard()[1],
+                "local_search_moves_per_tour": col.stats()["local_search_moves"] / max(col.stats()["iterations"], 1) / col.shard()[1]}
         print(json.dumps(line), flush=True)
     col.close()
     if world > 1:

@@ -67,23 +67,29 @@ __device__ __forceinline__ long long two_opt_route(const TwoOptArgs& T, uint16_t
         __syncwarp();
         int head = 0, count = n;
         sweep_moves = 0;
+        // the static data of a popped node (its neighbour list entry per lane and the
+        // coordinates) is loaded one pop AHEAD, behind the current pop's work
+        int a = queue[0];
+        int c = lane < K ? T.nn[(size_t)a * K + lane] : a;
+        double2 xa = __ldg(T.xy + a), xc = __ldg(T.xy + c);
         while (count > 0) {
-            const int a = queue[head];
             head = wrap_inc(head, n);
             --count;
             if (lane == 0) inq[a >> 5] &= ~(1u << (a & 31));
+            const bool ahead = count > 0;                  // the next pop is already queued
+            const int a2 = ahead ? (int)queue[head] : a;
             const int pa = pos[a];
             const int sa = route[wrap_inc(pa, n)];      // successor of a
             const int pr = route[wrap_dec(pa, n)];      // predecessor of a
-            const double2 xa = __ldg(T.xy + a);
+            const int c2 = lane < K ? T.nn[(size_t)a2 * K + lane] : a2;
+            const double2 xa2 = __ldg(T.xy + a2);
             const int64_t d_as = euc2d(xa, __ldg(T.xy + sa));
             const int64_t d_ap = euc2d(xa, __ldg(T.xy + pr));
             // lane k: the k-th nearest neighbour c of a, in both directions
             bool imp_s = false, imp_p = false;
-            int c = 0, sc = 0, pc = 0;
+            int sc = 0, pc = 0;
+            const double2 xc2 = __ldg(T.xy + c2);
             if (lane < K) {
-                c = T.nn[(size_t)a * K + lane];
-                const double2 xc = __ldg(T.xy + c);
                 const int64_t d_ac = euc2d(xa, xc);
                 const int qc = pos[c];
                 sc = route[wrap_inc(qc, n)];
@@ -108,27 +114,42 @@ __device__ __forceinline__ long long two_opt_route(const TwoOptArgs& T, uint16_t
                     warp_reverse(route, pos, n, pos[b], pos[cc], lane);
                 else            // edges (b,a),(d,c) -> (b,d),(a,c): reverse a .. d
                     warp_reverse(route, pos, n, pos[a], pos[dd], lane);
+                // enqueue a, b, c, d in that order (four distinct nodes: c != a, c != b,
+                // d != a and b != d for a valid move), all queued-bits read up front
                 const int ends[4] = {a, b, cc, dd};
+                uint32_t w4[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) w4[e] = inq[ends[e] >> 5];
+                __syncwarp();
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int v = ends[e];
                     const uint32_t bit = 1u << (v & 31);
-                    const bool queued = (inq[v >> 5] & bit) != 0u;
-                    __syncwarp();
-                    if (!queued) {
+                    if (!(w4[e] & bit)) {
                         int t = head + count;
                         if (t >= n) t -= n;
                         if (lane == 0) {
                             queue[t] = (uint16_t)v;
-                            inq[v >> 5] |= bit;
+                            atomicOr(inq + (v >> 5), bit);   // two endpoints may share a word
                         }
                         ++count;
                     }
-                    __syncwarp();
                 }
+                __syncwarp();
                 ++sweep_moves;
             }
             __syncwarp();
+            if (ahead) {
+                a = a2;
+                c = c2;
+                xa = xa2;
+                xc = xc2;
+            } else if (count > 0) {   // the queue had run empty: the next pop was just enqueued
+                a = queue[head];
+                c = lane < K ? T.nn[(size_t)a * K + lane] : a;
+                xa = __ldg(T.xy + a);
+                xc = __ldg(T.xy + c);
+            }
         }
         moves += sweep_moves;
     } while (sweep_moves > 0);
@@ -151,6 +172,38 @@ __global__ void __launch_bounds__(128) two_opt_kernel(TwoOptArgs T, ConstructArg
         uint16_t* route = T.routes + (size_t)al * T.ldr;
         moves += two_opt_route(T, route, T.pos + (size_t)al * T.ldr, T.queue + (size_t)al * T.ldr,
                                T.inq + (size_t)al * T.nwords, lane);
+        __syncwarp();
+        wbest = min(wbest, finish_ant(A, route, al, (uint32_t)(A.ant_lo + al), lane));
+    }
+    if (lane == 0 && moves) atomicAdd(T.moves, (unsigned long long)moves);
+    block_finish(A, wbest, 0, lane, warp);
+}
+
+}  // namespace mmas
+
+namespace mmas {
+
+// Same search with the route and its inverse (pos) of each ant in SHARED memory:
+// every position lookup and the segment reversal run at shared-memory latency.
+// Blocks of W warps, each warp one ant at a time; 4 * ldr bytes of smem per warp.
+__global__ void __launch_bounds__(256) two_opt_smem_kernel(TwoOptArgs T, ConstructArgs A) {
+    extern __shared__ __align__(16) uint16_t ls_smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int W = T.warps_per_block;
+    uint16_t* s_route = ls_smem + (size_t)warp * 2 * T.ldr;
+    uint16_t* s_pos = s_route + T.ldr;
+    unsigned long long wbest = ~0ull;
+    long long moves = 0;
+    for (int al = blockIdx.x * W + warp; al < T.m_local; al += gridDim.x * W) {
+        uint16_t* route = T.routes + (size_t)al * T.ldr;
+        for (int i = 2 * lane; i < T.ldr; i += 64)
+            *reinterpret_cast<uint32_t*>(s_route + i) = *reinterpret_cast<const uint32_t*>(route + i);
+        __syncwarp();
+        moves += two_opt_route(T, s_route, s_pos, T.queue + (size_t)al * T.ldr, T.inq + (size_t)al * T.nwords, lane);
+        __syncwarp();
+        for (int i = 2 * lane; i < T.ldr; i += 64)
+            *reinterpret_cast<uint32_t*>(route + i) = *reinterpret_cast<const uint32_t*>(s_route + i);
         __syncwarp();
         wbest = min(wbest, finish_ant(A, route, al, (uint32_t)(A.ant_lo + al), lane));
     }
