@@ -169,14 +169,20 @@ def run_ours(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
-    torch.cuda.set_device(local_rank)
+    # one process per GPU; MMAS_DIST_BACKEND=gloo lets several ranks share one GPU (path tests only)
+    backend = os.environ.get("MMAS_DIST_BACKEND", "nccl")
+    dev = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     w = CONFIGS[args.config]
     m_total = w.n_ants * world                      # weak scaling: n_ants per GPU
     coords = w.coords()
     stream = torch.cuda.current_stream().cuda_stream
-    col = mmas.Colony(coords, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=local_rank,
+    col = mmas.Colony(coords, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
                       local_search=bool(w.local_search),
                       stream=stream, rank=rank, world=world)
     rb = col.record_bytes
@@ -188,7 +194,12 @@ def run_ours(args):
             col.iterate(1)
         else:
             col.construct(local.data_ptr())
-            dist.all_gather_into_tensor(gathered, local)
+            if backend == "nccl":
+                dist.all_gather_into_tensor(gathered, local)
+            else:   # host staging for the CPU backends
+                g_cpu = torch.empty(gathered.shape, dtype=gathered.dtype)
+                dist.all_gather_into_tensor(g_cpu, local.cpu())
+                gathered.copy_(g_cpu)
             col.update(gathered.data_ptr(), world)
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MiB > 126 MB L2
@@ -202,7 +213,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev) as clk:
         for k in range(args.steps):
             flush.zero_()
             ev[k][0].record()
@@ -216,7 +227,7 @@ def run_ours(args):
     total_ms = float(np.sum(step_ms))
     phases = col.phase_times()
     col.profile(False)
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
@@ -250,7 +261,7 @@ def run_ours(args):
         pinned = torch.from_numpy(coords.copy()).pin_memory().numpy()
         out_steps = args.steps
         t0 = time.perf_counter()
-        c2 = mmas.Colony(pinned, w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=local_rank,
+        c2 = mmas.Colony(pinned, w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
                          local_search=bool(w.local_search))
         for _ in range(out_steps):
             c2.iterate(1)
