@@ -427,6 +427,20 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
             commit(nxt, s);
             return false;
         };
+        // SPECULATIVE step (register tabu): commits its argmax unconditionally and reports
+        // whether every candidate was visited (the caller then rolls the group back)
+        auto spec_step = [&](auto J, int s) -> bool {
+            constexpr int j = decltype(J)::value;
+            float Lv[kSlots];
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q) Lv[q] = L[q][j];
+            uint32_t bm, bc;
+            evaluate(Lv, [&] { slice_half(J, H0{}); }, [&] { slice_half(J, H1{}); }, bm, bc);
+            const uint32_t best = __reduce_min_sync(kFull, bm);
+            const uint32_t nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
+            commit(nxt & 0xFFFFu, s);   // garbage but in-range if best >= 2^31; undone by the caller
+            return best >= 0x80000000u;
+        };
         // GENERIC step (runtime j): guards, and the R9 fallback (row a3) inlined ONCE
         auto generic_step = [&](int j, int s) {
             float Lv[kSlots];
@@ -477,23 +491,46 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
             int j0 = 0;
             bool sliced_j0 = false;
             if (pipeline) next_group(g);
+            bool sliced_all = false;
             if (g >= 1 && g < n_full && pipeline) {
-                int jf = -1;
-                if (fast_step(I0{}, 4 * g + 0)) jf = 0;
-                else if (fast_step(I1{}, 4 * g + 1)) jf = 1;
-                else if (fast_step(I2{}, 4 * g + 2)) jf = 2;
-                else if (fast_step(I3{}, 4 * g + 3)) jf = 3;
-                if (jf < 0) {
-                    rotate();
-                    ++g;
-                    continue;
+                if constexpr (kRegTabu) {
+                    // SPECULATIVE group: the four steps run as one straight-line block (no
+                    // branch between them, so the scheduler can overlap one step's random-key
+                    // slices with the next step's chain); a step that needed the fallback is
+                    // detected once at the end and the whole group is rolled back (tabu word,
+                    // current city, route staging) and redone by the generic path
+                    const uint32_t w0 = tabu.w, cur0 = cur, stage0 = stage;
+                    bool hit = spec_step(I0{}, 4 * g + 0);
+                    hit |= spec_step(I1{}, 4 * g + 1);
+                    hit |= spec_step(I2{}, 4 * g + 2);
+                    hit |= spec_step(I3{}, 4 * g + 3);
+                    if (__builtin_expect(!hit, 1)) {
+                        rotate();
+                        ++g;
+                        continue;
+                    }
+                    tabu.w = w0;
+                    cur = cur0;
+                    stage = stage0;
+                    sliced_all = true;   // every slice of this group already ran
+                } else {
+                    int jf = -1;
+                    if (fast_step(I0{}, 4 * g + 0)) jf = 0;
+                    else if (fast_step(I1{}, 4 * g + 1)) jf = 1;
+                    else if (fast_step(I2{}, 4 * g + 2)) jf = 2;
+                    else if (fast_step(I3{}, 4 * g + 3)) jf = 3;
+                    if (jf < 0) {
+                        rotate();
+                        ++g;
+                        continue;
+                    }
+                    j0 = jf;
+                    sliced_j0 = true;   // that step's slices ran inside its fast attempt
                 }
-                j0 = jf;
-                sliced_j0 = true;   // that step's slices ran inside its fast attempt
             }
 #pragma unroll 1
             for (int j = j0; j < 4; ++j) {
-                if (pipeline && !(j == j0 && sliced_j0)) slice_rt(j);
+                if (pipeline && !sliced_all && !(j == j0 && sliced_j0)) slice_rt(j);
                 const int s = 4 * g + j;
                 if (s > 0 && s < n) generic_step(j, s);
             }

@@ -189,7 +189,6 @@ struct ConstructArgs {
 }  // namespace mmas
 
 #include "construct.cuh"
-#include "construct_ws.cuh"
 #include "two_opt.cuh"
 
 namespace mmas {

@@ -131,7 +131,7 @@ struct mmas_ctx {
 
     // launch plan for construction
     bool smem_table = false;
-    bool ws = false;         // warp-specialised construction (construct_ws.cuh; A/B via MMAS_WS=1)
+
     bool reg_tabu = false;   // n <= 1024: tabu words in registers
     int slots = 1;
     int cons_warps = 4, cons_grid = 1;
@@ -259,15 +259,11 @@ ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = f
 template <int S, bool T, bool R, bool F = false>
 void set_smem_attr(size_t bytes) {
     cudaFuncSetAttribute(construct_cl_kernel<S, T, R, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    cudaFuncSetAttribute(construct_ws_kernel<S, T, R, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 template <int S, bool T, bool R, bool F>
 void launch_cl_f(mmas_ctx* h, const ConstructArgs& A) {
-    if (h->ws)   // warp-specialised: a producer warp per ant warp
-        construct_ws_kernel<S, T, R, F><<<h->cons_grid, h->cons_warps * 64, h->cons_smem, h->stream>>>(A);
-    else
-        construct_cl_kernel<S, T, R, F><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+    construct_cl_kernel<S, T, R, F><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
 }
 
 template <int S, bool T, bool R>
@@ -549,15 +545,12 @@ int setup(mmas_ctx* h) {
     // ---- construction launch plan ----
     const int nwords = round_up((n + 31) / 32, 4);
     h->reg_tabu = n <= 1024;
-    if (const char* e = std::getenv("MMAS_REG_TABU")) h->reg_tabu = h->reg_tabu && std::atoi(e) != 0;   // A/B switch
     const size_t tabu_bytes = h->reg_tabu ? 0 : (size_t)nwords * 4;
     h->slots = h->cl <= 32 ? 1 : (h->cl <= 64 ? 2 : 4);
-    if (const char* e = std::getenv("MMAS_WS")) h->ws = std::atoi(e) != 0;   // A/B switch
     if (h->cl > 0) {
         h->tb_inv = (uint32_t)round_up(n * h->cl * 4, 16);
         h->tb_id = (uint32_t)round_up(n * h->cl * 2, 16);
-        // per consumer warp: tabu (smem variant) + [ws] ring of kRing steps + 2 counters
-        const size_t per_warp = tabu_bytes + (h->ws ? (size_t)kRing * h->slots * 32 * 4 + 8 : 0);
+        const size_t per_warp = tabu_bytes;   // per ant warp: its tabu (shared-memory variant)
         // one block per SM holding the whole table; as many ant warps as needed
         int w = std::max(1, std::min(8, (h->m_local + h->num_sms - 1) / std::max(h->num_sms, 1)));
         size_t need = 128 + (size_t)h->tb_inv + h->tb_id + 16 + (size_t)w * per_warp;

@@ -38,9 +38,12 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, PhiloxKey key) {
 
 // u = (2*(x>>9)+1) * 2^-24: 23 random bits, exactly representable, in the open
 // interval (0,1) that A-Res and the log key need.
+// Built without an int->float conversion (those issue on the narrow XU pipe, which
+// the construction kernels would otherwise saturate): 1 + j 2^-23 from the mantissa
+// bits, minus (1 - 2^-24); the difference (2j+1) 2^-24 has <= 24 significant bits,
+// so the subtraction is exact and the value equals (float)(2j+1) * 2^-24 bit for bit.
 __device__ __forceinline__ float uniform_open(uint32_t x) {
-    const uint32_t odd = ((x >> 9) << 1) | 1u;               // < 2^24: exact in fp32
-    return __fmul_rn(__uint2float_rn(odd), 5.9604644775390625e-8f);  // * 2^-24, exact
+    return __fsub_rn(__uint_as_float(0x3F800000u | (x >> 9)), 0.99999994039535522461f);
 }
 
 // det_log2 (R14): u = 2^e * m, m in [sqrt(1/2), sqrt(2)), f = m - 1 (exact),
@@ -65,7 +68,9 @@ __device__ __forceinline__ float det_log2(float u) {
     p = __fmaf_rn(p, f, 0.48091062903404236f);
     p = __fmaf_rn(p, f, -0.7213473320007324f);
     p = __fmaf_rn(p, f, 1.4426950216293335f);
-    return __fmaf_rn(f, p, __int2float_rn(e));
+    // (float)e without I2F: 1.5 * 2^23 + e is exact in the significand for |e| < 2^22
+    const float ef = __fsub_rn(__int_as_float(0x4B400000 + e), 12582912.0f);
+    return __fmaf_rn(f, p, ef);
 }
 
 // Counter layouts (R13).  x2 = global ant id, x3 = global iteration.
