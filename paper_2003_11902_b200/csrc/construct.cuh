@@ -90,38 +90,65 @@ __device__ __forceinline__ void philox_rounds(uint4& c, const RoundKeys& rk) {
 // visited are skipped.  Per-lane best with ties to the lower id; the caller
 // reduces across the warp.
 // ---------------------------------------------------------------------------
+// One 128-city chunk of the scan: lane l's cities c0 .. c0+3, nib = their visited
+// bits (bit j set = visited or beyond n).  Branch-free per city.
+template <bool kArgmax>
+__device__ __forceinline__ void scan_chunk(const float* __restrict__ row, int c0, uint32_t nib, uint32_t step,
+                                           uint32_t ant, uint32_t iter, PhiloxKey key, uint32_t& best_mag,
+                                           uint32_t& best_c) {
+    float4 iv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (nib != 0xFu) iv = __ldg(reinterpret_cast<const float4*>(row + c0));
+    const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
+    if (kArgmax) {
+        // R9 flag: the largest weight = the smallest inv_w (positive floats order as uints)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t mag = ((nib >> j) & 1u) ? kNone : __float_as_uint(ivs[j]);
+            if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
+        }
+    } else {
+        const uint4 x = philox4x32_10(ctr_city((uint32_t)c0 >> 2, step, ant, iter), key);
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float k = __fmul_rn(det_log2(uniform_open(xs[j])), ivs[j]);
+            const uint32_t mag = ((nib >> j) & 1u) ? kNone : key_magnitude(k);
+            if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
+        }
+    }
+}
+
+// Visited bits of lane l's four cities c0 .. c0+3 (cities >= n count as visited).
+template <class Tabu>
+__device__ __forceinline__ uint32_t chunk_nibble(const Tabu& tabu, int c0, int n) {
+    const uint32_t word = tabu.word(min(c0, n - 1) >> 5);   // all lanes (RegTabu shuffles)
+    if (c0 >= n) return 0xFu;
+    uint32_t nib = (word >> (c0 & 31)) & 0xFu;
+    if (c0 + 4 > n) nib |= (0xFu << (n - c0)) & 0xFu;
+    return nib;
+}
+
+// ---------------------------------------------------------------------------
+// Scan of ALL unvisited cities from `row` (= inv_w[cur]): the full-row WRS step
+// (row a4) and the candidate-list fallback (row a3, R9).  Lane l handles the
+// 4-city groups 128t + 4l (a coalesced float4 of inv_w and one Philox per group
+// whose word j is city 4g+j's uniform, R13).  Two chunks per trip give two
+// independent Philox/log chains; a trip whose 256 cities are all visited is
+// skipped by the whole warp at once (no divergence).  Per-lane best with ties to
+// the lower id (cities are scanned in increasing order); the caller reduces
+// across the warp.
+// ---------------------------------------------------------------------------
 template <bool kArgmax, class Tabu>
 __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, const Tabu& tabu, int n,
                                                uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
                                                int lane, uint32_t& best_mag, uint32_t& best_c) {
-    for (int base = 0; base < n; base += 128) {
-        const int c0 = base + 4 * lane;
-        const uint32_t word = tabu.word(min(c0, n - 1) >> 5);   // all lanes (RegTabu shuffles)
-        if (c0 >= n) continue;
-        uint32_t nib = (word >> (c0 & 31)) & 0xFu;
-        if (c0 + 4 > n) nib |= (0xFu << (n - c0)) & 0xFu;     // cities >= n count as visited
-        if (nib == 0xFu) continue;
-        const float4 iv = __ldg(reinterpret_cast<const float4*>(row + c0));
-        const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
-        if (kArgmax) {
-            // R9 flag: the largest weight = the smallest inv_w (positive floats order as uints)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if ((nib >> j) & 1u) continue;
-                const uint32_t mag = __float_as_uint(ivs[j]);
-                if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
-            }
-        } else {
-            const uint4 x = philox4x32_10(ctr_city((uint32_t)c0 >> 2, step, ant, iter), key);
-            const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if ((nib >> j) & 1u) continue;
-                const float k = __fmul_rn(det_log2(uniform_open(xs[j])), ivs[j]);
-                const uint32_t mag = key_magnitude(k);
-                if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
-            }
-        }
+    for (int base = 0; base < n; base += 256) {
+        const int ca = base + 4 * lane, cb = ca + 128;
+        const uint32_t na = chunk_nibble(tabu, ca, n);
+        const uint32_t nb = chunk_nibble(tabu, cb, n);
+        if (!__any_sync(kFull, (na & nb) != 0xFu)) continue;
+        scan_chunk<kArgmax>(row, ca, na, step, ant, iter, key, best_mag, best_c);
+        scan_chunk<kArgmax>(row, cb, nb, step, ant, iter, key, best_mag, best_c);
     }
 }
 
