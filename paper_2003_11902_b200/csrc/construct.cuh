@@ -285,6 +285,7 @@ extern __shared__ __align__(128) unsigned char g_smem[];
 // ---------------------------------------------------------------------------
 template <int kSlots, bool kSmemTable, bool kRegTabu, bool kFull32>
 __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
+    pdl_wait();
     static_assert(!kFull32 || kSlots == 1, "kFull32: cl == 32, one slot per lane");
     using Tabu = typename std::conditional<kRegTabu, RegTabu, SmemTabu>::type;
     const int lane = threadIdx.x & 31;
@@ -578,6 +579,7 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
 // ---------------------------------------------------------------------------
 template <bool kRegTabu>
 __global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
+    pdl_wait();
     using Tabu = typename std::conditional<kRegTabu, RegTabu, SmemTabu>::type;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;

@@ -18,6 +18,12 @@
 namespace mmas {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// Programmatic dependent launch: the iteration's kernels are launched with
+// programmatic stream serialisation, so a kernel's blocks are resident before its
+// predecessor finishes; each waits here before touching the predecessor's output
+// (a no-op when launched without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 // TSPLIB EUC_2D (R12): (int)(sqrt(dx*dx + dy*dy) + 0.5) in double.
@@ -160,6 +166,7 @@ __device__ __noinline__ void select_best_warp(const SelectArgs S, int lane) {
 }
 
 __global__ void select_best_kernel(SelectArgs S) {
+    pdl_wait();
     if (threadIdx.x < 32) select_best_warp(S, threadIdx.x);
 }
 
@@ -233,6 +240,7 @@ struct UpdateArgs {
 };
 
 __global__ void __launch_bounds__(256) pheromone_update_kernel(UpdateArgs U) {
+    pdl_wait();
     extern __shared__ __align__(16) float s_row[];   // new inv_w row (cl > 0: for the gather)
     const float tmin = U.scal[0], tmax = U.scal[1], delta = U.scal[2];
     const int n4 = (U.n + 3) >> 2;

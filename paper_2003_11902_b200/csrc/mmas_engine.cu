@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <utility>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -256,6 +257,25 @@ ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = f
     return A;
 }
 
+// Launch with programmatic stream serialisation (PDL): the kernel's blocks may be
+// scheduled while the previous kernel on the stream drains; kernels call pdl_wait()
+// before reading their predecessor's results.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <int S, bool T, bool R, bool F = false>
 void set_smem_attr(size_t bytes) {
     cudaFuncSetAttribute(construct_cl_kernel<S, T, R, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -263,7 +283,7 @@ void set_smem_attr(size_t bytes) {
 
 template <int S, bool T, bool R, bool F>
 void launch_cl_f(mmas_ctx* h, const ConstructArgs& A) {
-    construct_cl_kernel<S, T, R, F><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+    launch_pdl(construct_cl_kernel<S, T, R, F>, dim3(h->cons_grid), dim3(h->cons_warps * 32), h->cons_smem, h->stream, A);
 }
 
 template <int S, bool T, bool R>
@@ -401,7 +421,7 @@ int launch_update(mmas_ctx* h) {
     U.iter_dev = h->iter_dev;
     const int threads = 256;
     const size_t smem = h->cl > 0 ? sizeof(float) * (size_t)h->ld : 0;
-    pheromone_update_kernel<<<h->n, threads, smem, h->stream>>>(U);
+    launch_pdl(pheromone_update_kernel, dim3(h->n), dim3(threads), smem, h->stream, U);
     h->launches++;
     CU(cudaGetLastError());
     return MMAS_OK;

@@ -75,7 +75,7 @@ __device__ __forceinline__ long long two_opt_route(const TwoOptArgs& T, uint16_t
         while (count > 0) {
             head = wrap_inc(head, n);
             --count;
-            if (lane == 0) inq[a >> 5] &= ~(1u << (a & 31));
+            if (lane == 0) atomicAnd(inq + (a >> 5), ~(1u << (a & 31)));   // fire-and-forget (RED), no load on the pop path
             const bool ahead = count > 0;                  // the next pop is already queued
             const int a2 = ahead ? (int)queue[head] : a;
             const int pa = pos[a];
@@ -164,6 +164,7 @@ namespace mmas {
 // iteration-best bookkeeping (row a5) on the IMPROVED routes (R26: the local-search
 // output replaces the ant's tour).
 __global__ void __launch_bounds__(128) two_opt_kernel(TwoOptArgs T, ConstructArgs A) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     unsigned long long wbest = ~0ull;
@@ -187,6 +188,7 @@ namespace mmas {
 // every position lookup and the segment reversal run at shared-memory latency.
 // Blocks of W warps, each warp one ant at a time; 4 * ldr bytes of smem per warp.
 __global__ void __launch_bounds__(256) two_opt_smem_kernel(TwoOptArgs T, ConstructArgs A) {
+    pdl_wait();
     extern __shared__ __align__(16) uint16_t ls_smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
