@@ -144,7 +144,7 @@ struct mmas_ctx {
     int64_t launches = 0;
 
     // row a8: 2-opt local search (local_search != 0)
-    int ls_k = 0, ls_nwords = 0, ls_smem_max = 0;
+    int ls_k = 0, ls_nwords = 0, ls_coop_smem_max = 0;
     uint16_t* ls_nn = nullptr;         // n x ls_k neighbour lists
     uint16_t *ls_pos = nullptr, *ls_queue = nullptr;
     uint32_t* ls_inq = nullptr;
@@ -384,18 +384,16 @@ int launch_two_opt(mmas_ctx* h, bool fuse_select) {
     T.queue = h->ls_queue;
     T.inq = h->ls_inq;
     T.moves = h->ls_moves;
-    const size_t per_warp = (size_t)4 * h->ldr;   // route + pos (u16) in shared memory
-    const int w_smem = (int)std::min<size_t>(8, (size_t)h->ls_smem_max / per_warp);
-    if (w_smem >= 1) {
-        // as many ants per block as the shared memory holds; enough blocks for every ant
-        const int w = std::max(1, std::min(w_smem, (h->m_local + h->num_sms - 1) / h->num_sms));
-        T.warps_per_block = w;
-        const int grid = std::max(1, std::min((h->m_local + w - 1) / w, h->num_sms * std::max(1, w_smem / w)));
-        two_opt_smem_kernel<<<grid, 32 * w, per_warp * w, h->stream>>>(T, construct_args(h, fuse_select));
+    const size_t per_ant = (size_t)4 * h->ldr;   // route + pos (u16) in shared memory
+    if (per_ant <= (size_t)h->ls_coop_smem_max) {
+        // one block of kLsWarps warps per ant (speculative parallel FIFO, two_opt_coop_kernel)
+        T.warps_per_block = kLsWarps;
+        launch_pdl(two_opt_coop_kernel, dim3(std::max(1, h->m_local)), dim3(kLsWarps * 32), per_ant, h->stream, T,
+                   construct_args(h, fuse_select));
     } else {
         T.warps_per_block = 4;
         const int grid = std::max(1, (h->m_local + 3) / 4);
-        two_opt_kernel<<<grid, 128, 0, h->stream>>>(T, construct_args(h, fuse_select));
+        launch_pdl(two_opt_kernel, dim3(grid), dim3(128), 0, h->stream, T, construct_args(h, fuse_select));
     }
     h->launches++;
     CU(cudaGetLastError());
@@ -600,9 +598,9 @@ int setup(mmas_ctx* h) {
     }
     {
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, two_opt_smem_kernel);
-        h->ls_smem_max = h->smem_optin - (int)fa.sharedSizeBytes;   // dynamic = opt-in limit - static
-        cudaFuncSetAttribute(two_opt_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->ls_smem_max);
+        cudaFuncGetAttributes(&fa, two_opt_coop_kernel);
+        h->ls_coop_smem_max = h->smem_optin - (int)fa.sharedSizeBytes;   // dynamic = opt-in limit - static
+        cudaFuncSetAttribute(two_opt_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->ls_coop_smem_max);
     }
     cudaFuncSetAttribute(pheromone_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(float) * (size_t)h->ld));

@@ -184,32 +184,188 @@ __global__ void __launch_bounds__(128) two_opt_kernel(TwoOptArgs T, ConstructArg
 
 namespace mmas {
 
-// Same search with the route and its inverse (pos) of each ant in SHARED memory:
-// every position lookup and the segment reversal run at shared-memory latency.
-// Blocks of W warps, each warp one ant at a time; 4 * ldr bytes of smem per warp.
-__global__ void __launch_bounds__(256) two_opt_smem_kernel(TwoOptArgs T, ConstructArgs A) {
+}  // namespace mmas
+
+namespace mmas {
+
+// ---------------------------------------------------------------------------
+// Cooperative 2-opt: one BLOCK of kLsWarps warps per ant, route + pos in shared
+// memory.  Speculative parallel FIFO: in each round warp w evaluates the w-th
+// queued node on the SAME route; the results are then taken in queue order up
+// to and including the first improving one (exactly what the sequential FIFO of
+// R24 would do, since nothing changes the route until that move), the rest are
+// discarded and re-evaluated in the next round.  ~3/4 of the pops find no move,
+// so a round retires several pops for the latency of one evaluation; the
+// reversal of an applied move is spread over all kLsWarps * 32 lanes.
+// ---------------------------------------------------------------------------
+constexpr int kLsWarps = 8;
+
+struct MoveEval {
+    int found, dir, b, c, d;
+};
+
+// Evaluate node a on the current route (one warp).  Lane k: the k-th neighbour.
+__device__ __forceinline__ MoveEval eval_node(const TwoOptArgs& T, const uint16_t* route, const uint16_t* pos,
+                                              int a, int lane) {
+    const int n = T.n, K = T.K;
+    const int pa = pos[a];
+    const int sa = route[wrap_inc(pa, n)];
+    const int pr = route[wrap_dec(pa, n)];
+    const double2 xa = __ldg(T.xy + a);
+    int c = a, sc = 0, pc = 0;
+    if (lane < K) c = T.nn[(size_t)a * K + lane];
+    const double2 xc = __ldg(T.xy + c);
+    const int64_t d_as = euc2d(xa, __ldg(T.xy + sa));
+    const int64_t d_ap = euc2d(xa, __ldg(T.xy + pr));
+    bool imp_s = false, imp_p = false;
+    if (lane < K) {
+        const int64_t d_ac = euc2d(xa, xc);
+        const int qc = pos[c];
+        sc = route[wrap_inc(qc, n)];
+        pc = route[wrap_dec(qc, n)];
+        if (d_ac < d_as && c != sa && sc != a)   // Bentley pruning + degenerate moves
+            imp_s = d_ac + euc2d(__ldg(T.xy + sa), __ldg(T.xy + sc)) - d_as - euc2d(xc, __ldg(T.xy + sc)) < 0;
+        if (d_ac < d_ap && c != pr && pc != a)
+            imp_p = d_ac + euc2d(__ldg(T.xy + pr), __ldg(T.xy + pc)) - d_ap - euc2d(xc, __ldg(T.xy + pc)) < 0;
+    }
+    const uint32_t ms = __ballot_sync(kFull, imp_s);
+    const uint32_t mp = __ballot_sync(kFull, imp_p);
+    MoveEval m{0, 0, 0, 0, 0};
+    if (ms | mp) {
+        m.found = 1;
+        m.dir = ms ? 0 : 1;
+        const int kk = __ffs(ms ? ms : mp) - 1;
+        m.c = __shfl_sync(kFull, c, kk);
+        m.d = __shfl_sync(kFull, m.dir == 0 ? sc : pc, kk);
+        m.b = m.dir == 0 ? sa : pr;
+    }
+    return m;
+}
+
+__global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs T, ConstructArgs A) {
     pdl_wait();
     extern __shared__ __align__(16) uint16_t ls_smem[];
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int W = T.warps_per_block;
-    uint16_t* s_route = ls_smem + (size_t)warp * 2 * T.ldr;
-    uint16_t* s_pos = s_route + T.ldr;
+    __shared__ MoveEval s_eval[kLsWarps];
+    __shared__ int s_ctl[4];   // head, count, sweep_moves, winner
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int n = T.n;
+    uint16_t* s_route = ls_smem;
+    uint16_t* s_pos = ls_smem + T.ldr;
     unsigned long long wbest = ~0ull;
     long long moves = 0;
-    for (int al = blockIdx.x * W + warp; al < T.m_local; al += gridDim.x * W) {
+    for (int al = blockIdx.x; al < T.m_local; al += gridDim.x) {
         uint16_t* route = T.routes + (size_t)al * T.ldr;
-        for (int i = 2 * lane; i < T.ldr; i += 64)
+        uint16_t* queue = T.queue + (size_t)al * T.ldr;
+        uint32_t* inq = T.inq + (size_t)al * T.nwords;
+        for (int i = 2 * tid; i < T.ldr; i += 2 * blockDim.x)
             *reinterpret_cast<uint32_t*>(s_route + i) = *reinterpret_cast<const uint32_t*>(route + i);
-        __syncwarp();
-        moves += two_opt_route(T, s_route, s_pos, T.queue + (size_t)al * T.ldr, T.inq + (size_t)al * T.nwords, lane);
-        __syncwarp();
-        for (int i = 2 * lane; i < T.ldr; i += 64)
+        __syncthreads();
+        for (int i = tid; i < n; i += blockDim.x) s_pos[s_route[i]] = (uint16_t)i;
+        int sweep_moves;
+        do {
+            // (re-)seed the queue with every node in route order
+            for (int i = tid; i < n; i += blockDim.x) queue[i] = s_route[i];
+            for (int w = tid; w < T.nwords; w += blockDim.x) inq[w] = 0xFFFFFFFFu;
+            if (tid == 0) {
+                s_ctl[0] = 0;
+                s_ctl[1] = n;
+                s_ctl[2] = 0;
+            }
+            __syncthreads();
+            while (true) {
+                const int head = s_ctl[0], count = s_ctl[1];
+                if (count == 0) break;
+                // warp w evaluates the w-th queued node (all on the same route)
+                if (warp < count) {
+                    int q = head + warp;
+                    if (q >= n) q -= n;
+                    const MoveEval m = eval_node(T, s_route, s_pos, (int)queue[q], lane);
+                    if (lane == 0) s_eval[warp] = m;
+                }
+                __syncthreads();
+                // take the results in queue order up to the first improving one
+                const int avail = min(count, kLsWarps);
+                int win = -1;
+                for (int w = 0; w < avail; ++w)
+                    if (s_eval[w].found) { win = w; break; }
+                const int retired = win >= 0 ? win + 1 : avail;
+                if (tid == 0) {
+                    for (int w = 0; w < retired; ++w) {
+                        int q = head + w;
+                        if (q >= n) q -= n;
+                        const int a = queue[q];
+                        atomicAnd(inq + (a >> 5), ~(1u << (a & 31)));
+                    }
+                }
+                int nhead = head + retired;
+                if (nhead >= n) nhead -= n;
+                int ncount = count - retired;
+                if (win >= 0) {
+                    const MoveEval m = s_eval[win];
+                    int q = head + win;
+                    if (q >= n) q -= n;
+                    const int a = queue[q];
+                    // reverse (all lanes of all warps; disjoint pairs)
+                    int i = m.dir == 0 ? s_pos[m.b] : s_pos[a];
+                    int j = m.dir == 0 ? s_pos[m.c] : s_pos[m.d];
+                    __syncthreads();   // every thread has read the positions before they change
+                    int len = j - i;
+                    if (len < 0) len += n;
+                    len += 1;
+                    if (2 * len > n) {
+                        const int ni = wrap_inc(j, n), nj = wrap_dec(i, n);
+                        i = ni;
+                        j = nj;
+                        len = n - len;
+                    }
+                    for (int k = tid; k < len / 2; k += blockDim.x) {
+                        int p = i + k;
+                        if (p >= n) p -= n;
+                        int qq = j - k;
+                        if (qq < 0) qq += n;
+                        const uint16_t vp = s_route[p], vq = s_route[qq];
+                        s_route[p] = vq;
+                        s_route[qq] = vp;
+                        s_pos[vq] = (uint16_t)p;
+                        s_pos[vp] = (uint16_t)qq;
+                    }
+                    // enqueue a, b, c, d in that order (thread 0; the bits of a .. d)
+                    if (tid == 0) {
+                        const int ends[4] = {a, m.b, m.c, m.d};
+                        __threadfence_block();
+                        for (int e = 0; e < 4; ++e) {
+                            const int v = ends[e];
+                            const uint32_t bit = 1u << (v & 31);
+                            if (!(atomicOr(inq + (v >> 5), bit) & bit)) {
+                                int t = nhead + ncount;
+                                if (t >= n) t -= n;
+                                queue[t] = (uint16_t)v;
+                                ++ncount;
+                            }
+                        }
+                        s_ctl[2] += 1;
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    s_ctl[0] = nhead;
+                    s_ctl[1] = ncount;
+                }
+                __syncthreads();
+            }
+            sweep_moves = s_ctl[2];
+            moves += sweep_moves;
+            __syncthreads();
+        } while (sweep_moves > 0);
+        for (int i = 2 * tid; i < T.ldr; i += 2 * blockDim.x)
             *reinterpret_cast<uint32_t*>(route + i) = *reinterpret_cast<const uint32_t*>(s_route + i);
-        __syncwarp();
-        wbest = min(wbest, finish_ant(A, route, al, (uint32_t)(A.ant_lo + al), lane));
+        __syncthreads();
+        if (warp == 0) wbest = min(wbest, finish_ant(A, route, al, (uint32_t)(A.ant_lo + al), lane));
+        __syncthreads();
     }
-    if (lane == 0 && moves) atomicAdd(T.moves, (unsigned long long)moves);
+    if (tid == 0 && moves) atomicAdd(T.moves, (unsigned long long)moves);
     block_finish(A, wbest, 0, lane, warp);
 }
 
