@@ -1,5 +1,5 @@
 #!/bin/bash
-# One GPU session: device facts, parity tests, smoke, bench, ncu launch list + one full capture.
+# One GPU session: device facts, parity tests, smoke, benches, ncu launch list + full captures.
 # Usage (from the repo root, under gpurun): bash scripts/gpu_session.sh [tag] [what...]
 TAG=${1:-r01}
 shift || true
@@ -14,16 +14,9 @@ if has facts; then
   nproc > $OUT/nproc.txt; lscpu | grep -E "Model name|^CPU\(s\)" >> $OUT/nproc.txt
   python -c "import torch; p=torch.cuda.get_device_properties(0); print(p); print('sms',p.multi_processor_count,'l2',p.L2_cache_size)" > $OUT/device.txt 2>&1
 fi
-if has build; then
-  timeout 600 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1; echo "build rc=$?" >> $OUT/build.log
-fi
 if has tests; then
-  timeout 1500 python -m pytest tests -x -q -m gpu --durations=15 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
-  tail -5 $OUT/pytest_gpu.log
-fi
-if has alltests; then
-  timeout 1800 python -m pytest tests -q -m gpu --durations=15 > $OUT/pytest_gpu_all.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu_all.log
-  tail -5 $OUT/pytest_gpu_all.log
+  timeout 1500 python -m pytest tests -q -m gpu --durations=15 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+  tail -3 $OUT/pytest_gpu.log
 fi
 if has smoke; then
   timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
@@ -31,12 +24,13 @@ if has smoke; then
 fi
 if has bench; then
   timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
-  cat $OUT/bench.json | head -c 3000; echo
+  head -c 600 $OUT/bench.json; echo
 fi
-for cfg in C1 C3 C4; do
+for cfg in C1 C3 C4 C5; do
   if has bench$cfg; then
-    timeout 900 python bench.py --config $cfg --steps 50 --no-cpu-baseline > $OUT/bench_$cfg.json 2> $OUT/bench_$cfg.err
-    head -c 1500 $OUT/bench_$cfg.json; echo
+    steps=50; [ $cfg == C4 ] && steps=20; [ $cfg == C5 ] && steps=6
+    timeout 1200 python bench.py --config $cfg --steps $steps --warmup 3 --no-cpu-baseline > $OUT/bench_$cfg.json 2> $OUT/bench_$cfg.err
+    head -c 300 $OUT/bench_$cfg.json; echo
   fi
 done
 if has reference; then
@@ -46,9 +40,13 @@ fi
 if has ncu; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
      python bench.py --steps 30 --warmup 3 --no-cpu-baseline > $OUT/ncu_launches_bench.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:construct -s 3 -c 1 -o $OUT/prof_construct \
-     python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_construct.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pheromone_update -s 3 -c 1 -o $OUT/prof_update \
-     python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_update.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:construct -s 400 -c 1 -o $OUT/prof_construct \
+     python bench.py --steps 420 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_construct.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pheromone_update -s 400 -c 1 -o $OUT/prof_update \
+     python bench.py --steps 420 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_update.log 2>&1
   ls -la $OUT
+fi
+if has ncuC5; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:two_opt -s 2 -c 1 -o $OUT/prof_two_opt_C5 \
+     python bench.py --config C5 --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_two_opt.log 2>&1
 fi
