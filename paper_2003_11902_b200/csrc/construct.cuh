@@ -93,11 +93,8 @@ __device__ __forceinline__ void philox_rounds(uint4& c, const RoundKeys& rk) {
 // One 128-city chunk of the scan: lane l's cities c0 .. c0+3, nib = their visited
 // bits (bit j set = visited or beyond n).  Branch-free per city.
 template <bool kArgmax>
-__device__ __forceinline__ void scan_chunk(const float* __restrict__ row, int c0, uint32_t nib, uint32_t step,
-                                           uint32_t ant, uint32_t iter, PhiloxKey key, uint32_t& best_mag,
-                                           uint32_t& best_c) {
-    float4 iv = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (nib != 0xFu) iv = __ldg(reinterpret_cast<const float4*>(row + c0));
+__device__ __forceinline__ void scan_chunk(float4 iv, int c0, uint32_t nib, uint32_t step, uint32_t ant,
+                                           uint32_t iter, PhiloxKey key, uint32_t& best_mag, uint32_t& best_c) {
     const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
     if (kArgmax) {
         // R9 flag: the largest weight = the smallest inv_w (positive floats order as uints)
@@ -138,17 +135,47 @@ __device__ __forceinline__ uint32_t chunk_nibble(const Tabu& tabu, int c0, int n
 // the lower id (cities are scanned in increasing order); the caller reduces
 // across the warp.
 // ---------------------------------------------------------------------------
-template <bool kArgmax, class Tabu>
+template <bool kArgmax, bool kPrefetch = false, class Tabu>
 __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, const Tabu& tabu, int n,
                                                uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
                                                int lane, uint32_t& best_mag, uint32_t& best_c) {
-    for (int base = 0; base < n; base += 256) {
+    auto load_trip = [&](int base, uint32_t& na, uint32_t& nb, float4& iva, float4& ivb) {
         const int ca = base + 4 * lane, cb = ca + 128;
-        const uint32_t na = chunk_nibble(tabu, ca, n);
-        const uint32_t nb = chunk_nibble(tabu, cb, n);
-        if (!__any_sync(kFull, (na & nb) != 0xFu)) continue;
-        scan_chunk<kArgmax>(row, ca, na, step, ant, iter, key, best_mag, best_c);
-        scan_chunk<kArgmax>(row, cb, nb, step, ant, iter, key, best_mag, best_c);
+        na = chunk_nibble(tabu, ca, n);
+        nb = chunk_nibble(tabu, cb, n);
+        iva = na != 0xFu ? __ldg(reinterpret_cast<const float4*>(row + ca)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        ivb = nb != 0xFu ? __ldg(reinterpret_cast<const float4*>(row + cb)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    if constexpr (kPrefetch) {
+        // the next trip's visited bits and inv_w float4s are loaded one trip ahead
+        // (full-row path, where the scan is the whole step; costs ~20 registers)
+        uint32_t na, nb;
+        float4 iva, ivb;
+        load_trip(0, na, nb, iva, ivb);
+        for (int base = 0; base < n; base += 256) {
+            uint32_t na2 = 0xFu, nb2 = 0xFu;
+            float4 iva2 = make_float4(0.f, 0.f, 0.f, 0.f), ivb2 = iva2;
+            if (base + 256 < n) load_trip(base + 256, na2, nb2, iva2, ivb2);
+            if (__any_sync(kFull, (na & nb) != 0xFu)) {
+                const int ca = base + 4 * lane;
+                scan_chunk<kArgmax>(iva, ca, na, step, ant, iter, key, best_mag, best_c);
+                scan_chunk<kArgmax>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c);
+            }
+            na = na2;
+            nb = nb2;
+            iva = iva2;
+            ivb = ivb2;
+        }
+    } else {
+        for (int base = 0; base < n; base += 256) {
+            uint32_t na, nb;
+            float4 iva, ivb;
+            load_trip(base, na, nb, iva, ivb);
+            if (!__any_sync(kFull, (na & nb) != 0xFu)) continue;
+            const int ca = base + 4 * lane;
+            scan_chunk<kArgmax>(iva, ca, na, step, ant, iter, key, best_mag, best_c);
+            scan_chunk<kArgmax>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c);
+        }
     }
 }
 
@@ -601,7 +628,7 @@ __global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
         uint32_t cur = start;
         for (int s = 1; s < n; ++s) {
             uint32_t bm = kNone, bc = kNone;
-            scan_unvisited<false>(A.inv_w + (size_t)cur * A.ld, tabu, n, (uint32_t)s, ant, iter, A.key, lane, bm,
+            scan_unvisited<false, true>(A.inv_w + (size_t)cur * A.ld, tabu, n, (uint32_t)s, ant, iter, A.key, lane, bm,
                                   bc);
             const uint32_t nxt = warp_select(bm, bc);
             tabu.mark(nxt, lane);
