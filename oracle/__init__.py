@@ -31,6 +31,7 @@ class _Params(ctypes.Structure):
         ("p_best", ctypes.c_double), ("seed", ctypes.c_uint64),
         ("deposit_global", ctypes.c_int32), ("fallback_argmax", ctypes.c_int32),
         ("local_search", ctypes.c_int32), ("nthreads", ctypes.c_int32),
+        ("tabu", ctypes.c_int32),
     ]
 
 
@@ -75,6 +76,11 @@ def lib():
         L.orc_select_next.restype = ctypes.c_int32
         L.orc_start_node.argtypes = [ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint32, P(ctypes.c_uint32)]
         L.orc_start_node.restype = ctypes.c_int32
+        L.orc_ct_init.argtypes = [P(ctypes.c_int32), P(ctypes.c_int32), ctypes.c_int32]
+        L.orc_ct_mark.argtypes = [P(ctypes.c_int32), P(ctypes.c_int32), ctypes.c_int32, ctypes.c_int32]
+        L.orc_select_next_ct.argtypes = [P(ctypes.c_float), P(ctypes.c_int32), ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_uint32, ctypes.c_uint32, P(ctypes.c_uint32)]
+        L.orc_select_next_ct.restype = ctypes.c_int32
         for name in ("orc_iteration", "orc_ib_ant"):
             getattr(L, name).argtypes = [ctypes.c_void_p]
             getattr(L, name).restype = ctypes.c_int32
@@ -217,6 +223,31 @@ def select_next(inv_w_row, cand_row, visited, s, a, it, seed, fallback_argmax=0)
     return c, fb.value
 
 
+def ct_init(n):
+    """Compact tabu: returns (entries, L)."""
+    e = np.zeros(n, dtype=np.int32)
+    L = ctypes.c_int32()
+    lib().orc_ct_init(_ptr(e, ctypes.c_int32), ctypes.byref(L), n)
+    return e, L.value
+
+
+def ct_mark(entries, L, u):
+    """CT mark(u) on a copy; returns (entries, L)."""
+    e = np.array(entries, dtype=np.int32, copy=True)
+    Lc = ctypes.c_int32(L)
+    lib().orc_ct_mark(_ptr(e, ctypes.c_int32), ctypes.byref(Lc), len(e), int(u))
+    return e, Lc.value
+
+
+def select_next_ct(inv_w_row, entries, L, s, a, it, seed):
+    """One full-row step over the CT's list (Alg. 3, R27)."""
+    w = np.ascontiguousarray(inv_w_row, dtype=np.float32)
+    e = np.ascontiguousarray(entries, dtype=np.int32)
+    key = np.array([seed & 0xFFFFFFFF, seed >> 32], dtype=np.uint32)
+    return lib().orc_select_next_ct(_ptr(w, ctypes.c_float), _ptr(e, ctypes.c_int32), int(L), s, a, it,
+                                    _ptr(key, ctypes.c_uint32))
+
+
 def start_node(n, a, it, seed):
     key = np.array([seed & 0xFFFFFFFF, seed >> 32], dtype=np.uint32)
     return lib().orc_start_node(n, a, it, _ptr(key, ctypes.c_uint32))
@@ -228,7 +259,7 @@ class Colony:
 
     def __init__(self, coords, n_ants, cand_len, alpha=1.0, beta=2.0, rho=0.5, seed=42,
                  p_best=0.01, deposit_global=False, fallback_argmax=False, local_search=False,
-                 nthreads=None):
+                 nthreads=None, tabu=0):
         c = np.ascontiguousarray(coords, dtype=np.float64).reshape(-1, 2)
         self.coords = c
         self.n = c.shape[0]
@@ -238,7 +269,7 @@ class Colony:
             nthreads = os.cpu_count() or 1
         p = _Params(self.n, self.m, self.cl, float(alpha), float(beta), float(rho), float(p_best),
                     int(seed) & 0xFFFFFFFFFFFFFFFF, int(deposit_global), int(fallback_argmax),
-                    int(local_search), int(nthreads))
+                    int(local_search), int(nthreads), int(tabu))
         flat = c.ravel()
         h = lib().orc_create(ctypes.byref(p), _ptr(flat, ctypes.c_double))
         if not h:

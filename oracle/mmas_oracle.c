@@ -198,6 +198,7 @@ typedef struct {
     int32_t fallback_argmax;  /* R9: 0 = WRS over all unvisited (default), 1 = argmax weight */
     int32_t local_search;     /* a8: 2-opt on every route (R25) */
     int32_t nthreads;
+    int32_t tabu;             /* R27: 0 = bitmask tabu BT (default), 1 = compact tabu CT (cl = 0 only) */
 } orc_params;
 
 typedef struct {
@@ -279,6 +280,7 @@ ORC_EXPORT orc_t *orc_create(const orc_params *p, const double *coords)
     if (!(p->rho > 0.0 && p->rho < 1.0)) return NULL;
     if (!is_int_in(p->alpha, 0, 8) || p->beta < 0.0) return NULL;
     if (!(p->p_best > 0.0 && p->p_best < 1.0)) return NULL;
+    if (p->tabu < 0 || p->tabu > 1 || (p->tabu == 1 && p->cl != 0)) return NULL;   /* R27 */
     for (int32_t i = 0; i < 2 * p->n; ++i)
         if (!isfinite(coords[i])) return NULL;
 
@@ -379,6 +381,56 @@ ORC_EXPORT int32_t orc_select_next(const float *inv_w_row, const int32_t *cand_r
         float kk = orc_det_log2(u) * inv_w_row[c];
         if (best < 0 || kk > best_key) {   /* ascending c: a tie keeps the lower id */
             best = c;
+            best_key = kk;
+        }
+    }
+    return best;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Compact tabu CT (Sec. 4.1), used by the full-row path (cl = 0,   */
+/* the paper's MMAS-WRS-CT, recommended without candidate lists P:1998-2001).  */
+/* entries[0..L) is the list of unvisited nodes; a position p >= L holds the   */
+/* index of node p if p was relocated into the list, else the sentinel n.      */
+/* ------------------------------------------------------------------------- */
+ORC_EXPORT void orc_ct_init(int32_t *entries, int32_t *L, int32_t n)
+{
+    /* "Initially, the entries array contains consecutive numbers from 0 to n-1" */
+    for (int32_t i = 0; i < n; ++i) entries[i] = i;
+    *L = n;
+}
+
+/* mark(u) for an unvisited node u. */
+ORC_EXPORT void orc_ct_mark(int32_t *entries, int32_t *L, int32_t n, int32_t u)
+{
+    /* u < L: u is at its initial position; u >= L: entries[u] is its index */
+    int32_t iu = u < *L ? u : entries[u];
+    if (iu == *L - 1) {
+        entries[iu] = n;                      /* u is the last element: sentinel */
+    } else {
+        int32_t t = entries[*L - 1];          /* the last element replaces u */
+        entries[iu] = t;
+        entries[t] = iu;                      /* "the new position of t is saved" */
+    }
+    *L -= 1;
+}
+
+/* One full-row step over the CT (Alg. 3 P:964-994 with l = tabu.length() = L,
+ * v = tabu.get_candidate(i) = entries[i]).  R27: the uniform of the i-th
+ * enumerated element uses counter (0x40000000 | i>>2, s, a, it), word i&3 --
+ * the same counter as the bitmask scan, whose i-th element is city i.
+ * argmax key, ties -> lowest node id (R16). */
+ORC_EXPORT int32_t orc_select_next_ct(const float *inv_w_row, const int32_t *entries, int32_t L, int32_t s,
+                                      uint32_t a, uint32_t it, const uint32_t key[2])
+{
+    int32_t best = -1;
+    float best_key = -INFINITY;
+    for (int32_t i = 0; i < L; ++i) {
+        int32_t v = entries[i];
+        float u = rng_word(key, 0x40000000u | ((uint32_t)i >> 2), (uint32_t)s, a, it, i & 3);
+        float kk = orc_det_log2(u) * inv_w_row[v];
+        if (best < 0 || kk > best_key || (kk == best_key && v < best)) {
+            best = v;
             best_key = kk;
         }
     }
@@ -512,6 +564,22 @@ static int64_t build_route(const orc_t *o, int32_t a, int32_t *route, char *vis)
     int32_t cur = orc_start_node(n, (uint32_t)a, (uint32_t)o->iter, o->key);
     route[0] = cur;
     vis[cur] = 1;
+    if (o->p.tabu == 1) {
+        /* MMAS-WRS-CT (cl = 0): the list of unvisited nodes is the CT's left part */
+        int32_t *entries = malloc(sizeof(int32_t) * (size_t)n), L;
+        orc_ct_init(entries, &L, n);
+        orc_ct_mark(entries, &L, n, cur);
+        for (int32_t s = 1; s < n; ++s) {
+            int32_t nxt = orc_select_next_ct(o->inv_w + (size_t)cur * n, entries, L, s, (uint32_t)a,
+                                             (uint32_t)o->iter, o->key);
+            orc_ct_mark(entries, &L, n, nxt);
+            route[s] = nxt;
+            cur = nxt;
+        }
+        free(entries);
+        if (o->p.local_search) orc_two_opt(o->xy, n, o->ls_nn, o->ls_k, route, NULL);
+        return 0;
+    }
     for (int32_t s = 1; s < n; ++s) {
         int32_t f;
         int32_t nxt = orc_select_next(o->inv_w + (size_t)cur * n, o->cand + (size_t)cur * o->p.cl,
