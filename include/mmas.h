@@ -42,6 +42,13 @@ typedef enum mmas_status {
 
 enum { MMAS_DEPOSIT_ITERATION_BEST = 0, MMAS_DEPOSIT_GLOBAL_BEST = 1 }; /* Alg.1 l.288 / P:332-333 (R7) */
 enum { MMAS_FALLBACK_WRS = 0, MMAS_FALLBACK_ARGMAX = 1 };               /* R9 */
+/* Tabu of the full-row path (Sec. 4.1, Tab. 1; R27): the bitmask tabu (BT,
+ * default, every step scans all n nodes) or the compact tabu (CT, the
+ * paper's recommendation without candidate lists P:1998-2001: step s enumerates only
+ * the n-s unvisited nodes, and the i-th enumerated node draws the uniform the bitmask
+ * scan gives city i -- so the two modes sample the same distribution but different
+ * tours).  COMPACT requires cand_len == 0. */
+enum { MMAS_TABU_BITMASK = 0, MMAS_TABU_COMPACT = 1 };
 
 /* Full configuration (mmas_config_init() fills the defaults). */
 typedef struct mmas_config {
@@ -64,6 +71,7 @@ typedef struct mmas_config {
     int32_t use_caller_stream; /* 1: run on `stream` even when it is NULL (the legacy default
                               stream, e.g. torch's default stream); 0 (default): run on `stream`
                               if non-NULL, else on a non-blocking stream owned by the context */
+    int32_t tabu;          /* MMAS_TABU_*; default BITMASK.  COMPACT needs cand_len == 0 (R27) */
 } mmas_config;
 
 /* Per-context counters (cumulative since create). */

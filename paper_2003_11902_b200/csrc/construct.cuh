@@ -643,4 +643,117 @@ __global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
     block_finish(A, wbest, 0, lane, warp);
 }
 
+
+
+// ---------------------------------------------------------------------------
+// Full-row construction over the compact tabu (MMAS-WRS-CT, SURVEY NEXT-2,
+// DESIGN.md R27; cl = 0 with tabu = COMPACT).  One warp per ant; the CT's
+// `entries` (n u16) live in shared memory.  Step s enumerates the
+// L = n - s unvisited nodes entries[0..L) (Alg. 3 with l = tabu.length(),
+// P:964-994): lane l takes the 4-position groups 128t + 4l, one Philox per group
+// (word j = position 4g+j's uniform, counter (0x40000000 | g, s, a, it)), and
+// gathers inv_w[cur][v] for the four nodes.  Work per step is L instead of n, so
+// a tour costs ~n^2/2 keys instead of n^2 ("direct access to the
+// list of nodes to visit").  Keys compare as (magnitude, node), ties -> lowest
+// node id (R16), because list order is not node order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ct_group(uint2 e, float4 iv, int p0, int L, uint32_t step, uint32_t ant,
+                                         uint32_t iter, PhiloxKey key, uint32_t& best_mag, uint32_t& best_c) {
+    const uint4 x = philox4x32_10(ctr_city((uint32_t)p0 >> 2, step, ant, iter), key);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+    const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
+    const uint32_t vs[4] = {e.x & 0xFFFFu, e.x >> 16, e.y & 0xFFFFu, e.y >> 16};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float k = __fmul_rn(det_log2(uniform_open(xs[j])), ivs[j]);
+        const bool ok = p0 + j < L;
+        const uint32_t mag = ok ? key_magnitude(k) : kNone;
+        const uint32_t v = ok ? vs[j] : kNone;
+        if (mag < best_mag || (mag == best_mag && v < best_c)) {
+            best_mag = mag;
+            best_c = v;
+        }
+    }
+}
+
+// positions p0 .. p0+3 of the list: their nodes (u16 pairs) and inv_w[cur][node]
+__device__ __forceinline__ void ct_load(const uint16_t* ent, const float* __restrict__ row, int p0, int L, uint2& e,
+                                        float4& iv) {
+    e = *reinterpret_cast<const uint2*>(ent + p0);
+    iv.x = p0 + 0 < L ? __ldg(row + (e.x & 0xFFFFu)) : 0.f;
+    iv.y = p0 + 1 < L ? __ldg(row + (e.x >> 16)) : 0.f;
+    iv.z = p0 + 2 < L ? __ldg(row + (e.y & 0xFFFFu)) : 0.f;
+    iv.w = p0 + 3 < L ? __ldg(row + (e.y >> 16)) : 0.f;
+}
+
+// CT mark(u), by one lane; L = list length before the mark.
+__device__ __forceinline__ void ct_mark(uint16_t* ent, int L, int n, uint32_t u) {
+    const uint32_t last = (uint32_t)L - 1u;
+    const uint32_t t = ent[last];
+    const uint32_t iu = u < (uint32_t)L ? u : ent[u];
+    if (iu == last) {
+        ent[iu] = (uint16_t)n;
+    } else {
+        ent[iu] = (uint16_t)t;
+        ent[t] = (uint16_t)iu;
+    }
+}
+
+__global__ void __launch_bounds__(128) construct_ct_kernel(ConstructArgs A) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int n = A.n;
+    const int ent_len = (n + 255) & ~255;                 // padded: a trip may read past L
+    uint16_t* ent = reinterpret_cast<uint16_t*>(g_smem + 128) + (size_t)warp * ent_len;
+    const uint32_t iter = *A.iter_dev;
+    unsigned long long wbest = ~0ull;
+
+    for (int al = blockIdx.x * A.warps_per_block + warp; al < A.m_local; al += gridDim.x * A.warps_per_block) {
+        const uint32_t ant = (uint32_t)(A.ant_lo + al);
+        for (int i = lane; i < n; i += 32) ent[i] = (uint16_t)i;
+        __syncwarp();
+        const uint32_t start = __umulhi(philox4x32_10(ctr_start(ant, iter), A.key).x, (uint32_t)n);
+        if (lane == 0) ct_mark(ent, n, n, start);
+        __syncwarp();
+        uint16_t* route = A.routes + (size_t)al * A.ldr;
+        uint32_t stage = (lane == 0) ? start : 0u;
+        uint32_t cur = start;
+        for (int s = 1; s < n; ++s) {
+            const int L = n - s;
+            const float* row = A.inv_w + (size_t)cur * A.ld;
+            uint32_t bm = kNone, bc = kNone;
+            // the next trip's list entries and inv_w gathers are loaded one trip ahead
+            uint2 ea, eb;
+            float4 iva, ivb;
+            ct_load(ent, row, 4 * lane, L, ea, iva);
+            ct_load(ent, row, 4 * lane + 128, L, eb, ivb);
+            for (int base = 0; base < L; base += 256) {
+                uint2 ea2 = ea, eb2 = eb;
+                float4 iva2 = iva, ivb2 = ivb;
+                if (base + 256 < L) {
+                    ct_load(ent, row, base + 256 + 4 * lane, L, ea2, iva2);
+                    ct_load(ent, row, base + 384 + 4 * lane, L, eb2, ivb2);
+                }
+                const int pa = base + 4 * lane;
+                if (pa < L) ct_group(ea, iva, pa, L, (uint32_t)s, ant, iter, A.key, bm, bc);
+                if (pa + 128 < L) ct_group(eb, ivb, pa + 128, L, (uint32_t)s, ant, iter, A.key, bm, bc);
+                ea = ea2;
+                eb = eb2;
+                iva = iva2;
+                ivb = ivb2;
+            }
+            const uint32_t nxt = warp_select(bm, bc);
+            if (lane == 0) ct_mark(ent, L, n, nxt);
+            stage_route(route, s, nxt, lane, stage);
+            __syncwarp();
+            cur = nxt;
+        }
+        flush_route(route, n, lane, stage);
+        __syncwarp();
+        if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane));
+    }
+    block_finish(A, wbest, 0, lane, warp);
+}
+
 }  // namespace mmas

@@ -134,6 +134,7 @@ struct mmas_ctx {
     bool smem_table = false;
 
     bool reg_tabu = false;   // n <= 1024: tabu words in registers
+    bool compact_tabu = false;  // cl == 0 with MMAS_TABU_COMPACT: construct_ct_kernel (R27)
     int slots = 1;
     int cons_warps = 4, cons_grid = 1;
     size_t cons_smem = 0;
@@ -276,9 +277,20 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Raise a kernel's dynamic shared-memory limit to the opt-in maximum (minus its static
+// shared memory).  Always the maximum, never the context's own need: the attribute is
+// per function and process-wide, so a smaller value set by a later context would break
+// the launches of an earlier, larger one.  (Occupancy follows the launch's actual size.)
+template <class K>
+void allow_max_smem(K* kernel, int optin) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kernel);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+}
+
 template <int S, bool T, bool R, bool F = false>
-void set_smem_attr(size_t bytes) {
-    cudaFuncSetAttribute(construct_cl_kernel<S, T, R, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+void set_smem_attr(int optin) {
+    allow_max_smem(construct_cl_kernel<S, T, R, F>, optin);
 }
 
 template <int S, bool T, bool R, bool F>
@@ -312,7 +324,7 @@ void launch_cl_r(mmas_ctx* h, const ConstructArgs& A) {
 }
 
 template <bool R>
-void set_cl_attrs(size_t bytes) {
+void set_cl_attrs(int bytes) {
     set_smem_attr<1, true, R>(bytes); set_smem_attr<1, false, R>(bytes);
     set_smem_attr<1, true, R, true>(bytes); set_smem_attr<1, false, R, true>(bytes);
     set_smem_attr<2, true, R>(bytes); set_smem_attr<2, false, R>(bytes);
@@ -320,6 +332,16 @@ void set_cl_attrs(size_t bytes) {
 }
 
 int launch_two_opt(mmas_ctx* h, bool fuse_select);
+
+// full-row construction (cl == 0): compact-tabu list or bitmask scan
+void launch_full(mmas_ctx* h, const ConstructArgs& A) {
+    if (h->compact_tabu)
+        construct_ct_kernel<<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+    else if (h->reg_tabu)
+        construct_full_kernel<true><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+    else
+        construct_full_kernel<false><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+}
 
 // Construction (rows a1-a4) -- and, with local search on, the 2-opt pass (row a8) that
 // then owns the tour lengths and the iteration-best bookkeeping (row a5).
@@ -330,10 +352,7 @@ int launch_construct(mmas_ctx* h, bool fuse_select) {
             PhaseScope ps(h, 0);
             ConstructArgs A = construct_args(h, false, true);
             if (h->cl == 0) {
-                if (h->reg_tabu)
-                    construct_full_kernel<true><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
-                else
-                    construct_full_kernel<false><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+                launch_full(h, A);
             } else if (h->reg_tabu) {
                 launch_cl_r<true>(h, A);
             } else {
@@ -347,10 +366,7 @@ int launch_construct(mmas_ctx* h, bool fuse_select) {
     PhaseScope ps(h, 0);
     ConstructArgs A = construct_args(h, fuse_select);
     if (h->cl == 0) {
-        if (h->reg_tabu)
-            construct_full_kernel<true><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
-        else
-            construct_full_kernel<false><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+        launch_full(h, A);
     } else if (h->reg_tabu) {
         launch_cl_r<true>(h, A);
     } else {
@@ -561,6 +577,9 @@ int setup(mmas_ctx* h) {
     }
 
     // ---- construction launch plan ----
+    // dynamic shared memory a construction kernel may take: the opt-in limit minus its
+    // static shared memory (block_finish's slots; 128 B, reserve 1 KB)
+    const size_t cons_dyn_max = (size_t)h->smem_optin - 1024;
     const int nwords = round_up((n + 31) / 32, 4);
     h->reg_tabu = n <= 1024;
     const size_t tabu_bytes = h->reg_tabu ? 0 : (size_t)nwords * 4;
@@ -572,7 +591,7 @@ int setup(mmas_ctx* h) {
         // one block per SM holding the whole table; as many ant warps as needed
         int w = std::max(1, std::min(8, (h->m_local + h->num_sms - 1) / std::max(h->num_sms, 1)));
         size_t need = 128 + (size_t)h->tb_inv + h->tb_id + 16 + (size_t)w * per_warp;
-        h->smem_table = need <= (size_t)h->smem_optin;
+        h->smem_table = need <= cons_dyn_max;
         if (h->smem_table) {
             h->cons_warps = w;
             h->cons_grid = std::max(1, (h->m_local + w - 1) / w);
@@ -582,19 +601,29 @@ int setup(mmas_ctx* h) {
             h->cons_grid = std::max(1, (h->m_local + 3) / 4);
             h->cons_smem = 128 + 16 + 4 * per_warp;
         }
+    } else if (h->cfg.tabu == MMAS_TABU_COMPACT) {
+        // CT entries: n u16 per ant warp, padded to 256 positions (one scan trip)
+        h->compact_tabu = true;
+        const size_t ent_bytes = (size_t)round_up(n, 256) * 2;
+        int w = 4;
+        while (w > 1 && 128 + (size_t)w * ent_bytes > cons_dyn_max) --w;
+        h->cons_warps = w;
+        h->cons_grid = std::max(1, (h->m_local + w - 1) / w);
+        h->cons_smem = 128 + (size_t)w * ent_bytes;
     } else {
         h->cons_warps = 4;
         h->cons_grid = std::max(1, (h->m_local + 3) / 4);
         h->cons_smem = 128 + 4 * tabu_bytes;
     }
-    if (h->cons_smem > (size_t)h->smem_optin)
+    if (h->cons_smem > cons_dyn_max)
         return fail(MMAS_EINVAL, "n too large for the shared-memory tabu of one block");
     if (h->cl > 0) {
-        if (h->reg_tabu) set_cl_attrs<true>(h->cons_smem);
-        else set_cl_attrs<false>(h->cons_smem);
+        if (h->reg_tabu) set_cl_attrs<true>(h->smem_optin);
+        else set_cl_attrs<false>(h->smem_optin);
     } else {
-        cudaFuncSetAttribute(construct_full_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->cons_smem);
-        cudaFuncSetAttribute(construct_full_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->cons_smem);
+        allow_max_smem(construct_full_kernel<true>, h->smem_optin);
+        allow_max_smem(construct_full_kernel<false>, h->smem_optin);
+        allow_max_smem(construct_ct_kernel, h->smem_optin);
     }
     {
         cudaFuncAttributes fa{};
@@ -602,8 +631,7 @@ int setup(mmas_ctx* h) {
         h->ls_coop_smem_max = h->smem_optin - (int)fa.sharedSizeBytes;   // dynamic = opt-in limit - static
         cudaFuncSetAttribute(two_opt_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->ls_coop_smem_max);
     }
-    cudaFuncSetAttribute(pheromone_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(float) * (size_t)h->ld));
+    allow_max_smem(pheromone_update_kernel, h->smem_optin);
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(h->stream));
     return MMAS_OK;
@@ -625,6 +653,10 @@ int validate(const mmas_config* c) {
     if (c->fallback != MMAS_FALLBACK_WRS && c->fallback != MMAS_FALLBACK_ARGMAX)
         return fail(MMAS_EINVAL, "fallback must be MMAS_FALLBACK_*");
     if (c->local_search != 0 && c->local_search != 1) return fail(MMAS_EINVAL, "local_search must be 0 or 1");
+    if (c->tabu != MMAS_TABU_BITMASK && c->tabu != MMAS_TABU_COMPACT)
+        return fail(MMAS_EINVAL, "tabu must be MMAS_TABU_*");
+    if (c->tabu == MMAS_TABU_COMPACT && c->cand_len != 0)
+        return fail(MMAS_EINVAL, "tabu = MMAS_TABU_COMPACT requires cand_len == 0 (R27)");
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(MMAS_EINVAL, "need 0 <= rank < world");
     double lo_x = INFINITY, hi_x = -INFINITY, lo_y = INFINITY, hi_y = -INFINITY;
     for (int i = 0; i < c->n; ++i) {

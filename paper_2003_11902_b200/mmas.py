@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libmmas.so")
 MMAS_OK, MMAS_EINVAL, MMAS_ENOMEM, MMAS_ECUDA, MMAS_ENCCL, MMAS_ESTATE = 0, -1, -2, -3, -4, -5
 DEPOSIT_ITERATION_BEST, DEPOSIT_GLOBAL_BEST = 0, 1
 FALLBACK_WRS, FALLBACK_ARGMAX = 0, 1
+TABU_BITMASK, TABU_COMPACT = 0, 1
 
 # every symbol include/mmas.h declares (checked by tests/test_capi.py)
 EXPORTED = (
@@ -43,6 +44,7 @@ class Config(ctypes.Structure):
         ("p_best", ctypes.c_double), ("deposit", ctypes.c_int32), ("fallback", ctypes.c_int32),
         ("local_search", ctypes.c_int32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
         ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("use_caller_stream", ctypes.c_int32),
+        ("tabu", ctypes.c_int32),
     ]
 
 
@@ -124,7 +126,7 @@ class Colony:
 
     def __init__(self, coords, n_ants, cand_len, alpha=1.0, beta=2.0, rho=0.5, seed=42, p_best=0.01,
                  deposit_global=False, fallback_argmax=False, local_search=False, device=-1, stream=None,
-                 rank=0, world=1):
+                 rank=0, world=1, tabu=TABU_BITMASK):
         L = lib()
         c = np.ascontiguousarray(coords, dtype=np.float64).reshape(-1, 2)
         self.n = c.shape[0]
@@ -148,6 +150,7 @@ class Colony:
         cfg.stream = stream if stream else None
         cfg.use_caller_stream = 0 if stream is None else 1
         cfg.rank, cfg.world = int(rank), int(world)
+        cfg.tabu = int(tabu)
         h = ctypes.c_void_p()
         _err(L.mmas_create_ex(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h

@@ -47,6 +47,8 @@ def test_built_for_sm100a():
     (dict(n_ants=0), "n_ants"),
     (dict(beta=-1.0), "beta"),
     (dict(local_search=2), "local_search"),
+    (dict(tabu=2), "tabu"),
+    (dict(tabu=1), "cand_len == 0"),          # compact tabu needs the full-row path (R27)
     (dict(world=2, rank=2), "rank"),
 ])
 def test_invalid_arguments_rejected_without_gpu(L, kw, frag):

@@ -10,11 +10,14 @@ from paper_2003_11902_b200 import mmas  # noqa: E402
 from paper_2003_11902_b200.instances import CONFIGS  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+tabu = 0
+if cfg.endswith(":ct"):   # full-row configs over the compact tabu (R27)
+    cfg, tabu = cfg[:-3], mmas.TABU_COMPACT
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 300
 w = CONFIGS[cfg]
 s = torch.cuda.current_stream().cuda_stream
 col = mmas.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, stream=s,
-                  local_search=bool(w.local_search))
+                  local_search=bool(w.local_search), tabu=tabu)
 col.iterate(20)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
