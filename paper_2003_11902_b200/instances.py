@@ -102,6 +102,7 @@ class Workload:
     alpha: float = 1.0
     beta: float = 2.0
     mmas_seed: int = 42
+    tabu: int = 0         # full-row tabu: 0 = bitmask (BT), 1 = compact (CT, R27)
 
     def coords(self) -> np.ndarray:
         return make_coords(self.shape, self.n, self.seed)
@@ -129,5 +130,7 @@ CONFIGS = {
     "C2": Workload("pr1002-shaped", 1002, 1002, 32, 1000, 0.5, 0, "pr1002", 1002),
     "C3": Workload("fl3795-shaped", 3795, 3795, 32, 100, 0.5, 0, "fl3795", 3795),
     "C4": Workload("pr2392-shaped", 2392, 2392, 0, 100, 0.5, 0, "pr2392", 2392),
+    # C4 over the compact tabu (MMAS-WRS-CT, the paper's choice without candidate lists)
+    "C4CT": Workload("pr2392-shaped, compact tabu", 2392, 2392, 0, 100, 0.5, 0, "pr2392", 2392, tabu=1),
     "C5": Workload("d18512-shaped", 18512, 800, 32, 20, 0.7, 1, "d18512", 18512),
 }
