@@ -657,8 +657,11 @@ __global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
 // list of nodes to visit").  Keys compare as (magnitude, node), ties -> lowest
 // node id (R16), because list order is not node order.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void ct_group(uint2 e, float4 iv, int p0, int L, uint32_t step, uint32_t ant,
-                                         uint32_t iter, PhiloxKey key, uint32_t& best_mag, uint32_t& best_c) {
+// Positions >= L get inv_w = +inf: their key is -inf, whose magnitude 0x7F800000 loses
+// to every real key (det_log2 < 0 and finite on the u-grid, inv_w finite), and L >= 1
+// guarantees a real key in the warp -- so the select needs no position mask.
+__device__ __forceinline__ void ct_group(uint2 e, float4 iv, int p0, uint32_t step, uint32_t ant, uint32_t iter,
+                                         PhiloxKey key, uint32_t& best_mag, uint32_t& best_c) {
     const uint4 x = philox4x32_10(ctr_city((uint32_t)p0 >> 2, step, ant, iter), key);
     const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
     const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
@@ -666,24 +669,38 @@ __device__ __forceinline__ void ct_group(uint2 e, float4 iv, int p0, int L, uint
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const float k = __fmul_rn(det_log2(uniform_open(xs[j])), ivs[j]);
-        const bool ok = p0 + j < L;
-        const uint32_t mag = ok ? key_magnitude(k) : kNone;
-        const uint32_t v = ok ? vs[j] : kNone;
-        if (mag < best_mag || (mag == best_mag && v < best_c)) {
-            best_mag = mag;
-            best_c = v;
-        }
+        const uint32_t mag = key_magnitude(k);
+        // branch-free (mag, node) lexicographic minimum
+        const bool better = (mag < best_mag) | ((mag == best_mag) & (vs[j] < best_c));
+        best_c = better ? vs[j] : best_c;
+        best_mag = min(best_mag, mag);
     }
 }
 
 // positions p0 .. p0+3 of the list: their nodes (u16 pairs) and inv_w[cur][node]
 __device__ __forceinline__ void ct_load(const uint16_t* ent, const float* __restrict__ row, int p0, int L, uint2& e,
                                         float4& iv) {
+    const float inf = __int_as_float(0x7F800000);
     e = *reinterpret_cast<const uint2*>(ent + p0);
-    iv.x = p0 + 0 < L ? __ldg(row + (e.x & 0xFFFFu)) : 0.f;
-    iv.y = p0 + 1 < L ? __ldg(row + (e.x >> 16)) : 0.f;
-    iv.z = p0 + 2 < L ? __ldg(row + (e.y & 0xFFFFu)) : 0.f;
-    iv.w = p0 + 3 < L ? __ldg(row + (e.y >> 16)) : 0.f;
+    iv.x = p0 + 0 < L ? __ldg(row + (e.x & 0xFFFFu)) : inf;
+    iv.y = p0 + 1 < L ? __ldg(row + (e.x >> 16)) : inf;
+    iv.z = p0 + 2 < L ? __ldg(row + (e.y & 0xFFFFu)) : inf;
+    iv.w = p0 + 3 < L ? __ldg(row + (e.y >> 16)) : inf;
+}
+
+// one 256-position trip: lane l's groups base+4l and base+128+4l
+__device__ __forceinline__ void ct_trip(const uint2 (&e)[2], const float4 (&iv)[2], int base, int lane, int L,
+                                        uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
+                                        uint32_t& best_mag, uint32_t& best_c) {
+    const int pa = base + 4 * lane;
+    if (pa < L) ct_group(e[0], iv[0], pa, step, ant, iter, key, best_mag, best_c);
+    if (pa + 128 < L) ct_group(e[1], iv[1], pa + 128, step, ant, iter, key, best_mag, best_c);
+}
+
+__device__ __forceinline__ void ct_load_trip(const uint16_t* ent, const float* __restrict__ row, int base, int lane,
+                                             int L, uint2 (&e)[2], float4 (&iv)[2]) {
+    ct_load(ent, row, base + 4 * lane, L, e[0], iv[0]);
+    ct_load(ent, row, base + 128 + 4 * lane, L, e[1], iv[1]);
 }
 
 // CT mark(u), by one lane; L = list length before the mark.
@@ -724,24 +741,16 @@ __global__ void __launch_bounds__(128) construct_ct_kernel(ConstructArgs A) {
             const float* row = A.inv_w + (size_t)cur * A.ld;
             uint32_t bm = kNone, bc = kNone;
             // the next trip's list entries and inv_w gathers are loaded one trip ahead
-            uint2 ea, eb;
-            float4 iva, ivb;
-            ct_load(ent, row, 4 * lane, L, ea, iva);
-            ct_load(ent, row, 4 * lane + 128, L, eb, ivb);
-            for (int base = 0; base < L; base += 256) {
-                uint2 ea2 = ea, eb2 = eb;
-                float4 iva2 = iva, ivb2 = ivb;
-                if (base + 256 < L) {
-                    ct_load(ent, row, base + 256 + 4 * lane, L, ea2, iva2);
-                    ct_load(ent, row, base + 384 + 4 * lane, L, eb2, ivb2);
-                }
-                const int pa = base + 4 * lane;
-                if (pa < L) ct_group(ea, iva, pa, L, (uint32_t)s, ant, iter, A.key, bm, bc);
-                if (pa + 128 < L) ct_group(eb, ivb, pa + 128, L, (uint32_t)s, ant, iter, A.key, bm, bc);
-                ea = ea2;
-                eb = eb2;
-                iva = iva2;
-                ivb = ivb2;
+            // (two register sets, loop unrolled by two so no copies are needed)
+            uint2 eA[2], eB[2];
+            float4 ivA[2], ivB[2];
+            ct_load_trip(ent, row, 0, lane, L, eA, ivA);
+            for (int base = 0; base < L; base += 512) {
+                if (base + 256 < L) ct_load_trip(ent, row, base + 256, lane, L, eB, ivB);
+                ct_trip(eA, ivA, base, lane, L, (uint32_t)s, ant, iter, A.key, bm, bc);
+                if (base + 256 >= L) break;
+                if (base + 512 < L) ct_load_trip(ent, row, base + 512, lane, L, eA, ivA);
+                ct_trip(eB, ivB, base + 256, lane, L, (uint32_t)s, ant, iter, A.key, bm, bc);
             }
             const uint32_t nxt = warp_select(bm, bc);
             if (lane == 0) ct_mark(ent, L, n, nxt);
