@@ -31,7 +31,7 @@ class _Params(ctypes.Structure):
         ("p_best", ctypes.c_double), ("seed", ctypes.c_uint64),
         ("deposit_global", ctypes.c_int32), ("fallback_argmax", ctypes.c_int32),
         ("local_search", ctypes.c_int32), ("nthreads", ctypes.c_int32),
-        ("tabu", ctypes.c_int32),
+        ("tabu", ctypes.c_int32), ("selection", ctypes.c_int32),
     ]
 
 
@@ -76,6 +76,8 @@ def lib():
         L.orc_select_next.restype = ctypes.c_int32
         L.orc_start_node.argtypes = [ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint32, P(ctypes.c_uint32)]
         L.orc_start_node.restype = ctypes.c_int32
+        L.orc_prwm.argtypes = [P(ctypes.c_float), ctypes.c_int32, ctypes.c_float]
+        L.orc_prwm.restype = ctypes.c_int32
         L.orc_ct_init.argtypes = [P(ctypes.c_int32), P(ctypes.c_int32), ctypes.c_int32]
         L.orc_ct_mark.argtypes = [P(ctypes.c_int32), P(ctypes.c_int32), ctypes.c_int32, ctypes.c_int32]
         L.orc_select_next_ct.argtypes = [P(ctypes.c_float), P(ctypes.c_int32), ctypes.c_int32, ctypes.c_int32,
@@ -248,6 +250,12 @@ def select_next_ct(inv_w_row, entries, L, s, a, it, seed):
                                     _ptr(key, ctypes.c_uint32))
 
 
+def prwm(weights, u):
+    """Parallel roulette wheel over `weights` with uniform u (R28); -1 if all are 0."""
+    w = np.ascontiguousarray(weights, dtype=np.float32)
+    return lib().orc_prwm(_ptr(w, ctypes.c_float), len(w), float(np.float32(u)))
+
+
 def start_node(n, a, it, seed):
     key = np.array([seed & 0xFFFFFFFF, seed >> 32], dtype=np.uint32)
     return lib().orc_start_node(n, a, it, _ptr(key, ctypes.c_uint32))
@@ -259,7 +267,7 @@ class Colony:
 
     def __init__(self, coords, n_ants, cand_len, alpha=1.0, beta=2.0, rho=0.5, seed=42,
                  p_best=0.01, deposit_global=False, fallback_argmax=False, local_search=False,
-                 nthreads=None, tabu=0):
+                 nthreads=None, tabu=0, selection=0):
         c = np.ascontiguousarray(coords, dtype=np.float64).reshape(-1, 2)
         self.coords = c
         self.n = c.shape[0]
@@ -269,7 +277,7 @@ class Colony:
             nthreads = os.cpu_count() or 1
         p = _Params(self.n, self.m, self.cl, float(alpha), float(beta), float(rho), float(p_best),
                     int(seed) & 0xFFFFFFFFFFFFFFFF, int(deposit_global), int(fallback_argmax),
-                    int(local_search), int(nthreads), int(tabu))
+                    int(local_search), int(nthreads), int(tabu), int(selection))
         flat = c.ravel()
         h = lib().orc_create(ctypes.byref(p), _ptr(flat, ctypes.c_double))
         if not h:

@@ -199,6 +199,7 @@ typedef struct {
     int32_t local_search;     /* a8: 2-opt on every route (R25) */
     int32_t nthreads;
     int32_t tabu;             /* R27: 0 = bitmask tabu BT (default), 1 = compact tabu CT (cl = 0 only) */
+    int32_t selection;        /* R28: 0 = WRS (Sec. 4.2.2, default), 1 = parallel roulette wheel PRWM (Sec. 4.2.1) */
 } orc_params;
 
 typedef struct {
@@ -281,6 +282,7 @@ ORC_EXPORT orc_t *orc_create(const orc_params *p, const double *coords)
     if (!is_int_in(p->alpha, 0, 8) || p->beta < 0.0) return NULL;
     if (!(p->p_best > 0.0 && p->p_best < 1.0)) return NULL;
     if (p->tabu < 0 || p->tabu > 1 || (p->tabu == 1 && p->cl != 0)) return NULL;   /* R27 */
+    if (p->selection < 0 || p->selection > 1) return NULL;                          /* R28 */
     for (int32_t i = 0; i < 2 * p->n; ++i)
         if (!isfinite(coords[i])) return NULL;
 
@@ -437,6 +439,89 @@ ORC_EXPORT int32_t orc_select_next_ct(const float *inv_w_row, const int32_t *ent
     return best;
 }
 
+/* ------------------------------------------------------------------------- */
+/* Parallel roulette wheel PRWM (Sec. 4.2.1; reading R28), p = 32.  */
+/* Items 0..len-1 with weights w[i] >= 0 (0 = visited).  One stage over items  */
+/* [lo, hi): chunk size c = ceil((hi-lo)/p); thread t owns [lo+t c, lo+(t+1)c) */
+/* and sums its weights in item order ("computes a sum of the corresponding    */
+/* weights"); an inclusive prefix sum of the p chunk sums ("computed in        */
+/* parallel": the Hillis-Steele scan, R28); the first stage draws r = u*total  */
+/* ("the last thread draws a uniform random number and multiplies it by the    */
+/* total"); the winning chunk is the first t with prefix[t] > r; r is reduced  */
+/* by the preceding chunks' prefix and the stage repeats on the winning chunk  */
+/* until it holds one item ("up to ceil(log_p n) stages").  If rounding leaves */
+/* r >= prefix[p-1], the last chunk with a positive sum wins.                  */
+/* Returns the selected item, or -1 when every weight is 0.                    */
+/* ------------------------------------------------------------------------- */
+#define ORC_P 32
+ORC_EXPORT int32_t orc_prwm(const float *w, int32_t len, float u)
+{
+    int32_t lo = 0, hi = len;
+    float r = 0.0f;
+    int first = 1;
+    do {
+        int32_t c = (hi - lo + ORC_P - 1) / ORC_P;
+        float sum[ORC_P], pre[ORC_P], nxt[ORC_P];
+        for (int32_t t = 0; t < ORC_P; ++t) {
+            float acc = 0.0f;
+            for (int32_t i = lo + t * c; i < lo + (t + 1) * c && i < hi; ++i) acc = acc + w[i];
+            sum[t] = acc;
+            pre[t] = acc;
+        }
+        /* Hillis-Steele inclusive scan: log2(p) rounds, pre[t] += pre[t - d] */
+        for (int32_t d = 1; d < ORC_P; d *= 2) {
+            for (int32_t t = 0; t < ORC_P; ++t) nxt[t] = t >= d ? pre[t] + pre[t - d] : pre[t];
+            memcpy(pre, nxt, sizeof(pre));
+        }
+        if (first) {
+            if (pre[ORC_P - 1] == 0.0f) return -1;
+            r = u * pre[ORC_P - 1];
+            first = 0;
+        }
+        int32_t win = -1;
+        for (int32_t t = 0; t < ORC_P; ++t)
+            if (pre[t] > r) { win = t; break; }
+        if (win < 0)
+            for (int32_t t = ORC_P - 1; t >= 0; --t)
+                if (sum[t] > 0.0f) { win = t; break; }
+        if (win > 0) r = r - pre[win - 1];
+        lo = lo + win * c;
+        hi = lo + c < hi ? lo + c : hi;
+    } while (hi - lo > 1);
+    return lo;
+}
+
+/* weight of edge (i, j) for the roulette wheel: choice_info = tau^alpha * eta^beta */
+static float rwm_weight(const orc_t *o, int32_t i, int32_t j)
+{
+    size_t e = (size_t)i * o->p.n + j;
+    return pow_alpha(o->tau[e], (int32_t)o->p.alpha) * o->heur[e];
+}
+
+/* One PRWM construction step: candidate list first (cl > 0), else / on fallback
+ * all nodes with visited weights 0 (BT) or the CT's list (R27).  One uniform per
+ * step: counter (0x20000000, s, a, it), word 0 (R28). */
+static int32_t select_next_rwm(const orc_t *o, int32_t cur, const char *vis, const int32_t *entries, int32_t L,
+                               int32_t s, uint32_t a, float *wbuf, int32_t *fell_back)
+{
+    int32_t n = o->p.n, cl = o->p.cl;
+    float u = rng_word(o->key, 0x20000000u, (uint32_t)s, a, (uint32_t)o->iter, 0);
+    *fell_back = 0;
+    if (cl > 0) {
+        const int32_t *cand = o->cand + (size_t)cur * cl;
+        for (int32_t k = 0; k < cl; ++k) wbuf[k] = vis[cand[k]] ? 0.0f : rwm_weight(o, cur, cand[k]);
+        int32_t k = orc_prwm(wbuf, cl, u);
+        if (k >= 0) return cand[k];
+        *fell_back = 1;
+    }
+    if (entries) {
+        for (int32_t i = 0; i < L; ++i) wbuf[i] = rwm_weight(o, cur, entries[i]);
+        return entries[orc_prwm(wbuf, L, u)];
+    }
+    for (int32_t c = 0; c < n; ++c) wbuf[c] = vis[c] ? 0.0f : rwm_weight(o, cur, c);
+    return orc_prwm(wbuf, n, u);
+}
+
 /* Start node u ~ U{0, n-1} (Alg. 1): counter (0x80000000, 0, a, it), word 0,
  * start = floor(x * n / 2^32). */
 ORC_EXPORT int32_t orc_start_node(int32_t n, uint32_t a, uint32_t it, const uint32_t key[2])
@@ -564,6 +649,29 @@ static int64_t build_route(const orc_t *o, int32_t a, int32_t *route, char *vis)
     int32_t cur = orc_start_node(n, (uint32_t)a, (uint32_t)o->iter, o->key);
     route[0] = cur;
     vis[cur] = 1;
+    if (o->p.selection == 1) {
+        /* MMAS-RWM (R28): parallel roulette wheel over the candidate list / BT / CT */
+        float *wbuf = malloc(sizeof(float) * (size_t)n);
+        int32_t *entries = NULL, L = 0;
+        if (o->p.tabu == 1) {
+            entries = malloc(sizeof(int32_t) * (size_t)n);
+            orc_ct_init(entries, &L, n);
+            orc_ct_mark(entries, &L, n, cur);
+        }
+        for (int32_t s = 1; s < n; ++s) {
+            int32_t f;
+            int32_t nxt = select_next_rwm(o, cur, vis, entries, L, s, (uint32_t)a, wbuf, &f);
+            fb += f;
+            if (entries) orc_ct_mark(entries, &L, n, nxt);
+            route[s] = nxt;
+            vis[nxt] = 1;
+            cur = nxt;
+        }
+        free(wbuf);
+        free(entries);
+        if (o->p.local_search) orc_two_opt(o->xy, n, o->ls_nn, o->ls_k, route, NULL);
+        return fb;
+    }
     if (o->p.tabu == 1) {
         /* MMAS-WRS-CT (cl = 0): the list of unvisited nodes is the CT's left part */
         int32_t *entries = malloc(sizeof(int32_t) * (size_t)n), L;
