@@ -49,6 +49,11 @@ enum { MMAS_FALLBACK_WRS = 0, MMAS_FALLBACK_ARGMAX = 1 };               /* R9 */
  * scan gives city i -- so the two modes sample the same distribution but different
  * tours).  COMPACT requires cand_len == 0. */
 enum { MMAS_TABU_BITMASK = 0, MMAS_TABU_COMPACT = 1 };
+/* Node selection (Sec. 4.2, R28): weighted reservoir sampling (WRS, Alg. 3, default) or
+ * the parallel roulette wheel (PRWM, Sec. 4.2.1) the paper compares it with --
+ * a warp-wide chunked prefix-sum wheel over choice_info = tau^alpha * eta^beta, one
+ * uniform per step.  Both follow Eq. (1); they draw different random numbers. */
+enum { MMAS_SELECT_WRS = 0, MMAS_SELECT_RWM = 1 };
 
 /* Full configuration (mmas_config_init() fills the defaults). */
 typedef struct mmas_config {
@@ -72,6 +77,7 @@ typedef struct mmas_config {
                               stream, e.g. torch's default stream); 0 (default): run on `stream`
                               if non-NULL, else on a non-blocking stream owned by the context */
     int32_t tabu;          /* MMAS_TABU_*; default BITMASK.  COMPACT needs cand_len == 0 (R27) */
+    int32_t selection;     /* MMAS_SELECT_*; default WRS (R28) */
 } mmas_config;
 
 /* Per-context counters (cumulative since create). */

@@ -283,6 +283,7 @@ ORC_EXPORT orc_t *orc_create(const orc_params *p, const double *coords)
     if (!(p->p_best > 0.0 && p->p_best < 1.0)) return NULL;
     if (p->tabu < 0 || p->tabu > 1 || (p->tabu == 1 && p->cl != 0)) return NULL;   /* R27 */
     if (p->selection < 0 || p->selection > 1) return NULL;                          /* R28 */
+    if (p->selection == 1 && p->fallback_argmax) return NULL;   /* R28: the wheel is its own fallback */
     for (int32_t i = 0; i < 2 * p->n; ++i)
         if (!isfinite(coords[i])) return NULL;
 
@@ -478,9 +479,11 @@ ORC_EXPORT int32_t orc_prwm(const float *w, int32_t len, float u)
             r = u * pre[ORC_P - 1];
             first = 0;
         }
+        /* a chunk with a zero sum never wins: with the scan's association its prefix can
+         * round above the previous one (R28) */
         int32_t win = -1;
         for (int32_t t = 0; t < ORC_P; ++t)
-            if (pre[t] > r) { win = t; break; }
+            if (pre[t] > r && sum[t] > 0.0f) { win = t; break; }
         if (win < 0)
             for (int32_t t = ORC_P - 1; t >= 0; --t)
                 if (sum[t] > 0.0f) { win = t; break; }

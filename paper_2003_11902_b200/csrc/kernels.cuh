@@ -191,11 +191,16 @@ struct ConstructArgs {
     int skip_finish;             // local search follows: lengths / best keys come from two_opt_kernel
     unsigned int* done;          // ants finished this launch (reset by the last warp)
     SelectArgs sel;
+    // roulette-wheel selection (R28) reads choice_info = tau^alpha * heur
+    const float* __restrict__ tau;   // n x ld
+    const float* __restrict__ heur;  // n x ld
+    int alpha;
 };
 
 }  // namespace mmas
 
 #include "construct.cuh"
+#include "rwm.cuh"
 #include "two_opt.cuh"
 
 namespace mmas {

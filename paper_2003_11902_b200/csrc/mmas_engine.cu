@@ -135,6 +135,7 @@ struct mmas_ctx {
 
     bool reg_tabu = false;   // n <= 1024: tabu words in registers
     bool compact_tabu = false;  // cl == 0 with MMAS_TABU_COMPACT: construct_ct_kernel (R27)
+    bool rwm = false;           // MMAS_SELECT_RWM: construct_rwm_kernel (R28)
     int slots = 1;
     int cons_warps = 4, cons_grid = 1;
     size_t cons_smem = 0;
@@ -255,6 +256,9 @@ ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = f
     A.lengths = h->lengths;
     A.best_key = h->best_key;
     A.fallback_count = h->fallback_count;
+    A.tau = h->tau;
+    A.heur = h->heur;
+    A.alpha = h->alpha;
     return A;
 }
 
@@ -333,9 +337,13 @@ void set_cl_attrs(int bytes) {
 
 int launch_two_opt(mmas_ctx* h, bool fuse_select);
 
-// full-row construction (cl == 0): compact-tabu list or bitmask scan
+// full-row construction (cl == 0): compact-tabu list or bitmask scan; or the roulette wheel
 void launch_full(mmas_ctx* h, const ConstructArgs& A) {
-    if (h->compact_tabu)
+    if (h->rwm && h->compact_tabu)
+        construct_rwm_kernel<true><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+    else if (h->rwm)
+        construct_rwm_kernel<false><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+    else if (h->compact_tabu)
         construct_ct_kernel<<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
     else if (h->reg_tabu)
         construct_full_kernel<true><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
@@ -351,7 +359,7 @@ int launch_construct(mmas_ctx* h, bool fuse_select) {
         {
             PhaseScope ps(h, 0);
             ConstructArgs A = construct_args(h, false, true);
-            if (h->cl == 0) {
+            if (h->cl == 0 || h->rwm) {
                 launch_full(h, A);
             } else if (h->reg_tabu) {
                 launch_cl_r<true>(h, A);
@@ -365,7 +373,7 @@ int launch_construct(mmas_ctx* h, bool fuse_select) {
     }
     PhaseScope ps(h, 0);
     ConstructArgs A = construct_args(h, fuse_select);
-    if (h->cl == 0) {
+    if (h->cl == 0 || h->rwm) {
         launch_full(h, A);
     } else if (h->reg_tabu) {
         launch_cl_r<true>(h, A);
@@ -584,7 +592,18 @@ int setup(mmas_ctx* h) {
     h->reg_tabu = n <= 1024;
     const size_t tabu_bytes = h->reg_tabu ? 0 : (size_t)nwords * 4;
     h->slots = h->cl <= 32 ? 1 : (h->cl <= 64 ? 2 : 4);
-    if (h->cl > 0) {
+    if (h->cfg.selection == MMAS_SELECT_RWM) {
+        // roulette wheel: smem bitmask tabu (or CT entries) per ant warp, rows from L2
+        h->rwm = true;
+        h->compact_tabu = h->cfg.tabu == MMAS_TABU_COMPACT;
+        const int words = h->compact_tabu ? (n + 1) / 2 : (n + 31) / 32;
+        const size_t per_warp = (size_t)round_up(words, 4) * 4;
+        int w = 4;
+        while (w > 1 && 128 + (size_t)w * per_warp > cons_dyn_max) --w;
+        h->cons_warps = w;
+        h->cons_grid = std::max(1, (h->m_local + w - 1) / w);
+        h->cons_smem = 128 + (size_t)w * per_warp;
+    } else if (h->cl > 0) {
         h->tb_inv = (uint32_t)round_up(n * h->cl * 4, 16);
         h->tb_id = (uint32_t)round_up(n * h->cl * 2, 16);
         const size_t per_warp = tabu_bytes;   // per ant warp: its tabu (shared-memory variant)
@@ -617,6 +636,8 @@ int setup(mmas_ctx* h) {
     }
     if (h->cons_smem > cons_dyn_max)
         return fail(MMAS_EINVAL, "n too large for the shared-memory tabu of one block");
+    allow_max_smem(construct_rwm_kernel<false>, h->smem_optin);
+    allow_max_smem(construct_rwm_kernel<true>, h->smem_optin);
     if (h->cl > 0) {
         if (h->reg_tabu) set_cl_attrs<true>(h->smem_optin);
         else set_cl_attrs<false>(h->smem_optin);
@@ -657,6 +678,10 @@ int validate(const mmas_config* c) {
         return fail(MMAS_EINVAL, "tabu must be MMAS_TABU_*");
     if (c->tabu == MMAS_TABU_COMPACT && c->cand_len != 0)
         return fail(MMAS_EINVAL, "tabu = MMAS_TABU_COMPACT requires cand_len == 0 (R27)");
+    if (c->selection != MMAS_SELECT_WRS && c->selection != MMAS_SELECT_RWM)
+        return fail(MMAS_EINVAL, "selection must be MMAS_SELECT_*");
+    if (c->selection == MMAS_SELECT_RWM && c->fallback == MMAS_FALLBACK_ARGMAX)
+        return fail(MMAS_EINVAL, "selection = MMAS_SELECT_RWM uses the roulette wheel as its fallback (R28)");
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(MMAS_EINVAL, "need 0 <= rank < world");
     double lo_x = INFINITY, hi_x = -INFINITY, lo_y = INFINITY, hi_y = -INFINITY;
     for (int i = 0; i < c->n; ++i) {

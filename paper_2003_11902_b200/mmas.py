@@ -18,6 +18,7 @@ MMAS_OK, MMAS_EINVAL, MMAS_ENOMEM, MMAS_ECUDA, MMAS_ENCCL, MMAS_ESTATE = 0, -1, 
 DEPOSIT_ITERATION_BEST, DEPOSIT_GLOBAL_BEST = 0, 1
 FALLBACK_WRS, FALLBACK_ARGMAX = 0, 1
 TABU_BITMASK, TABU_COMPACT = 0, 1
+SELECT_WRS, SELECT_RWM = 0, 1
 
 # every symbol include/mmas.h declares (checked by tests/test_capi.py)
 EXPORTED = (
@@ -44,7 +45,7 @@ class Config(ctypes.Structure):
         ("p_best", ctypes.c_double), ("deposit", ctypes.c_int32), ("fallback", ctypes.c_int32),
         ("local_search", ctypes.c_int32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
         ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("use_caller_stream", ctypes.c_int32),
-        ("tabu", ctypes.c_int32),
+        ("tabu", ctypes.c_int32), ("selection", ctypes.c_int32),
     ]
 
 
@@ -126,7 +127,7 @@ class Colony:
 
     def __init__(self, coords, n_ants, cand_len, alpha=1.0, beta=2.0, rho=0.5, seed=42, p_best=0.01,
                  deposit_global=False, fallback_argmax=False, local_search=False, device=-1, stream=None,
-                 rank=0, world=1, tabu=TABU_BITMASK):
+                 rank=0, world=1, tabu=TABU_BITMASK, selection=SELECT_WRS):
         L = lib()
         c = np.ascontiguousarray(coords, dtype=np.float64).reshape(-1, 2)
         self.n = c.shape[0]
@@ -151,6 +152,7 @@ class Colony:
         cfg.use_caller_stream = 0 if stream is None else 1
         cfg.rank, cfg.world = int(rank), int(world)
         cfg.tabu = int(tabu)
+        cfg.selection = int(selection)
         h = ctypes.c_void_p()
         _err(L.mmas_create_ex(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h

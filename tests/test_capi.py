@@ -49,6 +49,8 @@ def test_built_for_sm100a():
     (dict(local_search=2), "local_search"),
     (dict(tabu=2), "tabu"),
     (dict(tabu=1), "cand_len == 0"),          # compact tabu needs the full-row path (R27)
+    (dict(selection=2), "selection"),
+    (dict(selection=1, fallback=1), "roulette"),
     (dict(world=2, rank=2), "rank"),
 ])
 def test_invalid_arguments_rejected_without_gpu(L, kw, frag):
