@@ -115,6 +115,12 @@ def algorithmic_bytes_per_tour(w):
     cl > 0: (n-1) steps x cl candidates x (4 B inv_w + 2 B id);  cl = 0: sum over steps of
     the unvisited entries of the inv_w row, (n-1) n / 2 x 4 B (+ 2 B per list entry with the
     compact tabu)."""
+    if w.selection:
+        # roulette wheel (R28): tau + heur (8 B) per considered node (+ 2 B id or list
+        # entry); the later stages re-read about 1/31 more (P:909-915) -- not counted
+        if w.cand_len:
+            return (w.n - 1) * w.cand_len * 10
+        return (w.n - 1) * w.n // 2 * (10 if w.tabu else 8)
     if w.cand_len:
         return (w.n - 1) * w.cand_len * 6
     if w.tabu:   # compact tabu: + the 2 B list entry of every enumerated node (R27)
@@ -127,7 +133,7 @@ def cpu_baseline_leg(w, budget_s=12.0):
     import oracle
     cores = os.cpu_count() or 1
     col = oracle.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, nthreads=cores,
-                        local_search=bool(w.local_search), tabu=w.tabu)
+                        local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection)
     t0 = time.perf_counter()
     iters = 0
     while True:
@@ -149,7 +155,7 @@ def run_reference(args):
     import oracle
     cores = os.cpu_count() or 1
     col = oracle.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, nthreads=cores,
-                        local_search=bool(w.local_search), tabu=w.tabu)
+                        local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection)
     for _ in range(args.warmup if args.warmup < 3 else 1):
         col.iterate(1)
     # bounded: each step is one full oracle iteration; cap the number of timed steps
@@ -197,7 +203,7 @@ def run_ours(args):
     coords = w.coords()
     stream = torch.cuda.current_stream().cuda_stream
     col = mmas.Colony(coords, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
-                      local_search=bool(w.local_search), tabu=w.tabu,
+                      local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection,
                       stream=stream, rank=rank, world=world)
     rb = col.record_bytes
     local = torch.zeros(rb, dtype=torch.uint8, device="cuda")
@@ -251,7 +257,7 @@ def run_ours(args):
     # roofline of the dominant kernel (construction), live CUDA-event time on its stream
     cons_ms = phases["construct_ms"] / max(phases["iterations"], 1)
     bytes_per_launch = algorithmic_bytes_per_tour(w) * col.shard()[1]
-    cons_kernel = ("construct_cl_kernel" if w.cand_len else
+    cons_kernel = ("construct_rwm_kernel" if w.selection else "construct_cl_kernel" if w.cand_len else
                    "construct_ct_kernel" if w.tabu else "construct_full_kernel")
     hbm_peak, peak_src = measured_peaks()
     achieved = bytes_per_launch / (cons_ms * 1e-3) / 1e9
@@ -283,7 +289,7 @@ def run_ours(args):
         out_steps = args.steps
         t0 = time.perf_counter()
         c2 = mmas.Colony(pinned, w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
-                         local_search=bool(w.local_search), tabu=w.tabu)
+                         local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection)
         for _ in range(out_steps):
             c2.iterate(1)
             c2.best_length()

@@ -103,6 +103,7 @@ class Workload:
     beta: float = 2.0
     mmas_seed: int = 42
     tabu: int = 0         # full-row tabu: 0 = bitmask (BT), 1 = compact (CT, R27)
+    selection: int = 0    # node selection: 0 = WRS (Alg. 3), 1 = parallel roulette wheel (R28)
 
     def coords(self) -> np.ndarray:
         return make_coords(self.shape, self.n, self.seed)
@@ -132,5 +133,10 @@ CONFIGS = {
     "C4": Workload("pr2392-shaped", 2392, 2392, 0, 100, 0.5, 0, "pr2392", 2392),
     # C4 over the compact tabu (MMAS-WRS-CT, the paper's choice without candidate lists)
     "C4CT": Workload("pr2392-shaped, compact tabu", 2392, 2392, 0, 100, 0.5, 0, "pr2392", 2392, tabu=1),
+    # the paper's comparison (T3-T6): the same workloads with the parallel roulette wheel
+    "C2RWM": Workload("pr1002-shaped, roulette wheel", 1002, 1002, 32, 1000, 0.5, 0, "pr1002", 1002, selection=1),
+    "C4RWM": Workload("pr2392-shaped, roulette wheel", 2392, 2392, 0, 100, 0.5, 0, "pr2392", 2392, selection=1),
+    "C4RWMCT": Workload("pr2392-shaped, roulette wheel, compact tabu", 2392, 2392, 0, 100, 0.5, 0, "pr2392", 2392,
+                        tabu=1, selection=1),
     "C5": Workload("d18512-shaped", 18512, 800, 32, 20, 0.7, 1, "d18512", 18512),
 }

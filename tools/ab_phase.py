@@ -17,7 +17,7 @@ iters = int(sys.argv[2]) if len(sys.argv) > 2 else 300
 w = CONFIGS[cfg]
 s = torch.cuda.current_stream().cuda_stream
 col = mmas.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, stream=s,
-                  local_search=bool(w.local_search), tabu=tabu)
+                  local_search=bool(w.local_search), tabu=max(tabu, w.tabu), selection=w.selection)
 col.iterate(20)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
