@@ -99,15 +99,35 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": sorted(self.reasons)}
 
 
-def ncu_traffic(config, kernel):
-    """DRAM bytes per launch from the committed ncu --set full capture (profiles/ncu_traffic.json)."""
+def ncu_entry(config, kernel):
+    """Per-launch numbers of the committed ncu --set full capture (profiles/ncu_traffic.json,
+    written by scripts/ncu_json.py), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)[config][kernel]
-        return d["dram_bytes_read"] + d["dram_bytes_write"]
+            return json.load(f)[config][kernel]
     except (OSError, KeyError, ValueError):
         return None
+
+
+def ncu_traffic(config, kernel):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) or None."""
+    d = ncu_entry(config, kernel)
+    return None if d is None else d["dram_bytes_read"] + d["dram_bytes_write"]
+
+
+# the paper's construction-only numbers for the same instance shape (other hardware: context)
+PAPER_CONTEXT = {
+    "C1": "V100 d198 WRS-BT cl=32 construction 0.19 ms -> 1.04M tours/s (T6 P:1549); ours uses cl=16",
+    "C2": "V100 pr1002 WRS-BT cl=32 construction 0.93 ms -> 1.08M tours/s (T6 P:1549)",
+    "C2RWM": "the paper's RWM variants are slower than WRS on every instance (T3-T6, P:1269-1273)",
+    "C3": "V100 fl3795 WRS-BT cl=32 construction 12.65 ms -> 300k tours/s (T6 P:1549)",
+    "C4": "V100 pr2392 WRS-BT full row 52.54 ms -> 46k tours/s (T4 P:1418)",
+    "C4CT": "V100 pr2392 WRS-CT full row 39.24 ms -> 61k tours/s (T4 P:1419)",
+    "C4RWM": "the paper's RWM variants are slower than WRS on every instance (T3-T4)",
+    "C4RWMCT": "the paper's RWM variants are slower than WRS on every instance (T3-T4)",
+    "C5": "d18512 with 2-opt: total runtime only in the paper (T9 P:1821), no per-iteration figure",
+}
 
 
 def algorithmic_bytes_per_tour(w):
@@ -263,15 +283,36 @@ def run_ours(args):
     achieved = bytes_per_launch / (cons_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                 "traffic": ncu_traffic(args.config, cons_kernel),
-                "traffic_note": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json): the candidate rows are read "
-                                "from shared memory (TMA-staged once per launch), so HBM traffic is ~0.2% of the "
-                                "algorithmic bytes",
+                "traffic_note": "DRAM bytes per launch (ncu capture, profiles/ncu_traffic.json); with the "
+                                "candidate table in shared memory (C1, C2: TMA-staged once per launch) or "
+                                "L2-resident rows, HBM traffic is far below the algorithmic bytes",
                 "kernel": cons_kernel,
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
                 "kernel_ms": cons_ms, "kernel_share_of_step": cons_ms / (total_ms / args.steps),
                 "algorithmic_bytes_per_launch": bytes_per_launch,
-                "note": "bytes = (n-1)*cl*6 per tour (4 B inv_w + 2 B id per candidate), SURVEY 8(d); the kernel "
-                        "is issue/latency-bound (ALU + dependent chain), see DESIGN.md Sec. 6"}
+                "note": "algorithmic bytes per tour: see algorithmic_bytes_per_tour() and DESIGN.md Sec. 5; the "
+                        "construction kernels are issue/latency-bound (ALU + the per-step dependent chain), so "
+                        "the issue and chain views below are the ones that bound them (SURVEY 8(d))"}
+    # (2) issue roofline: warp instructions per launch (ncu capture of the same launch configuration)
+    # over the live kernel time, against 4 schedulers x SMs x the SM clock sampled during the run
+    sm_mhz = clk.summary().get("sm_mhz") or 0.0
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    ent = ncu_entry(args.config, cons_kernel)
+    if ent and ent.get("inst_executed") and sm_mhz:
+        ach = ent["inst_executed"] / (cons_ms * 1e-3) / 1e9
+        pk = 4 * nsm * sm_mhz * 1e6 / 1e9
+        roofline["issue"] = {"achieved": ach, "peak": pk, "unit": "Ginst/s (warp)", "frac": ach / pk,
+                             "inst_per_launch": ent["inst_executed"],
+                             "note": "smsp__inst_executed.sum of one captured launch / live kernel time; "
+                                     "peak = 4 issue slots x %d SMs x %.0f MHz" % (nsm, sm_mhz)}
+    # (3) chain model: every ant's n-1 dependent steps; time per step of one resident warp
+    warps_per_sm = col.shard()[1] / nsm
+    roofline["chain"] = {"ns_per_step": cons_ms * 1e6 / (w.n - 1),
+                         "cycles_per_step": cons_ms * 1e-3 * sm_mhz * 1e6 / (w.n - 1) if sm_mhz else None,
+                         "ant_warps_per_sm": warps_per_sm,
+                         "note": "kernel time / (n-1): the per-step latency of an ant's warp when all ants are "
+                                 "resident at once (warps_per_sm <= 64); tools/micro_step.cu measures the "
+                                 "chain alone at ~145-160 cycles/step"}
     update_ms = phases["update_ms"] / max(phases["iterations"], 1)
     upd_bytes = 16 * w.n * w.n
     update_roof = {"kernel": "pheromone_update_kernel", "kernel_ms": update_ms,
@@ -314,8 +355,10 @@ def run_ours(args):
                            "n": w.n, "ants_per_gpu": w.n_ants, "global_ants": m_total, "cand_len": w.cand_len,
                            "parallelism": f"ant-sharded x{world}" if world > 1 else "single GPU",
                            "l2": "flushed between timed steps (256 MiB write, outside the step events)",
-                           "paper_context": "V100 pr1002 WRS-BT cl=32 construction: 1.08M tours/s (P:1549), "
-                                            "other hardware, construction only"},
+                           "tabu": "compact" if w.tabu else "bitmask",
+                           "selection": "roulette wheel" if w.selection else "WRS",
+                           "local_search": "2-opt" if w.local_search else "none",
+                           "paper_context": PAPER_CONTEXT.get(args.config, "") + " (other hardware, context only)"},
                 "roofline": roofline, "update_roofline": update_roof,
                 "phases_ms_per_step": {"construct": cons_ms, "select": phases["select_ms"] / max(phases["iterations"], 1),
                                        "update": update_ms,

@@ -26,9 +26,9 @@ if has bench; then
   timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
   head -c 600 $OUT/bench.json; echo
 fi
-for cfg in C1 C3 C4 C4CT C5; do
+for cfg in C1 C3 C4 C4CT C5 C2RWM C4RWM C4RWMCT; do
   if has bench$cfg; then
-    steps=50; [[ $cfg == C4* ]] && steps=20; [ $cfg == C5 ] && steps=6
+    steps=50; [[ $cfg == C4* ]] && steps=20; [ $cfg == C5 ] && steps=6; [ $cfg == C2RWM ] && steps=200
     timeout 1200 python bench.py --config $cfg --steps $steps --warmup 3 --no-cpu-baseline > $OUT/bench_$cfg.json 2> $OUT/bench_$cfg.err
     head -c 300 $OUT/bench_$cfg.json; echo
   fi
@@ -46,7 +46,7 @@ if has ncu; then
      python bench.py --steps 420 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_update.log 2>&1
   ls -la $OUT
 fi
-for cfg in C3 C4 C4CT; do
+for cfg in C1 C3 C4 C4CT C2RWM C4RWMCT C5; do
   if has ncu$cfg; then
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:construct -s 5 -c 1 -o $OUT/prof_construct_$cfg \
        python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_construct_$cfg.log 2>&1

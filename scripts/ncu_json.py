@@ -1,0 +1,54 @@
+"""Collect per-launch numbers from ncu --set full captures into profiles/ncu_traffic.json
+(read by bench.py for roofline.traffic and the issue roofline).
+
+usage: python scripts/ncu_json.py CONFIG:KERNEL:report.ncu-rep [...]
+KERNEL is the key bench.py looks up (e.g. construct_cl_kernel, pheromone_update_kernel)."""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+WANT = {"dram__bytes_read.sum": "dram_bytes_read", "dram__bytes_write.sum": "dram_bytes_write",
+        "smsp__inst_executed.sum": "inst_executed", "gpu__time_duration.sum": "duration",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+        "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
+        "lts__t_bytes.sum": "l2_bytes"}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "inst": 1, "ns": 1e-3, "us": 1, "usecond": 1,
+         "ms": 1e3, "msecond": 1e3, "%": 1, "": 1}
+
+
+def main():
+    d = json.load(open(OUT)) if os.path.exists(OUT) else {}
+    srcs = []
+    for arg in sys.argv[1:]:
+        cfg, kern, rep = arg.split(":", 2)
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        h, units, v = rows[0], rows[1], rows[2]
+        e = {}
+        for name, key in WANT.items():
+            if name in h:
+                i = h.index(name)
+                val = float(v[i].replace(",", ""))
+                if key == "duration":
+                    e["duration_us"] = val * SCALE.get(units[i], 1)
+                else:
+                    e[key] = val * SCALE.get(units[i], 1)
+        for k in ("dram_bytes_read", "dram_bytes_write", "inst_executed", "l2_bytes"):
+            if k in e:
+                e[k] = int(round(e[k]))
+        d.setdefault(cfg, {})[kern] = e
+        srcs.append(os.path.relpath(rep, ROOT))
+    d["source"] = ("ncu --set full --clock-control none captures (one launch each): " + ", ".join(srcs) +
+                   "; dram__bytes_read/write.sum, smsp__inst_executed.sum (warp instructions), "
+                   "gpu__time_duration.sum per launch")
+    json.dump(d, open(OUT, "w"), indent=1, sort_keys=True)
+    print(json.dumps(d, indent=1, sort_keys=True))
+
+
+if __name__ == "__main__":
+    main()

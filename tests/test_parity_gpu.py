@@ -279,3 +279,26 @@ def test_c5_sampled_ants_with_two_opt():
         assert L[a] == l
     assert np.all(np.sort(T, axis=1) == np.arange(w.n))
     assert g.stats()["local_search_moves"] > 0
+
+
+# ---- maximum size (u16 ids: n = 65535) --------------------------------------------
+def test_maximum_n_properties():
+    """n = 65535 (the largest n with u16 city ids; 3 x 17 GB n^2 matrices in
+    HBM): one iteration with cl = 32 and fallbacks; properties that hold at any size --
+    every route a permutation, lengths equal to the EUC_2D sum recomputed here, the
+    global best is the shortest route, trails inside the limits."""
+    n, m = 65535, 16
+    c = make_coords("uniform", n, 65535)
+    g = mmas.Colony(c, m, 32, seed=3)
+    g.iterate(1)
+    T, L = g.tours(), g.lengths()
+    assert np.all(np.sort(T, axis=1) == np.arange(n))
+    for a in range(m):
+        p = c[T[a]]
+        d = np.floor(np.sqrt(((p - np.roll(p, -1, axis=0)) ** 2).sum(axis=1)) + 0.5).astype(np.int64)
+        assert L[a] == d.sum()
+    gb, gl = g.best_tour()
+    assert gl == L.min() and np.array_equal(gb, T[int(np.argmin(L))])
+    assert g.stats()["fallback_steps"] > 0
+    tmin, tmax = g.limits()
+    assert tmax == np.float32(1.0 / ((1.0 - 0.5) * gl))
