@@ -493,7 +493,10 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
             evaluate(Lv, [&] { slice_half(J, H0{}); }, [&] { slice_half(J, H1{}); }, bm, bc);
             const uint32_t best = __reduce_min_sync(kFull, bm);
             const uint32_t nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
-            commit(nxt & 0xFFFFu, s);   // garbage but in-range if best >= 2^31; undone by the caller
+            // every lane holds a real candidate (a visited one has bit 31 set), so nxt is a city
+            // id < n even when best >= 2^31 (then it is undone by the caller)
+            __builtin_assume(nxt < 65536u);
+            commit(nxt, s);
             return best >= 0x80000000u;
         };
         // GENERIC step (runtime j): guards, and the R9 fallback (row a3) inlined ONCE

@@ -241,6 +241,7 @@ struct UpdateArgs {
     const uint16_t* cand_id;
     float* cand_inv;
     int cl;
+    int smem_row;      // 1: the new inv_w row is staged in smem for the cand gather (ld floats fit)
     uint32_t* iter_dev;
 };
 
@@ -251,6 +252,8 @@ __global__ void __launch_bounds__(256) pheromone_update_kernel(UpdateArgs U) {
     const int n4 = (U.n + 3) >> 2;
     for (int i = blockIdx.x; i < U.n; i += gridDim.x) {
         const int si = U.succ[i], pi = U.pred[i];
+        // candidate ids of the row, loaded now so the gather after the barrier does not wait
+        const int cid = (U.cl > 0 && (int)threadIdx.x < U.cl) ? U.cand_id[(size_t)i * U.cl + threadIdx.x] : 0;
         float4* trow = reinterpret_cast<float4*>(U.tau + (size_t)i * U.ld);
         float4* wrow = reinterpret_cast<float4*>(U.inv_w + (size_t)i * U.ld);
         const float4* hrow = reinterpret_cast<const float4*>(U.heur + (size_t)i * U.ld);
@@ -284,13 +287,15 @@ __global__ void __launch_bounds__(256) pheromone_update_kernel(UpdateArgs U) {
                 trow[q] = make_float4(tv[0], tv[1], tv[2], tv[3]);
                 const float4 w4 = make_float4(wv[0], wv[1], wv[2], wv[3]);
                 wrow[q] = w4;
-                if (U.cl > 0) reinterpret_cast<float4*>(s_row)[q] = w4;
+                if (U.cl > 0 && U.smem_row) reinterpret_cast<float4*>(s_row)[q] = w4;
             }
         }
         if (U.cl > 0) {
             __syncthreads();
-            for (int k = threadIdx.x; k < U.cl; k += blockDim.x)
-                U.cand_inv[(size_t)i * U.cl + k] = s_row[U.cand_id[(size_t)i * U.cl + k]];
+            // cl <= 128; rows too long for smem are gathered from the block's own global writes
+            if ((int)threadIdx.x < U.cl)
+                U.cand_inv[(size_t)i * U.cl + threadIdx.x] =
+                    U.smem_row ? s_row[cid] : U.inv_w[(size_t)i * U.ld + cid];
             __syncthreads();
         }
     }

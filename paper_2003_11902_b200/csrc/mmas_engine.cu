@@ -408,7 +408,8 @@ int launch_two_opt(mmas_ctx* h, bool fuse_select) {
     T.queue = h->ls_queue;
     T.inq = h->ls_inq;
     T.moves = h->ls_moves;
-    const size_t per_ant = (size_t)4 * h->ldr;   // route + pos (u16) in shared memory
+    // route + pos (u16) and the queued bits in shared memory
+    const size_t per_ant = (size_t)4 * h->ldr + (size_t)4 * h->ls_nwords;
     if (per_ant <= (size_t)h->ls_coop_smem_max) {
         // one block of kLsWarps warps per ant (speculative parallel FIFO, two_opt_coop_kernel)
         T.warps_per_block = kLsWarps;
@@ -442,7 +443,8 @@ int launch_update(mmas_ctx* h) {
     U.cl = h->cl;
     U.iter_dev = h->iter_dev;
     const int threads = 256;
-    const size_t smem = h->cl > 0 ? sizeof(float) * (size_t)h->ld : 0;
+    U.smem_row = h->cl > 0 && sizeof(float) * (size_t)h->ld <= (size_t)h->smem_optin - 1024;
+    const size_t smem = U.smem_row ? sizeof(float) * (size_t)h->ld : 0;
     launch_pdl(pheromone_update_kernel, dim3(h->n), dim3(threads), smem, h->stream, U);
     h->launches++;
     CU(cudaGetLastError());

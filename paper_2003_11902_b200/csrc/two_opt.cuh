@@ -253,12 +253,12 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
     const int n = T.n;
     uint16_t* s_route = ls_smem;
     uint16_t* s_pos = ls_smem + T.ldr;
+    uint32_t* inq = reinterpret_cast<uint32_t*>(ls_smem + 2 * T.ldr);   // queued bits (smem atomics)
     unsigned long long wbest = ~0ull;
     long long moves = 0;
     for (int al = blockIdx.x; al < T.m_local; al += gridDim.x) {
         uint16_t* route = T.routes + (size_t)al * T.ldr;
         uint16_t* queue = T.queue + (size_t)al * T.ldr;
-        uint32_t* inq = T.inq + (size_t)al * T.nwords;
         for (int i = 2 * tid; i < T.ldr; i += 2 * blockDim.x)
             *reinterpret_cast<uint32_t*>(s_route + i) = *reinterpret_cast<const uint32_t*>(route + i);
         __syncthreads();
@@ -291,13 +291,11 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
                 for (int w = 0; w < avail; ++w)
                     if (s_eval[w].found) { win = w; break; }
                 const int retired = win >= 0 ? win + 1 : avail;
-                if (tid == 0) {
-                    for (int w = 0; w < retired; ++w) {
-                        int q = head + w;
-                        if (q >= n) q -= n;
-                        const int a = queue[q];
-                        atomicAnd(inq + (a >> 5), ~(1u << (a & 31)));
-                    }
+                if (warp == 0 && lane < retired) {
+                    int q = head + lane;
+                    if (q >= n) q -= n;
+                    const int a = queue[q];
+                    atomicAnd(inq + (a >> 5), ~(1u << (a & 31)));
                 }
                 int nhead = head + retired;
                 if (nhead >= n) nhead -= n;

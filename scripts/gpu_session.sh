@@ -37,22 +37,37 @@ if has reference; then
   timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
   cat $OUT/bench_reference.json
 fi
+# summarise a capture on the box (text summary + per-launch json); keep the report only if
+# KEEP_REPS=1 (gpurun copies back at most 64 MiB)
+digest() {  # digest CONFIG KERNEL REPORT_BASENAME
+  if [ -f $OUT/$3.ncu-rep ]; then
+    python scripts/ncu_summary.py $OUT/$3.ncu-rep 40 > $OUT/$3.txt 2>&1
+    python scripts/ncu_json.py --out $OUT/ncu_traffic.json $1:$2:$OUT/$3.ncu-rep > /dev/null 2>&1
+    [ "${KEEP_REPS:-0}" == 1 ] || rm -f $OUT/$3.ncu-rep
+  fi
+}
 if has ncu; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
      python bench.py --steps 30 --warmup 3 --no-cpu-baseline > $OUT/ncu_launches_bench.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:construct -s 400 -c 1 -o $OUT/prof_construct \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:construct -s 400 -c 1 -o $OUT/prof_construct_C2 \
      python bench.py --steps 420 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_construct.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pheromone_update -s 400 -c 1 -o $OUT/prof_update \
+  digest C2 construct_cl_kernel prof_construct_C2
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pheromone_update -s 400 -c 1 -o $OUT/prof_update_C2 \
      python bench.py --steps 420 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_update.log 2>&1
+  digest C2 pheromone_update_kernel prof_update_C2
   ls -la $OUT
 fi
-for cfg in C1 C3 C4 C4CT C2RWM C4RWMCT C5; do
+for cfg in C1 C3 C4 C4CT C2RWM C4RWM C4RWMCT C5; do
   if has ncu$cfg; then
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:construct -s 5 -c 1 -o $OUT/prof_construct_$cfg \
        python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_construct_$cfg.log 2>&1
+    kern=construct_cl_kernel
+    case $cfg in C4) kern=construct_full_kernel;; C4CT) kern=construct_ct_kernel;; *RWM*) kern=construct_rwm_kernel;; esac
+    digest $cfg $kern prof_construct_$cfg
   fi
 done
 if has ncuC5; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:two_opt -s 2 -c 1 -o $OUT/prof_two_opt_C5 \
      python bench.py --config C5 --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_two_opt.log 2>&1
+  digest C5 two_opt_coop_kernel prof_two_opt_C5
 fi

@@ -1,7 +1,7 @@
 """Collect per-launch numbers from ncu --set full captures into profiles/ncu_traffic.json
 (read by bench.py for roofline.traffic and the issue roofline).
 
-usage: python scripts/ncu_json.py CONFIG:KERNEL:report.ncu-rep [...]
+usage: python scripts/ncu_json.py [--out FILE] CONFIG:KERNEL:report.ncu-rep [...]
 KERNEL is the key bench.py looks up (e.g. construct_cl_kernel, pheromone_update_kernel)."""
 import csv
 import io
@@ -22,9 +22,13 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "inst": 1, "ns": 1
 
 
 def main():
-    d = json.load(open(OUT)) if os.path.exists(OUT) else {}
+    args = sys.argv[1:]
+    out = OUT
+    if args and args[0] == "--out":
+        out, args = args[1], args[2:]
+    d = json.load(open(out)) if os.path.exists(out) else {}
     srcs = []
-    for arg in sys.argv[1:]:
+    for arg in args:
         cfg, kern, rep = arg.split(":", 2)
         out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(out)))
@@ -43,10 +47,12 @@ def main():
                 e[k] = int(round(e[k]))
         d.setdefault(cfg, {})[kern] = e
         srcs.append(os.path.relpath(rep, ROOT))
-    d["source"] = ("ncu --set full --clock-control none captures (one launch each): " + ", ".join(srcs) +
+    d["source"] = ("ncu --set full --clock-control none captures (one launch each): " +
+                   ", ".join(sorted(set(srcs) | set(d.get("_reps", [])))) +
                    "; dram__bytes_read/write.sum, smsp__inst_executed.sum (warp instructions), "
                    "gpu__time_duration.sum per launch")
-    json.dump(d, open(OUT, "w"), indent=1, sort_keys=True)
+    d["_reps"] = sorted(set(srcs) | set(d.get("_reps", [])))
+    json.dump(d, open(out, "w"), indent=1, sort_keys=True)
     print(json.dumps(d, indent=1, sort_keys=True))
 
 
