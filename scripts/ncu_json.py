@@ -13,7 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 WANT = {"dram__bytes_read.sum": "dram_bytes_read", "dram__bytes_write.sum": "dram_bytes_write",
-        "smsp__inst_executed.sum": "inst_executed", "gpu__time_duration.sum": "duration",
+        "smsp__inst_executed.sum": "inst_executed", "gpu__time_duration.sum": "duration", "sm__inst_executed.sum": "sm_inst_executed",
         "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
         "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
         "lts__t_bytes.sum": "l2_bytes"}
@@ -30,9 +30,18 @@ def main():
     srcs = []
     for arg in args:
         cfg, kern, rep = arg.split(":", 2)
-        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-        rows = list(csv.reader(io.StringIO(out)))
-        h, units, v = rows[0], rows[1], rows[2]
+        if rep.endswith(".txt"):   # a scripts/ncu_summary.py digest: "  metric  value unit" lines
+            h, units, v = [], [], []
+            for line in open(rep):
+                parts = line.split()
+                if len(parts) >= 2 and parts[0] in WANT:
+                    h.append(parts[0])
+                    v.append(parts[1])
+                    units.append(parts[2] if len(parts) > 2 else "")
+        else:
+            raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+            rows = list(csv.reader(io.StringIO(raw)))
+            h, units, v = rows[0], rows[1], rows[2]
         e = {}
         for name, key in WANT.items():
             if name in h:
