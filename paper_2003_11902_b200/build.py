@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmmas.so")
 SOURCES = [os.path.join(CSRC, "mmas_engine.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "rng.cuh", "construct.cuh", "two_opt.cuh")] + [os.path.join(ROOT, "include", "mmas.h")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "rng.cuh", "construct.cuh", "rwm.cuh", "two_opt.cuh")] + [os.path.join(ROOT, "include", "mmas.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [

@@ -287,9 +287,10 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
                 __syncthreads();
                 // take the results in queue order up to the first improving one
                 const int avail = min(count, kLsWarps);
-                int win = -1;
-                for (int w = 0; w < avail; ++w)
-                    if (s_eval[w].found) { win = w; break; }
+                uint32_t fmask = 0;
+#pragma unroll
+                for (int w = 0; w < kLsWarps; ++w) fmask |= (w < avail && s_eval[w].found) ? 1u << w : 0u;
+                const int win = fmask ? __ffs(fmask) - 1 : -1;
                 const int retired = win >= 0 ? win + 1 : avail;
                 if (warp == 0 && lane < retired) {
                     int q = head + lane;
@@ -346,7 +347,9 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
                         s_ctl[2] += 1;
                     }
                 }
-                __syncthreads();
+                // every thread read head / count before the first barrier of this round, so
+                // thread 0 may publish the next round's values now; one barrier covers both
+                // the reversal and the queue state
                 if (tid == 0) {
                     s_ctl[0] = nhead;
                     s_ctl[1] = ncount;
