@@ -24,19 +24,32 @@ namespace mmas {
 
 // ---- bitmask tabu (Sec. 4.1) ------------------------------------------
 // n <= 1024: lane j keeps word j in a register; a test is one SHFL, a mark one OR.
+// The same bits are also kept transposed (wt: lane j holds cities j, j+32, j+64, ...,
+// city c at bit c>>5 of lane c&31) for the candidate test, whose SHFL then takes c itself
+// as the source lane (the shuffle uses its low 5 bits) with no shift before it.
 struct RegTabu {
-    uint32_t w;
-    __device__ __forceinline__ void init(uint32_t*, int, int) { w = 0u; }
+    uint32_t w, wt;
+    __device__ __forceinline__ void init(uint32_t*, int, int) { w = 0u; wt = 0u; }
     // every lane of the warp must call word()/visited() (warp shuffle)
     __device__ __forceinline__ uint32_t word(int idx) const { return __shfl_sync(kFull, w, idx); }
     __device__ __forceinline__ bool visited(uint32_t c) const { return (word((int)(c >> 5)) >> (c & 31)) & 1u; }
     // bit 31 = "c visited" (other bits garbage); lanes may pass any c < 1024
-    __device__ __forceinline__ uint32_t top_bit(uint32_t c) const { return word((int)(c >> 5)) << (~c & 31u); }
+    __device__ __forceinline__ uint32_t top_bit(uint32_t c) const {
+        return __shfl_sync(kFull, wt, (int)c) << (~(c >> 5) & 31u);
+    }
     __device__ __forceinline__ void mark(uint32_t c, int lane) {
         if (lane == (int)(c >> 5)) w |= 1u << (c & 31);
+        if (lane == (int)(c & 31)) wt |= 1u << (c >> 5);
     }
     __device__ __forceinline__ void sync() {}
 };
+
+// (a & ~m) | (b & m) in one LOP3
+__device__ __forceinline__ uint32_t bit_select(uint32_t a, uint32_t b, uint32_t m) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(d) : "r"(a), "r"(b), "r"(m));
+    return d;
+}
 // any n: ceil(n/32) words per warp in shared memory.
 struct SmemTabu {
     uint32_t* t;
@@ -432,7 +445,8 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
                 hook_a();
                 const uint32_t t = tabu.top_bit(c);
                 hook_b();
-                bm = (__float_as_uint(__fmul_rn(Lv[0], iv)) & 0x7FFFFFFFu) | (t & 0x80000000u);
+                // bit 31 from the tabu, bits 0-30 the key magnitude
+                bm = bit_select(t, __float_as_uint(__fmul_rn(Lv[0], iv)), 0x7FFFFFFFu);
                 bc = c;
             } else {
                 hook_a();
@@ -557,7 +571,7 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
                     // slices with the next step's chain); a step that needed the fallback is
                     // detected once at the end and the whole group is rolled back (tabu word,
                     // current city, route staging) and redone by the generic path
-                    const uint32_t w0 = tabu.w, cur0 = cur, stage0 = stage;
+                    const uint32_t w0 = tabu.w, wt0 = tabu.wt, cur0 = cur, stage0 = stage;
                     bool hit = spec_step(I0{}, 4 * g + 0);
                     hit |= spec_step(I1{}, 4 * g + 1);
                     hit |= spec_step(I2{}, 4 * g + 2);
@@ -568,6 +582,7 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
                         continue;
                     }
                     tabu.w = w0;
+                    tabu.wt = wt0;
                     cur = cur0;
                     stage = stage0;
                     sliced_all = true;   // every slice of this group already ran
