@@ -103,11 +103,21 @@ __device__ __forceinline__ void philox_rounds(uint4& c, const RoundKeys& rk) {
 // visited are skipped.  Per-lane best with ties to the lower id; the caller
 // reduces across the warp.
 // ---------------------------------------------------------------------------
+// Exact pruning of the key computations.  A city's key
+// magnitude is |det_log2(u)| * inv_w >= (1 - u) * log2(e) * inv_w, because -ln u >= 1 - u
+// and det_log2 is within 1.61 ulp of log2.  lb = (1-u) * (inv_w * kLog2eLow) in fp32, with
+// log2(e) deflated by 2^-20, stays below the fp32 magnitude for every u of the grid and
+// every inv_w (tests/test_oracle_rng.py pins the ratio), so a city with lb > thr, thr the
+// warp's best magnitude so far, can neither win nor tie: its det_log2 is not evaluated.
+constexpr float kLog2eLow = 1.4426935911178589f;
+
 // One 128-city chunk of the scan: lane l's cities c0 .. c0+3, nib = their visited
-// bits (bit j set = visited or beyond n).  Branch-free per city.
-template <bool kArgmax>
+// bits (bit j set = visited or beyond n).  Keys are evaluated (in increasing city order)
+// only for the unvisited cities whose lower bound does not exceed thr.
+template <bool kArgmax, bool kPrune>
 __device__ __forceinline__ void scan_chunk(float4 iv, int c0, uint32_t nib, uint32_t step, uint32_t ant,
-                                           uint32_t iter, PhiloxKey key, uint32_t& best_mag, uint32_t& best_c) {
+                                           uint32_t iter, PhiloxKey key, uint32_t& best_mag, uint32_t& best_c,
+                                           float thr) {
     const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
     if (kArgmax) {
         // R9 flag: the largest weight = the smallest inv_w (positive floats order as uints)
@@ -116,7 +126,9 @@ __device__ __forceinline__ void scan_chunk(float4 iv, int c0, uint32_t nib, uint
             const uint32_t mag = ((nib >> j) & 1u) ? kNone : __float_as_uint(ivs[j]);
             if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
         }
-    } else {
+    } else if (!kPrune) {
+        // branch-free: four independent key chains (the fallback scan of the candidate path,
+        // whose few warps per SM need the ILP more than the saved work)
         const uint4 x = philox4x32_10(ctr_city((uint32_t)c0 >> 2, step, ant, iter), key);
         const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -125,7 +137,32 @@ __device__ __forceinline__ void scan_chunk(float4 iv, int c0, uint32_t nib, uint
             const uint32_t mag = ((nib >> j) & 1u) ? kNone : key_magnitude(k);
             if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
         }
+    } else {
+        const uint4 x = philox4x32_10(ctr_city((uint32_t)c0 >> 2, step, ant, iter), key);
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+        float us[4];
+        uint32_t todo = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            us[j] = uniform_open(xs[j]);
+            const float lb = __fmul_rn(__fsub_rn(1.0f, us[j]), __fmul_rn(ivs[j], kLog2eLow));
+            todo |= (((nib >> j) & 1u) == 0u && !(lb > thr)) ? (1u << j) : 0u;
+        }
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1u;
+            const float u = j == 0 ? us[0] : j == 1 ? us[1] : j == 2 ? us[2] : us[3];
+            const float v = j == 0 ? ivs[0] : j == 1 ? ivs[1] : j == 2 ? ivs[2] : ivs[3];
+            const uint32_t mag = key_magnitude(__fmul_rn(det_log2(u), v));
+            if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
+        }
     }
+}
+
+// the warp's best magnitude so far as a float threshold (+inf while nothing is found)
+__device__ __forceinline__ float warp_threshold(uint32_t best_mag) {
+    const uint32_t b = __reduce_min_sync(kFull, best_mag);
+    return b == kNone ? __int_as_float(0x7F800000) : __uint_as_float(b);
 }
 
 // Visited bits of lane l's four cities c0 .. c0+3 (cities >= n count as visited).
@@ -148,10 +185,14 @@ __device__ __forceinline__ uint32_t chunk_nibble(const Tabu& tabu, int c0, int n
 // the lower id (cities are scanned in increasing order); the caller reduces
 // across the warp.
 // ---------------------------------------------------------------------------
+// kPrefetch (the full-row path, where the scan is the whole step and 16+ warps per SM hide the
+// serial pruned key chains): next trip loaded one trip ahead + exact pruning of the keys.
 template <bool kArgmax, bool kPrefetch = false, class Tabu>
 __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, const Tabu& tabu, int n,
                                                uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
                                                int lane, uint32_t& best_mag, uint32_t& best_c) {
+    // pruning threshold (full-row path only: kPrefetch; unused by the argmax flag)
+    float thr = kPrefetch && !kArgmax ? warp_threshold(best_mag) : 0.f;
     auto load_trip = [&](int base, uint32_t& na, uint32_t& nb, float4& iva, float4& ivb) {
         const int ca = base + 4 * lane, cb = ca + 128;
         na = chunk_nibble(tabu, ca, n);
@@ -171,8 +212,9 @@ __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, co
             if (base + 256 < n) load_trip(base + 256, na2, nb2, iva2, ivb2);
             if (__any_sync(kFull, (na & nb) != 0xFu)) {
                 const int ca = base + 4 * lane;
-                scan_chunk<kArgmax>(iva, ca, na, step, ant, iter, key, best_mag, best_c);
-                scan_chunk<kArgmax>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c);
+                scan_chunk<kArgmax, kPrefetch>(iva, ca, na, step, ant, iter, key, best_mag, best_c, thr);
+                scan_chunk<kArgmax, kPrefetch>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c, thr);
+                if (!kArgmax) thr = warp_threshold(best_mag);
             }
             na = na2;
             nb = nb2;
@@ -186,8 +228,8 @@ __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, co
             load_trip(base, na, nb, iva, ivb);
             if (!__any_sync(kFull, (na & nb) != 0xFu)) continue;
             const int ca = base + 4 * lane;
-            scan_chunk<kArgmax>(iva, ca, na, step, ant, iter, key, best_mag, best_c);
-            scan_chunk<kArgmax>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c);
+            scan_chunk<kArgmax, false>(iva, ca, na, step, ant, iter, key, best_mag, best_c, thr);
+            scan_chunk<kArgmax, false>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c, thr);
         }
     }
 }
@@ -678,20 +720,33 @@ __global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
 // Positions >= L get inv_w = +inf: their key is -inf, whose magnitude 0x7F800000 loses
 // to every real key (det_log2 < 0 and finite on the u-grid, inv_w finite), and L >= 1
 // guarantees a real key in the warp -- so the select needs no position mask.
+// Keys are evaluated only for positions whose lower bound does not exceed thr (the exact
+// pruning of scan_chunk; +inf padding gives lb = +inf, pruned once thr is finite).
 __device__ __forceinline__ void ct_group(uint2 e, float4 iv, int p0, uint32_t step, uint32_t ant, uint32_t iter,
-                                         PhiloxKey key, uint32_t& best_mag, uint32_t& best_c) {
+                                         PhiloxKey key, uint32_t& best_mag, uint32_t& best_c, float thr) {
     const uint4 x = philox4x32_10(ctr_city((uint32_t)p0 >> 2, step, ant, iter), key);
     const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
     const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
-    const uint32_t vs[4] = {e.x & 0xFFFFu, e.x >> 16, e.y & 0xFFFFu, e.y >> 16};
+    float us[4];
+    uint32_t todo = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const float k = __fmul_rn(det_log2(uniform_open(xs[j])), ivs[j]);
-        const uint32_t mag = key_magnitude(k);
-        // branch-free (mag, node) lexicographic minimum
-        const bool better = (mag < best_mag) | ((mag == best_mag) & (vs[j] < best_c));
-        best_c = better ? vs[j] : best_c;
-        best_mag = min(best_mag, mag);
+        us[j] = uniform_open(xs[j]);
+        const float lb = __fmul_rn(__fsub_rn(1.0f, us[j]), __fmul_rn(ivs[j], kLog2eLow));
+        todo |= !(lb > thr) ? (1u << j) : 0u;
+    }
+    while (todo) {
+        const int j = __ffs(todo) - 1;
+        todo &= todo - 1u;
+        const float u = j == 0 ? us[0] : j == 1 ? us[1] : j == 2 ? us[2] : us[3];
+        const float v = j == 0 ? ivs[0] : j == 1 ? ivs[1] : j == 2 ? ivs[2] : ivs[3];
+        const uint32_t vj = j == 0 ? (e.x & 0xFFFFu) : j == 1 ? (e.x >> 16) : j == 2 ? (e.y & 0xFFFFu) : (e.y >> 16);
+        const uint32_t mag = key_magnitude(__fmul_rn(det_log2(u), v));
+        // (mag, node) lexicographic minimum
+        if ((mag < best_mag) | ((mag == best_mag) & (vj < best_c))) {
+            best_mag = mag;
+            best_c = vj;
+        }
     }
 }
 
@@ -709,10 +764,11 @@ __device__ __forceinline__ void ct_load(const uint16_t* ent, const float* __rest
 // one 256-position trip: lane l's groups base+4l and base+128+4l
 __device__ __forceinline__ void ct_trip(const uint2 (&e)[2], const float4 (&iv)[2], int base, int lane, int L,
                                         uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
-                                        uint32_t& best_mag, uint32_t& best_c) {
+                                        uint32_t& best_mag, uint32_t& best_c, float& thr) {
     const int pa = base + 4 * lane;
-    if (pa < L) ct_group(e[0], iv[0], pa, step, ant, iter, key, best_mag, best_c);
-    if (pa + 128 < L) ct_group(e[1], iv[1], pa + 128, step, ant, iter, key, best_mag, best_c);
+    if (pa < L) ct_group(e[0], iv[0], pa, step, ant, iter, key, best_mag, best_c, thr);
+    if (pa + 128 < L) ct_group(e[1], iv[1], pa + 128, step, ant, iter, key, best_mag, best_c, thr);
+    thr = warp_threshold(best_mag);
 }
 
 __device__ __forceinline__ void ct_load_trip(const uint16_t* ent, const float* __restrict__ row, int base, int lane,
@@ -762,13 +818,14 @@ __global__ void __launch_bounds__(128) construct_ct_kernel(ConstructArgs A) {
             // (two register sets, loop unrolled by two so no copies are needed)
             uint2 eA[2], eB[2];
             float4 ivA[2], ivB[2];
+            float thr = __int_as_float(0x7F800000);
             ct_load_trip(ent, row, 0, lane, L, eA, ivA);
             for (int base = 0; base < L; base += 512) {
                 if (base + 256 < L) ct_load_trip(ent, row, base + 256, lane, L, eB, ivB);
-                ct_trip(eA, ivA, base, lane, L, (uint32_t)s, ant, iter, A.key, bm, bc);
+                ct_trip(eA, ivA, base, lane, L, (uint32_t)s, ant, iter, A.key, bm, bc, thr);
                 if (base + 256 >= L) break;
                 if (base + 512 < L) ct_load_trip(ent, row, base + 512, lane, L, eA, ivA);
-                ct_trip(eB, ivB, base + 256, lane, L, (uint32_t)s, ant, iter, A.key, bm, bc);
+                ct_trip(eB, ivB, base + 256, lane, L, (uint32_t)s, ant, iter, A.key, bm, bc, thr);
             }
             const uint32_t nxt = warp_select(bm, bc);
             if (lane == 0) ct_mark(ent, L, n, nxt);

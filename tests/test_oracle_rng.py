@@ -82,3 +82,28 @@ def test_start_node_uniform():
         for a in range(1000):
             counts[oracle.start_node(n, a, it, seed)] += 1
     assert chisquare(counts).pvalue > 1e-3
+
+
+def test_pruning_lower_bound_holds_on_the_whole_grid():
+    """The exact key pruning of the GPU scans skips det_log2
+    when lb = fl(fl(1-u) * fl(inv * C)) > thr, C = log2(e)(1 - 2^-20) rounded down.  That is
+    safe iff lb <= fl(|det_log2(u)| * inv) for every u of the grid and every inv; with each
+    fp32 rounding bounded by 2^-24 it suffices that |det_log2(u)| / ((1-u) C) >=
+    (1 + 2^-24)^2 / (1 - 2^-24).  Checked exhaustively on all 2^23 uniforms (the bound
+    follows from -ln u >= 1 - u and det_log2's 1.61-ulp accuracy)."""
+    C = np.float32(1.4426935911178589)
+    assert float(C) <= np.log2(np.e) * (1 - 2.0 ** -20)
+    j = np.arange(1 << 23, dtype=np.float64)
+    u = ((2.0 * j + 1.0) / 2.0 ** 24).astype(np.float32)
+    D = np.abs(oracle.det_log2_many(u).astype(np.float64))
+    one_minus_u = (np.float32(1.0) - u).astype(np.float64)      # exact on the grid
+    assert np.all(one_minus_u == 1.0 - u.astype(np.float64))
+    ratio = D / (one_minus_u * float(C))
+    assert ratio.min() >= (1 + 2.0 ** -24) ** 2 / (1 - 2.0 ** -24)
+    # and directly in fp32 for a spread of inv_w values (the GPU's exact operation order)
+    rng = np.random.default_rng(0)
+    sub = rng.choice(1 << 23, size=200000, replace=False)
+    inv = (10.0 ** rng.uniform(-3, 12, size=sub.size)).astype(np.float32)
+    lb = (np.float32(1.0) - u[sub]) * (inv * C)
+    mag = np.abs(oracle.det_log2_many(u[sub]) * inv)
+    assert np.all(lb <= mag)
