@@ -657,6 +657,7 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
         if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane));
         wfb += fb;
     }
+    pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
     block_finish(A, wbest, wfb, lane, warp);
 }
 
@@ -700,6 +701,7 @@ __global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
         __syncwarp();
         if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane));
     }
+    pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
     block_finish(A, wbest, 0, lane, warp);
 }
 
@@ -837,6 +839,7 @@ __global__ void __launch_bounds__(128) construct_ct_kernel(ConstructArgs A) {
         __syncwarp();
         if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane));
     }
+    pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
     block_finish(A, wbest, 0, lane, warp);
 }
 

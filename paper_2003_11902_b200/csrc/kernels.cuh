@@ -24,6 +24,10 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 // predecessor finishes; each waits here before touching the predecessor's output
 // (a no-op when launched without the attribute).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Lets the next kernel on the stream launch its blocks now (they run their prologue up to
+// their own pdl_wait).  Construction and 2-opt kernels trigger right after their wait, so the
+// update's blocks are resident during the construction tail and prefetch the trails.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 // TSPLIB EUC_2D (R12): (int)(sqrt(dx*dx + dy*dy) + 0.5) in double.
@@ -246,28 +250,49 @@ struct UpdateArgs {
 };
 
 __global__ void __launch_bounds__(256) pheromone_update_kernel(UpdateArgs U) {
-    pdl_wait();
     extern __shared__ __align__(16) float s_row[];   // new inv_w row (cl > 0: for the gather)
-    const float tmin = U.scal[0], tmax = U.scal[1], delta = U.scal[2];
     const int n4 = (U.n + 3) >> 2;
+    // Prologue before the dependency wait: tau, heur and the candidate ids are not written
+    // by the construction / 2-opt / selection kernels this one depends on (tau's last writer
+    // is the previous update, complete before the construction passed its own wait and
+    // triggered this launch), so the first row chunk is fetched while they drain.
+    float4 t[4], h[4];
+    int cid = 0;
+    if ((int)blockIdx.x < U.n) {
+        const size_t r0 = (size_t)blockIdx.x * U.ld;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int q = (int)threadIdx.x + u * (int)blockDim.x;
+            if (q < n4) {
+                t[u] = reinterpret_cast<const float4*>(U.tau + r0)[q];
+                h[u] = __ldg(reinterpret_cast<const float4*>(U.heur + r0) + q);
+            }
+        }
+        if (U.cl > 0 && (int)threadIdx.x < U.cl) cid = U.cand_id[(size_t)blockIdx.x * U.cl + threadIdx.x];
+    }
+    pdl_wait();
+    const float tmin = U.scal[0], tmax = U.scal[1], delta = U.scal[2];
+    bool first = true;
     for (int i = blockIdx.x; i < U.n; i += gridDim.x) {
         const int si = U.succ[i], pi = U.pred[i];
-        // candidate ids of the row, loaded now so the gather after the barrier does not wait
-        const int cid = (U.cl > 0 && (int)threadIdx.x < U.cl) ? U.cand_id[(size_t)i * U.cl + threadIdx.x] : 0;
+        // candidate ids of the row, loaded before the barrier so the gather does not wait
+        if (!first && U.cl > 0 && (int)threadIdx.x < U.cl) cid = U.cand_id[(size_t)i * U.cl + threadIdx.x];
         float4* trow = reinterpret_cast<float4*>(U.tau + (size_t)i * U.ld);
         float4* wrow = reinterpret_cast<float4*>(U.inv_w + (size_t)i * U.ld);
         const float4* hrow = reinterpret_cast<const float4*>(U.heur + (size_t)i * U.ld);
         // up to 4 float4 per thread in flight: all loads first, then compute + store
         for (int q0 = threadIdx.x; q0 < n4; q0 += 4 * blockDim.x) {
-            float4 t[4], h[4];
+            if (!first) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int q = q0 + u * blockDim.x;
-                if (q < n4) {
-                    t[u] = trow[q];
-                    h[u] = __ldg(hrow + q);
+                for (int u = 0; u < 4; ++u) {
+                    const int q = q0 + u * blockDim.x;
+                    if (q < n4) {
+                        t[u] = trow[q];
+                        h[u] = __ldg(hrow + q);
+                    }
                 }
             }
+            first = false;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int q = q0 + u * blockDim.x;
@@ -290,6 +315,7 @@ __global__ void __launch_bounds__(256) pheromone_update_kernel(UpdateArgs U) {
                 if (U.cl > 0 && U.smem_row) reinterpret_cast<float4*>(s_row)[q] = w4;
             }
         }
+        first = false;   // the prologue's prefetch belongs to the first row only
         if (U.cl > 0) {
             __syncthreads();
             // cl <= 128; rows too long for smem are gathered from the block's own global writes

@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(128) construct_rwm_kernel(ConstructArgs A) {
         __syncwarp();
         if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane));
     }
+    pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
     block_finish(A, wbest, wfb, lane, warp);
 }
 

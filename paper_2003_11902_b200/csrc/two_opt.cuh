@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(128) two_opt_kernel(TwoOptArgs T, ConstructArg
         wbest = min(wbest, finish_ant(A, route, al, (uint32_t)(A.ant_lo + al), lane));
     }
     if (lane == 0 && moves) atomicAdd(T.moves, (unsigned long long)moves);
+    pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
     block_finish(A, wbest, 0, lane, warp);
 }
 
@@ -367,6 +368,7 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
         __syncthreads();
     }
     if (tid == 0 && moves) atomicAdd(T.moves, (unsigned long long)moves);
+    pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
     block_finish(A, wbest, 0, lane, warp);
 }
 
