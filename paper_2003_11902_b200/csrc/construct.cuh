@@ -27,10 +27,25 @@ namespace mmas {
 // The same bits are also kept transposed (wt: lane j holds cities j, j+32, j+64, ...,
 // city c at bit c>>5 of lane c&31) for the candidate test, whose SHFL then takes c itself
 // as the source lane (the shuffle uses its low 5 bits) with no shift before it.
-struct RegTabu {
+// kLazyW (cl == 32 path): only wt is maintained per step; w, which the fallback scan reads,
+// is rebuilt from wt by a warp bit-matrix transpose in prepare() when a scan needs it.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+    // lane i holds row i of a 32x32 bit matrix; returns column `lane` (bit i = row i's bit)
+    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int j = 16 >> k;
+        const uint32_t m = masks[k];
+        const uint32_t y = __shfl_xor_sync(kFull, x, j);
+        x = (lane & j) ? (((y >> j) & m) | (x & ~m)) : ((x & m) | ((y & m) << j));
+    }
+    return x;
+}
+template <bool kLazyW>
+struct RegTabuX {
     uint32_t w, wt;
     __device__ __forceinline__ void init(uint32_t*, int, int) { w = 0u; wt = 0u; }
-    // every lane of the warp must call word()/visited() (warp shuffle)
+    // every lane of the warp must call word()/visited() (warp shuffle); kLazyW: after prepare()
     __device__ __forceinline__ uint32_t word(int idx) const { return __shfl_sync(kFull, w, idx); }
     __device__ __forceinline__ bool visited(uint32_t c) const { return (word((int)(c >> 5)) >> (c & 31)) & 1u; }
     // bit 31 = "c visited" (other bits garbage); lanes may pass any c < 1024
@@ -38,11 +53,15 @@ struct RegTabu {
         return __shfl_sync(kFull, wt, (int)c) << (~(c >> 5) & 31u);
     }
     __device__ __forceinline__ void mark(uint32_t c, int lane) {
-        if (lane == (int)(c >> 5)) w |= 1u << (c & 31);
+        if (!kLazyW && lane == (int)(c >> 5)) w |= 1u << (c & 31);
         if (lane == (int)(c & 31)) wt |= 1u << (c >> 5);
+    }
+    __device__ __forceinline__ void prepare(int lane) {
+        if (kLazyW) w = warp_transpose32(wt, lane);
     }
     __device__ __forceinline__ void sync() {}
 };
+using RegTabu = RegTabuX<false>;
 
 // (a & ~m) | (b & m) in one LOP3
 __device__ __forceinline__ uint32_t bit_select(uint32_t a, uint32_t b, uint32_t m) {
@@ -64,6 +83,7 @@ struct SmemTabu {
     __device__ __forceinline__ void mark(uint32_t c, int lane) {
         if (lane == 0) t[c >> 5] |= 1u << (c & 31);
     }
+    __device__ __forceinline__ void prepare(int) {}
     __device__ __forceinline__ void sync() { __syncwarp(); }
 };
 
@@ -369,7 +389,7 @@ template <int kSlots, bool kSmemTable, bool kRegTabu, bool kFull32>
 __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
     pdl_wait();
     static_assert(!kFull32 || kSlots == 1, "kFull32: cl == 32, one slot per lane");
-    using Tabu = typename std::conditional<kRegTabu, RegTabu, SmemTabu>::type;
+    using Tabu = typename std::conditional<kRegTabu, RegTabuX<kFull32>, SmemTabu>::type;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int n = A.n, cl = A.cl;
@@ -567,6 +587,7 @@ __global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
             uint32_t nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
             if (best >= 0x80000000u) {   // every candidate visited: R9 fallback
                 ++fb;
+                tabu.prepare(lane);
                 const float* row = A.inv_w + (size_t)cur * A.ld;
                 uint32_t fm = kNone, fc = kNone;
                 if (A.fallback_argmax)
