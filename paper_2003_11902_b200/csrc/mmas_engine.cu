@@ -104,6 +104,8 @@ bool is_int_in(double x, int lo, int hi) { return x == std::floor(x) && x >= lo 
 struct mmas_ctx {
     mmas_config cfg{};
     int n = 0, ld = 0, cl = 0, ldr = 0;
+    int cl_ld = 0;   // row stride of the candidate tables: 32 for 0 < cl <= 32 (rows padded with the
+                     // row's own city, which is always visited), else cl
     int m = 0, ant_lo = 0, m_local = 0;
     int alpha = 1;
     int device = 0, num_sms = 148, smem_optin = 0;
@@ -244,7 +246,7 @@ ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = f
     A.key = h->key;
     A.n = h->n;
     A.ld = h->ld;
-    A.cl = h->cl;
+    A.cl = h->cl_ld;   // padded rows: the kernels see cl_ld slots, the padding is always visited
     A.ldr = h->ldr;
     A.ant_lo = h->ant_lo;
     A.m_local = h->m_local;
@@ -305,7 +307,7 @@ void launch_cl_f(mmas_ctx* h, const ConstructArgs& A) {
 template <int S, bool T, bool R>
 void launch_cl(mmas_ctx* h, const ConstructArgs& A) {
     if constexpr (S == 1) {
-        if (h->cl == 32) {
+        if (h->cl_ld == 32) {
             launch_cl_f<1, T, R, true>(h, A);
             return;
         }
@@ -440,7 +442,7 @@ int launch_update(mmas_ctx* h) {
     U.pred = h->pred;
     U.cand_id = h->cand_id;
     U.cand_inv = h->cand_inv;
-    U.cl = h->cl;
+    U.cl = h->cl_ld;
     U.iter_dev = h->iter_dev;
     const int threads = 256;
     U.smem_row = h->cl > 0 && sizeof(float) * (size_t)h->ld <= (size_t)h->smem_optin - 1024;
@@ -490,6 +492,7 @@ int setup(mmas_ctx* h) {
     h->ld = round_up(n, 32);
     h->ldr = round_up(n, 32);
     h->cl = c.cand_len;
+    h->cl_ld = (h->cl > 0 && h->cl < 32) ? 32 : h->cl;
     h->m = c.n_ants;
     h->alpha = (int)c.alpha;
     h->ant_lo = (int)((int64_t)c.rank * c.n_ants / c.world);
@@ -501,8 +504,8 @@ int setup(mmas_ctx* h) {
     const size_t nn = (size_t)n * h->ld;
     int st;
     if ((st = dalloc(&h->xy, n)) || (st = dalloc(&h->heur, nn)) || (st = dalloc(&h->tau, nn)) ||
-        (st = dalloc(&h->inv_w, nn)) || (st = dalloc(&h->cand_inv, (size_t)n * h->cl + 64)) ||
-        (st = dalloc(&h->cand_id, (size_t)n * h->cl + 64)) ||
+        (st = dalloc(&h->inv_w, nn)) || (st = dalloc(&h->cand_inv, (size_t)n * h->cl_ld + 64)) ||
+        (st = dalloc(&h->cand_id, (size_t)n * h->cl_ld + 64)) ||
         (st = dalloc(&h->routes, (size_t)std::max(h->m_local, 1) * h->ldr)) ||
         (st = dalloc(&h->lengths, (size_t)std::max(h->m_local, 1))) || (st = dalloc(&h->best_key, 1)) ||
         (st = dalloc(&h->fallback_count, 1)) || (st = dalloc(&h->ib_route, n)) || (st = dalloc(&h->gb_route, (size_t)h->ldr)) ||
@@ -545,6 +548,13 @@ int setup(mmas_ctx* h) {
     if (h->cl > 0) {
         std::vector<uint16_t> cand;
         candidate_lists(c.coords, n, h->cl, cand);
+        if (h->cl_ld != h->cl) {   // pad every row to cl_ld slots with the row's own city
+            std::vector<uint16_t> padded((size_t)n * h->cl_ld);
+            for (int i = 0; i < n; ++i)
+                for (int k = 0; k < h->cl_ld; ++k)
+                    padded[(size_t)i * h->cl_ld + k] = k < h->cl ? cand[(size_t)i * h->cl + k] : (uint16_t)i;
+            cand.swap(padded);
+        }
         CU(cudaMemcpyAsync(h->cand_id, cand.data(), sizeof(uint16_t) * cand.size(), cudaMemcpyHostToDevice,
                            h->stream));
         CU(cudaStreamSynchronize(h->stream));
@@ -580,8 +590,8 @@ int setup(mmas_ctx* h) {
         CU(cudaGetLastError());
     }
     if (h->cl > 0) {
-        gather_cand_kernel<<<std::max(1, std::min(4096, (n * h->cl + 255) / 256)), 256, 0, h->stream>>>(
-            h->inv_w, n, h->ld, h->cand_id, h->cand_inv, h->cl);
+        gather_cand_kernel<<<std::max(1, std::min(4096, (n * h->cl_ld + 255) / 256)), 256, 0, h->stream>>>(
+            h->inv_w, n, h->ld, h->cand_id, h->cand_inv, h->cl_ld);
         h->launches++;
         CU(cudaGetLastError());
     }
@@ -606,8 +616,8 @@ int setup(mmas_ctx* h) {
         h->cons_grid = std::max(1, (h->m_local + w - 1) / w);
         h->cons_smem = 128 + (size_t)w * per_warp;
     } else if (h->cl > 0) {
-        h->tb_inv = (uint32_t)round_up(n * h->cl * 4, 16);
-        h->tb_id = (uint32_t)round_up(n * h->cl * 2, 16);
+        h->tb_inv = (uint32_t)round_up(n * h->cl_ld * 4, 16);
+        h->tb_id = (uint32_t)round_up(n * h->cl_ld * 2, 16);
         const size_t per_warp = tabu_bytes;   // per ant warp: its tabu (shared-memory variant)
         // one block per SM holding the whole table; as many ant warps as needed
         int w = std::max(1, std::min(8, (h->m_local + h->num_sms - 1) / std::max(h->num_sms, 1)));
@@ -885,10 +895,11 @@ int mmas_get_candidates(mmas_ctx* h, int32_t* out) {
     if (!out) return fail(MMAS_EINVAL, "out is NULL");
     if (h->cl == 0) return MMAS_OK;
     CU(cudaSetDevice(h->device));
-    std::vector<uint16_t> r((size_t)h->n * h->cl);
+    std::vector<uint16_t> r((size_t)h->n * h->cl_ld);
     CU(cudaMemcpyAsync(r.data(), h->cand_id, sizeof(uint16_t) * r.size(), cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
-    for (size_t e = 0; e < r.size(); ++e) out[e] = r[e];
+    for (int i = 0; i < h->n; ++i)
+        for (int k = 0; k < h->cl; ++k) out[(size_t)i * h->cl + k] = r[(size_t)i * h->cl_ld + k];
     return MMAS_OK;
 }
 
