@@ -323,24 +323,44 @@ def run_ours(args):
 
     # e2e through the C ABI with host buffers: create from host coords (H2D), then per step
     # iterate + read the global best back to the host (D2H), all inside the timed region.
+    # e2e through the C ABI with host buffers, at N GPUs: every rank creates its shard from
+    # pinned host coords (H2D), then per step construct + exchange + update (iterate at N = 1)
+    # and reads the global best length back to the host (D2H); max over ranks.
     e2e = None
-    if rank == 0 and world == 1:
-        torch.cuda.synchronize()
-        pinned = torch.from_numpy(coords.copy()).pin_memory().numpy()
-        out_steps = args.steps
-        t0 = time.perf_counter()
-        c2 = mmas.Colony(pinned, w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
-                         local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection)
-        for _ in range(out_steps):
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    pinned = torch.from_numpy(coords.copy()).pin_memory().numpy()
+    out_steps = args.steps
+    t0 = time.perf_counter()
+    c2 = mmas.Colony(pinned, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
+                     local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection,
+                     stream=stream, rank=rank, world=world)
+    for _ in range(out_steps):
+        if world == 1:
             c2.iterate(1)
-            c2.best_length()
-        tour, _ = c2.best_tour()
-        el = time.perf_counter() - t0
-        c2.close()
-        e2e = {"value": w.n_ants * out_steps / el, "unit": UNIT,
-               "h2d_bytes_per_step": 16 * w.n / out_steps, "d2h_bytes_per_step": 8 + 2 * w.n / out_steps,
-               "note": "timed: mmas_create from pinned host coords (H2D), per step mmas_iterate(1) + "
-                       "mmas_best_length (sync + 8-byte D2H), final mmas_best_tour (D2H of the route)"}
+        else:
+            c2.construct(local.data_ptr())
+            if backend == "nccl":
+                dist.all_gather_into_tensor(gathered, local)
+            else:
+                g_cpu = torch.empty(gathered.shape, dtype=gathered.dtype)
+                dist.all_gather_into_tensor(g_cpu, local.cpu())
+                gathered.copy_(g_cpu)
+            c2.update(gathered.data_ptr(), world)
+        c2.best_length()
+    c2.best_tour()
+    el = time.perf_counter() - t0
+    c2.close()
+    if world > 1:
+        te = torch.tensor([el], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = float(te.item())
+    e2e = {"value": m_total * out_steps / el, "unit": UNIT,
+           "h2d_bytes_per_step": 16 * w.n / out_steps, "d2h_bytes_per_step": 8 + 2 * w.n / out_steps,
+           "note": "timed on every rank, max over ranks: mmas_create from pinned host coords (H2D), per "
+                   "step mmas_iterate(1) (N = 1) or mmas_construct + all-gather + mmas_update (N > 1) + "
+                   "mmas_best_length (sync + 8-byte D2H), final mmas_best_tour (D2H of the route)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
