@@ -100,3 +100,18 @@ def test_ct_sharded_identical_to_single():
         assert np.array_equal(np.concatenate([sh.tours() for sh in shards]), ref.tours())
         for sh in shards:
             assert np.array_equal(sh.tau(), ref.tau())
+
+
+def test_ct_global_best_resume_and_padding_sizes():
+    """Deposit of the global best, resume identity, and list lengths that end exactly on /
+    just past the 512-position unrolled trip pair."""
+    c = make_coords("uniform", 120, 8)
+    lockstep(c, 25, 0, 3, seed=3, tabu=CT, deposit_global=True)
+    a = mmas.Colony(c, 25, 0, seed=5, tabu=CT)
+    b = mmas.Colony(c, 25, 0, seed=5, tabu=CT)
+    a.iterate(1)
+    a.iterate(2)
+    b.iterate(3)
+    assert np.array_equal(a.tours(), b.tours()) and np.array_equal(a.tau(), b.tau())
+    for n in (512, 513, 769):
+        lockstep(make_coords("uniform", n, 90 + n), 6, 0, 1, seed=n, tabu=CT)

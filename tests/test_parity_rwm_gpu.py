@@ -67,3 +67,35 @@ def test_rwm_full_size_sampled_ants(cfg, kw):
         assert np.array_equal(T[a], r), f"ant {a}"
         assert L[a] == l
     assert np.all(np.sort(T, axis=1) == np.arange(w.n))
+
+
+def test_rwm_sharded_identical_to_single():
+    """R21 with the roulette wheel: shards with gathered records == one context."""
+    import torch
+    c = make_coords("uniform", 130, 21)
+    m, world, cl = 37, 3, 12
+    s = torch.cuda.current_stream().cuda_stream
+    ref = mmas.Colony(c, m, cl, seed=6, selection=RWM)
+    shards = [mmas.Colony(c, m, cl, seed=6, stream=s, rank=r, world=world, selection=RWM) for r in range(world)]
+    rb = shards[0].record_bytes
+    recs = torch.zeros(world * rb, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        ref.iterate(1)
+        for r, sh in enumerate(shards):
+            sh.construct(recs.data_ptr() + r * rb)
+        for sh in shards:
+            sh.update(recs.data_ptr(), world)
+        assert np.array_equal(np.concatenate([sh.tours() for sh in shards]), ref.tours())
+        for sh in shards:
+            assert np.array_equal(sh.tau(), ref.tau())
+
+
+def test_rwm_global_best_deposit_and_resume():
+    c = make_coords("uniform", 90, 31)
+    lockstep(c, 20, 0, 3, seed=2, selection=RWM, tabu=CT, deposit_global=True)
+    a = mmas.Colony(c, 20, 8, seed=4, selection=RWM)
+    b = mmas.Colony(c, 20, 8, seed=4, selection=RWM)
+    a.iterate(2)
+    a.iterate(2)
+    b.iterate(4)
+    assert np.array_equal(a.tours(), b.tours()) and np.array_equal(a.tau(), b.tau())
