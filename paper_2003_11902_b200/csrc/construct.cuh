@@ -385,10 +385,13 @@ extern __shared__ __align__(128) unsigned char g_smem[];
 // (1/w, id) table is staged once per block into shared memory by TMA bulk
 // copies, else rows are read through L1/L2; kRegTabu: n <= 1024.
 // ---------------------------------------------------------------------------
-template <int kSlots, bool kSmemTable, bool kRegTabu, bool kFull32>
-__global__ void __launch_bounds__(256, 1) construct_cl_kernel(ConstructArgs A) {
+// kWide: up to 16 ant warps per block (large colonies with the shared-memory table; the
+// register budget drops to 128), else up to 8
+template <int kSlots, bool kSmemTable, bool kRegTabu, bool kFull32, bool kWide = false>
+__global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(ConstructArgs A) {
     pdl_wait();
     static_assert(!kFull32 || kSlots == 1, "kFull32: cl == 32, one slot per lane");
+    static_assert(!kWide || (kFull32 && kSmemTable), "kWide: one-slot shared-memory-table variant only");
     using Tabu = typename std::conditional<kRegTabu, RegTabuX<kFull32>, SmemTabu>::type;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;

@@ -294,25 +294,32 @@ void allow_max_smem(K* kernel, int optin) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
 }
 
-template <int S, bool T, bool R, bool F = false>
+template <int S, bool T, bool R, bool F, bool W = false>
 void set_smem_attr(int optin) {
-    allow_max_smem(construct_cl_kernel<S, T, R, F>, optin);
+    allow_max_smem(construct_cl_kernel<S, T, R, F, W>, optin);
 }
 
-template <int S, bool T, bool R, bool F>
+template <int S, bool T, bool R, bool F, bool W = false>
 void launch_cl_f(mmas_ctx* h, const ConstructArgs& A) {
-    launch_pdl(construct_cl_kernel<S, T, R, F>, dim3(h->cons_grid), dim3(h->cons_warps * 32), h->cons_smem, h->stream, A);
+    launch_pdl(construct_cl_kernel<S, T, R, F, W>, dim3(h->cons_grid), dim3(h->cons_warps * 32), h->cons_smem,
+               h->stream, A);
 }
 
+// cl <= 32 (tables padded to 32 slots): one slot per lane; more than 8 ant warps per block
+// (large colonies, shared-memory table) take the 16-warp instantiation
 template <int S, bool T, bool R>
 void launch_cl(mmas_ctx* h, const ConstructArgs& A) {
     if constexpr (S == 1) {
-        if (h->cl_ld == 32) {
-            launch_cl_f<1, T, R, true>(h, A);
-            return;
+        if constexpr (T) {
+            if (h->cons_warps > 8) {
+                launch_cl_f<1, T, R, true, true>(h, A);
+                return;
+            }
         }
+        launch_cl_f<1, T, R, true>(h, A);
+    } else {
+        launch_cl_f<S, T, R, false>(h, A);
     }
-    launch_cl_f<S, T, R, false>(h, A);
 }
 
 // dispatch over the compile-time variants: slots per lane, table placement, tabu placement
@@ -331,10 +338,10 @@ void launch_cl_r(mmas_ctx* h, const ConstructArgs& A) {
 
 template <bool R>
 void set_cl_attrs(int bytes) {
-    set_smem_attr<1, true, R>(bytes); set_smem_attr<1, false, R>(bytes);
     set_smem_attr<1, true, R, true>(bytes); set_smem_attr<1, false, R, true>(bytes);
-    set_smem_attr<2, true, R>(bytes); set_smem_attr<2, false, R>(bytes);
-    set_smem_attr<4, true, R>(bytes); set_smem_attr<4, false, R>(bytes);
+    set_smem_attr<1, true, R, true, true>(bytes);
+    set_smem_attr<2, true, R, false>(bytes); set_smem_attr<2, false, R, false>(bytes);
+    set_smem_attr<4, true, R, false>(bytes); set_smem_attr<4, false, R, false>(bytes);
 }
 
 int launch_two_opt(mmas_ctx* h, bool fuse_select);
@@ -620,12 +627,15 @@ int setup(mmas_ctx* h) {
         h->tb_id = (uint32_t)round_up(n * h->cl_ld * 2, 16);
         const size_t per_warp = tabu_bytes;   // per ant warp: its tabu (shared-memory variant)
         // one block per SM holding the whole table; as many ant warps as needed
-        int w = std::max(1, std::min(8, (h->m_local + h->num_sms - 1) / std::max(h->num_sms, 1)));
+        const int wmax = h->slots == 1 ? 16 : 8;   // construct_cl_kernel's launch bounds
+        int w = std::max(1, std::min(wmax, (h->m_local + h->num_sms - 1) / std::max(h->num_sms, 1)));
         size_t need = 128 + (size_t)h->tb_inv + h->tb_id + 16 + (size_t)w * per_warp;
         h->smem_table = need <= cons_dyn_max;
         if (h->smem_table) {
+            // persistent: at most one block per SM, each loads the table once and loops over
+            // its ants (large colonies do not re-stage the table per wave)
             h->cons_warps = w;
-            h->cons_grid = std::max(1, (h->m_local + w - 1) / w);
+            h->cons_grid = std::max(1, std::min(h->num_sms, (h->m_local + w - 1) / w));
             h->cons_smem = need;
         } else {
             h->cons_warps = 4;
