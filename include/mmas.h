@@ -141,6 +141,13 @@ int64_t mmas_best_tour(mmas_ctx *h, int32_t *tour_out);
  * MMAS_ESTATE before the first iteration. */
 int64_t mmas_best_length(mmas_ctx *h);
 
+/* Enqueues, on the context's stream and without synchronising, the copy of the current
+ * global best length (int64; -1 while there is none) into `host_dst` (host memory,
+ * caller-owned; pinned memory keeps the copy asynchronous).  The value is valid once the
+ * stream has reached this point (mmas_sync, or any later synchronising call).  Lets a
+ * driver read every iteration's result without a per-iteration host round trip. */
+int mmas_best_length_async(mmas_ctx *h, int64_t *host_dst);
+
 /* Frees every device and host resource.  NULL is a no-op. */
 void mmas_destroy(mmas_ctx *h);
 

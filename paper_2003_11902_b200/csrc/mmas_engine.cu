@@ -854,6 +854,15 @@ int64_t mmas_best_length(mmas_ctx* h) {
     return len;
 }
 
+int mmas_best_length_async(mmas_ctx* h, int64_t* host_dst) {
+    int st = check(h);
+    if (st) return st;
+    if (!host_dst) return fail(MMAS_EINVAL, "host_dst is NULL");
+    CU(cudaSetDevice(h->device));
+    CU(cudaMemcpyAsync(host_dst, h->gb_len, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    return MMAS_OK;
+}
+
 void mmas_destroy(mmas_ctx* h) { free_ctx(h); }
 
 int32_t mmas_n(const mmas_ctx* h) { return h ? h->n : 0; }

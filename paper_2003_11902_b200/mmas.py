@@ -23,7 +23,8 @@ SELECT_WRS, SELECT_RWM = 0, 1
 # every symbol include/mmas.h declares (checked by tests/test_capi.py)
 EXPORTED = (
     "mmas_last_error", "mmas_config_init", "mmas_create", "mmas_create_ex", "mmas_iterate",
-    "mmas_record_bytes", "mmas_construct", "mmas_update", "mmas_best_tour", "mmas_best_length", "mmas_destroy",
+    "mmas_record_bytes", "mmas_construct", "mmas_update", "mmas_best_tour", "mmas_best_length",
+    "mmas_best_length_async", "mmas_destroy",
     "mmas_n", "mmas_iteration", "mmas_get_tours", "mmas_get_lengths", "mmas_get_pheromone",
     "mmas_get_inv_w", "mmas_get_heuristic", "mmas_get_candidates", "mmas_get_limits",
     "mmas_get_stats", "mmas_profile", "mmas_get_phase_times", "mmas_kernel_launches",
@@ -88,6 +89,7 @@ def lib():
     L.mmas_best_tour.restype = ctypes.c_int64
     L.mmas_best_length.argtypes = [V]
     L.mmas_best_length.restype = ctypes.c_int64
+    L.mmas_best_length_async.argtypes = [V, ctypes.c_void_p]
     L.mmas_destroy.argtypes = [V]
     L.mmas_destroy.restype = None
     L.mmas_n.argtypes = [V]
@@ -204,6 +206,11 @@ class Colony:
         if L == MMAS_ESTATE:
             return None
         return int(_err(L))
+
+    def best_length_async(self, host_ptr: int):
+        """Enqueue the 8-byte copy of the global best length (int64, -1 if none) to host_ptr
+        (pinned host memory) on the context's stream; no synchronisation."""
+        _err(lib().mmas_best_length_async(self._h, ctypes.c_void_p(host_ptr)))
 
     # -- introspection --
     @property

@@ -302,3 +302,19 @@ def test_maximum_n_properties():
     assert g.stats()["fallback_steps"] > 0
     tmin, tmax = g.limits()
     assert tmax == np.float32(1.0 / ((1.0 - 0.5) * gl))
+
+
+def test_best_length_async_matches_sync_reads():
+    import torch
+    c = make_coords("uniform", 100, 4)
+    g = mmas.Colony(c, 20, 8, seed=2)
+    buf = torch.full((6,), -7, dtype=torch.int64).pin_memory()
+    g.best_length_async(buf.data_ptr())           # before the first iteration: -1
+    for k in range(5):
+        g.iterate(1)
+        g.best_length_async(buf.data_ptr() + 8 * (k + 1))
+    g.sync()
+    vals = buf.numpy().tolist()
+    assert vals[0] == -1
+    assert vals[-1] == g.best_length() == g.best_tour()[1]
+    assert all(a >= b for a, b in zip(vals[1:], vals[2:]))
