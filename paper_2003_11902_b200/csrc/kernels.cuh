@@ -348,6 +348,59 @@ __global__ void heur_kernel(const double2* __restrict__ xy, int n, int ld, int b
     }
 }
 
+// Nearest-neighbour tour from city 0 (R3; the initial trail limits, Alg. 1):
+// one 1024-thread block; per step every thread takes the closest unvisited city among
+// j = tid, tid + 1024, ... as a (d, j) key, the block reduces the key to its minimum (ties
+// -> lowest id) and thread 0 moves there.  Visited bits in shared memory (n <= 65535).
+constexpr int kNnThreads = 1024;
+__global__ void __launch_bounds__(kNnThreads) nn_tour_kernel(const double2* __restrict__ xy, int n,
+                                                             long long* len_out) {
+    __shared__ uint32_t vis[2048];
+    __shared__ unsigned long long s_key[kNnThreads / 32];
+    __shared__ int s_cur;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int w = tid; w < 2048; w += kNnThreads) vis[w] = 0u;
+    if (tid == 0) {
+        vis[0] = 1u;
+        s_cur = 0;
+    }
+    __syncthreads();
+    long long len = 0;
+    for (int s = 1; s < n; ++s) {
+        const int cur = s_cur;
+        const double2 pc = xy[cur];
+        unsigned long long best = ~0ull;
+        for (int j = tid; j < n; j += kNnThreads) {
+            if ((vis[j >> 5] >> (j & 31)) & 1u) continue;
+            const unsigned long long k = ((unsigned long long)(uint32_t)euc2d(pc, xy[j]) << 32) | (uint32_t)j;
+            best = k < best ? k : best;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long v = __shfl_xor_sync(kFull, best, o);
+            best = v < best ? v : best;
+        }
+        if (lane == 0) s_key[warp] = best;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long b = s_key[lane];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long v = __shfl_xor_sync(kFull, b, o);
+                b = v < b ? v : b;
+            }
+            if (lane == 0) {
+                const int nxt = (int)(b & 0xFFFFFFFFu);
+                len += (long long)(b >> 32);
+                vis[nxt >> 5] |= 1u << (nxt & 31);
+                s_cur = nxt;
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *len_out = len + euc2d(xy[s_cur], xy[0]);
+}
+
 // tau = tau_max (Alg. 1) and inv_w = 1/choice_info.
 __global__ void init_trails_kernel(float* tau, float* inv_w, const float* heur, int n, int ld, int alpha,
                                    const float* scal) {

@@ -68,26 +68,6 @@ void candidate_lists(const double* xy, int n, int cl, std::vector<uint16_t>& out
 }
 
 // nearest-neighbour tour from city 0, ties -> lowest id; returns its length (R3)
-int64_t nn_tour_length(const double* xy, int n) {
-    std::vector<char> vis((size_t)n, 0);
-    int cur = 0;
-    vis[0] = 1;
-    int64_t len = 0;
-    for (int s = 1; s < n; ++s) {
-        int best = -1;
-        int32_t bd = 0;
-        for (int j = 0; j < n; ++j) {
-            if (vis[j]) continue;
-            const int32_t d = host_dist(xy, cur, j);
-            if (best < 0 || d < bd) { best = j; bd = d; }
-        }
-        vis[best] = 1;
-        len += bd;
-        cur = best;
-    }
-    return len + host_dist(xy, cur, 0);
-}
-
 // R2: limits in double, cast to float
 void host_limits(double rho, int64_t cost, double factor, float* tmin, float* tmax) {
     const double tx = 1.0 / ((1.0 - rho) * (double)cost);
@@ -584,7 +564,19 @@ int setup(mmas_ctx* h) {
     }
 
     // initial limits from the NN tour (Alg. 1); F from libm pow (R2)
-    h->nn_len = nn_tour_length(c.coords, n);
+    {
+        // NN tour on the device (one block; the host loop was O(n^2) on one core)
+        long long* d_len = nullptr;
+        CU(cudaMallocAsync(reinterpret_cast<void**>(&d_len), sizeof(long long), h->stream));
+        nn_tour_kernel<<<1, kNnThreads, 0, h->stream>>>(h->xy, n, d_len);
+        h->launches++;
+        CU(cudaGetLastError());
+        long long len = 0;
+        CU(cudaMemcpyAsync(&len, d_len, sizeof(len), cudaMemcpyDeviceToHost, h->stream));
+        CU(cudaFreeAsync(d_len, h->stream));
+        CU(cudaStreamSynchronize(h->stream));
+        h->nn_len = len;
+    }
     const double pn = std::pow(c.p_best, 1.0 / (double)n);
     h->factor = (1.0 - pn) / (((double)n / 2.0 - 1.0) * pn);
     float lim[4] = {0, 0, 0, 0};
