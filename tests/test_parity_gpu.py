@@ -204,13 +204,14 @@ def test_split_calls_equal_iterate():
     assert a.best_tour()[1] == b.best_tour()[1]
 
 
-@pytest.mark.parametrize("world", [2, 3, 5])
-def test_sharded_colony_identical_to_single(world):
+@pytest.mark.parametrize("world,m", [(2, 43), (3, 43), (5, 43), (4, 3)])
+def test_sharded_colony_identical_to_single(world, m):
     """R21: ants sharded over `world` contexts (one GPU here; one per GPU in
-    production) with their records gathered give bit-identical tours and trails."""
+    production) with their records gathered give bit-identical tours and trails;
+    (4, 3) leaves rank 0 without ants (its record never wins)."""
     import torch
     c = make_coords("uniform", 140, 12)
-    m, cl = 43, 16
+    cl = 16
     s = torch.cuda.current_stream().cuda_stream
     ref = mmas.Colony(c, m, cl, seed=4)
     shards = [mmas.Colony(c, m, cl, seed=4, stream=s, rank=r, world=world) for r in range(world)]
