@@ -229,9 +229,34 @@ def run_ours(args):
     local = torch.zeros(rb, dtype=torch.uint8, device="cuda")
     gathered = torch.zeros(world * rb, dtype=torch.uint8, device="cuda")
 
+    # N > 1: the per-iteration exchange goes through the ranks' device memory (CUDA IPC
+    # handles gathered once; P2P stores + device flags, include/mmas.h) unless
+    # MMAS_EXCHANGE=collective, or the wiring fails on any rank (then the NCCL all-gather).
+    exchange = os.environ.get("MMAS_EXCHANGE", "p2p") if world > 1 else "none"
+
+    def wire_p2p(colony):
+        ok = 1
+        try:
+            mine = colony.exchange_ipc_handle()
+            handles = [None] * world
+            dist.all_gather_object(handles, mine)
+            colony.exchange_open_ipc(handles)
+        except Exception as e:   # noqa: BLE001 -- any failure: every rank falls back together
+            print(f"rank {rank}: peer exchange unavailable ({e}); using the collective", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        return bool(flag.item())
+
+    if exchange == "p2p" and not wire_p2p(col):
+        exchange = "collective"
+
     def step():
         if world == 1:
             col.iterate(1)
+        elif exchange == "p2p":
+            col.construct_publish()
+            col.update_exchange()
         else:
             col.construct(local.data_ptr())
             if backend == "nccl":
@@ -246,6 +271,8 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if exchange == "p2p":
+        col.exchange_status()   # raises if a device-side wait timed out during the warm-up
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = col.kernel_launches
@@ -337,9 +364,14 @@ def run_ours(args):
     c2 = mmas.Colony(pinned, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
                      local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection,
                      stream=stream, rank=rank, world=world)
+    if exchange == "p2p":
+        wire_p2p(c2)
     for k in range(out_steps):
         if world == 1:
             c2.iterate(1)
+        elif exchange == "p2p":
+            c2.construct_publish()
+            c2.update_exchange()
         else:
             c2.construct(local.data_ptr())
             if backend == "nccl":
@@ -382,6 +414,9 @@ def run_ours(args):
                                        f"cl={w.cand_len}, rho={w.rho}, alpha=1, beta=2",
                            "n": w.n, "ants_per_gpu": w.n_ants, "global_ants": m_total, "cand_len": w.cand_len,
                            "parallelism": f"ant-sharded x{world}" if world > 1 else "single GPU",
+                           "exchange": {"p2p": "peer memory: CUDA IPC buffers, P2P record stores + device flags",
+                                        "collective": f"{backend} all-gather of the records",
+                                        "none": "none (one GPU)"}[exchange],
                            "l2": "flushed between timed steps (256 MiB write, outside the step events)",
                            "tabu": "compact" if w.tabu else "bitmask",
                            "selection": "roulette wheel" if w.selection else "WRS",

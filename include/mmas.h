@@ -131,6 +131,33 @@ int mmas_construct(mmas_ctx *h, void *record_dev);
  * the global best and limits, and runs the pheromone update.  Asynchronous. */
 int mmas_update(mmas_ctx *h, const void *records_dev, int32_t count);
 
+/* ---- Peer-memory exchange (row a7 without a collective library) ----------------------
+ * Instead of mmas_construct -> all-gather -> mmas_update, the ranks can exchange their
+ * records through each other's device memory (NVLink P2P stores on an NVSwitch node).
+ * Every context owns an exchange buffer of mmas_exchange_bytes(h) bytes ([2][world]
+ * records, then [2][world] uint32 flags).  Wire them up once, collectively:
+ *   - across processes: mmas_exchange_ipc_handle(h, 64-byte cudaIpcMemHandle out), gather
+ *     every rank's handle (world x 64 bytes, rank order) and mmas_exchange_open_ipc(h, all);
+ *   - within one process: mmas_exchange_buffer(h, &dev_ptr) on every context and
+ *     mmas_exchange_attach(h, ptrs) with the world device pointers in rank order.
+ * Then each iteration is mmas_construct_publish(h) (construction; the shard's best record
+ * is written into slot `rank` of every buffer and a flag raised in each) followed by
+ * mmas_update_exchange(h) (waits on the device until every rank's flag of this iteration
+ * is up, selects, updates); mmas_iterate_exchange(h, iters) does both.  The wait is
+ * bounded (~2^34 GPU cycles): a lost peer sets an error that mmas_exchange_status(h)
+ * reports as MMAS_ENCCL.  Iteration t uses buffer half t & 1, so ranks stay lockstep
+ * without further synchronisation.  All calls are asynchronous except the wiring and
+ * mmas_exchange_status. */
+int64_t mmas_exchange_bytes(const mmas_ctx *h);
+int mmas_exchange_buffer(mmas_ctx *h, void **buffer_dev);
+int mmas_exchange_ipc_handle(mmas_ctx *h, void *handle_out);
+int mmas_exchange_open_ipc(mmas_ctx *h, const void *handles);
+int mmas_exchange_attach(mmas_ctx *h, void *const *peer_buffers);
+int mmas_construct_publish(mmas_ctx *h);
+int mmas_update_exchange(mmas_ctx *h);
+int mmas_iterate_exchange(mmas_ctx *h, int32_t iters);
+int mmas_exchange_status(mmas_ctx *h);
+
 /* Synchronises the context's stream and copies the global best route (n city
  * ids, starting at its route[0]) into tour_out (host, n int32, caller-owned).
  * Returns its length (>= 0), or MMAS_ESTATE before the first iteration (gb

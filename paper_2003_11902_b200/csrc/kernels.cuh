@@ -226,6 +226,73 @@ __global__ void publish_kernel(unsigned long long* local_key, const uint16_t* ro
 }
 
 // ---------------------------------------------------------------------------
+// Peer-memory exchange (row a7 without a collective library): every rank's exchange
+// buffer holds [2 parities][world] records then [2][world] u32 flags.  Iteration t uses
+// parity t & 1 and sequence number t + 1.  A rank writes its record straight into slot
+// `rank` of every peer's buffer (NVLink P2P stores; its own buffer included), fences
+// system-wide, then raises its flag in every peer.  Double buffering by parity is enough:
+// a rank publishes iteration t + 2 only after its update t + 1, which waited for every
+// rank's record of t + 1, published after that rank had finished reading iteration t.
+// ---------------------------------------------------------------------------
+struct ExchangeArgs {
+    unsigned char* const* peers;   // device array: every rank's exchange buffer (peer-mapped)
+    int world, rank, rec_bytes;
+    uint32_t parity, seq;
+};
+__device__ __forceinline__ unsigned char* xrecord(unsigned char* buf, const ExchangeArgs& X, int p, int r) {
+    return buf + ((size_t)p * X.world + r) * X.rec_bytes;
+}
+__device__ __forceinline__ uint32_t* xflag(unsigned char* buf, const ExchangeArgs& X, int p, int r) {
+    return reinterpret_cast<uint32_t*>(buf + (size_t)2 * X.world * X.rec_bytes) + p * X.world + r;
+}
+
+// One block: this shard's best record (key = len << 24 | global ant, route) to every peer.
+__global__ void publish_peers_kernel(unsigned long long* local_key, const uint16_t* routes, int ldr, int ant_lo,
+                                     int n, int m_local, ExchangeArgs X) {
+    pdl_wait();
+    __shared__ unsigned long long key;
+    if (threadIdx.x == 0) key = m_local > 0 ? *local_key : ~0ull;   // an empty shard never wins
+    __syncthreads();
+    const int al = (int)(key & 0xFFFFFFu) - ant_lo;
+    for (int p = 0; p < X.world; ++p) {
+        unsigned char* rec = xrecord(X.peers[p], X, (int)X.parity, X.rank);
+        if (m_local > 0) {
+            uint16_t* dst = reinterpret_cast<uint16_t*>(rec + 8);
+            for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = routes[(size_t)al * ldr + k];
+        }
+        if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned long long*>(rec) = key;
+    }
+    __threadfence_system();   // records visible to every peer before any flag
+    __syncthreads();
+    if (threadIdx.x < X.world) {
+        volatile uint32_t* f = xflag(X.peers[threadIdx.x], X, (int)X.parity, X.rank);
+        *f = X.seq;
+    }
+    if (threadIdx.x == 0 && m_local > 0) *local_key = ~0ull;
+}
+
+// One warp: wait until every rank's flag of this parity carries this iteration's sequence
+// number (bounded: after ~2^34 cycles the error word is set and the wait gives up, so a
+// lost peer fails the context instead of hanging the GPU), then acquire.
+__global__ void wait_peers_kernel(unsigned char* own, ExchangeArgs X, uint32_t* err) {
+    pdl_wait();
+    const int r = threadIdx.x;
+    if (r < X.world) {
+        volatile uint32_t* f = xflag(own, X, (int)X.parity, r);
+        const long long t0 = clock64();
+        while (*f != X.seq) {
+            if (clock64() - t0 > (1ll << 34)) {
+                atomicExch(err, 1u);
+                break;
+            }
+            __nanosleep(200);
+        }
+    }
+    __syncwarp();
+    __threadfence();
+}
+
+// ---------------------------------------------------------------------------
 // Pheromone update (row a6; Alg. 1, R1/R4-R6, R22):
 //   tau <- min(max(rho tau, tau_min) + Delta [(i,j) in T_dep], tau_max)
 //   inv_w <- 1 / (tau^alpha heur);  cand_inv[i][k] <- inv_w[i][cand_id[i][k]]

@@ -134,6 +134,13 @@ struct mmas_ctx {
     uint32_t* ls_inq = nullptr;
     unsigned long long* ls_moves = nullptr;
 
+    // peer-memory exchange (row a7 without a collective library; world > 1)
+    unsigned char* xbuf = nullptr;            // own buffer: [2][world] records + [2][world] flags
+    unsigned char** xpeers_dev = nullptr;     // device array of every rank's (peer-mapped) buffer
+    std::vector<void*> xopened;               // IPC mappings to close
+    uint32_t* xerr = nullptr;                 // set by wait_peers_kernel on timeout
+    bool xattached = false;
+
     // profiling
     bool profiling = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -450,6 +457,10 @@ void free_ctx(mmas_ctx* h) {
                     h->ls_nn, h->ls_pos, h->ls_queue, h->ls_inq, h->ls_moves};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (void* p : h->xopened) cudaIpcCloseMemHandle(p);
+    if (h->xbuf) cudaFree(h->xbuf);
+    if (h->xpeers_dev) cudaFree(h->xpeers_dev);
+    if (h->xerr) cudaFree(h->xerr);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
@@ -791,6 +802,139 @@ int mmas_construct(mmas_ctx* h, void* record_dev) {
     }
     CU(cudaGetLastError());
     return MMAS_OK;
+}
+
+// ---- peer-memory exchange ----------------------------------------------------------
+int64_t mmas_exchange_bytes(const mmas_ctx* h) {
+    if (!h) return MMAS_EINVAL;
+    return (int64_t)2 * h->cfg.world * h->rec_bytes + (int64_t)2 * h->cfg.world * 4;
+}
+
+static int ensure_xbuf(mmas_ctx* h) {
+    if (h->xbuf) return MMAS_OK;
+    if (h->cfg.world < 2) return fail(MMAS_ESTATE, "the peer exchange needs world > 1");
+    CU(cudaSetDevice(h->device));
+    const size_t bytes = (size_t)mmas_exchange_bytes(h);
+    CU(cudaMalloc(reinterpret_cast<void**>(&h->xbuf), bytes));   // cudaMalloc: IPC-exportable
+    CU(cudaMemset(h->xbuf, 0, bytes));
+    CU(cudaMalloc(reinterpret_cast<void**>(&h->xerr), sizeof(uint32_t)));
+    CU(cudaMemset(h->xerr, 0, sizeof(uint32_t)));
+    CU(cudaMalloc(reinterpret_cast<void**>(&h->xpeers_dev), sizeof(unsigned char*) * h->cfg.world));
+    return MMAS_OK;
+}
+
+int mmas_exchange_buffer(mmas_ctx* h, void** buffer_dev) {
+    int st = check(h);
+    if (st) return st;
+    if (!buffer_dev) return fail(MMAS_EINVAL, "buffer_dev is NULL");
+    if ((st = ensure_xbuf(h))) return st;
+    *buffer_dev = h->xbuf;
+    return MMAS_OK;
+}
+
+int mmas_exchange_ipc_handle(mmas_ctx* h, void* handle_out) {
+    int st = check(h);
+    if (st) return st;
+    if (!handle_out) return fail(MMAS_EINVAL, "handle_out is NULL");
+    if ((st = ensure_xbuf(h))) return st;
+    cudaIpcMemHandle_t hd;
+    CU(cudaIpcGetMemHandle(&hd, h->xbuf));
+    std::memcpy(handle_out, &hd, sizeof(hd));
+    return MMAS_OK;
+}
+
+int mmas_exchange_attach(mmas_ctx* h, void* const* peer_buffers) {
+    int st = check(h);
+    if (st) return st;
+    if (!peer_buffers) return fail(MMAS_EINVAL, "peer_buffers is NULL");
+    if ((st = ensure_xbuf(h))) return st;
+    std::vector<unsigned char*> v((size_t)h->cfg.world);
+    for (int p = 0; p < h->cfg.world; ++p) {
+        v[p] = p == h->cfg.rank ? h->xbuf : static_cast<unsigned char*>(peer_buffers[p]);
+        if (!v[p]) return fail(MMAS_EINVAL, "peer buffer is NULL");
+    }
+    CU(cudaMemcpy(h->xpeers_dev, v.data(), sizeof(unsigned char*) * v.size(), cudaMemcpyHostToDevice));
+    h->xattached = true;
+    return MMAS_OK;
+}
+
+int mmas_exchange_open_ipc(mmas_ctx* h, const void* handles) {
+    int st = check(h);
+    if (st) return st;
+    if (!handles) return fail(MMAS_EINVAL, "handles is NULL");
+    if ((st = ensure_xbuf(h))) return st;
+    std::vector<void*> bufs((size_t)h->cfg.world, nullptr);
+    for (int p = 0; p < h->cfg.world; ++p) {
+        if (p == h->cfg.rank) continue;
+        cudaIpcMemHandle_t hd;
+        std::memcpy(&hd, static_cast<const unsigned char*>(handles) + (size_t)p * sizeof(hd), sizeof(hd));
+        CU(cudaIpcOpenMemHandle(&bufs[p], hd, cudaIpcMemLazyEnablePeerAccess));
+        h->xopened.push_back(bufs[p]);
+    }
+    return mmas_exchange_attach(h, bufs.data());
+}
+
+static ExchangeArgs exchange_args(mmas_ctx* h) {
+    ExchangeArgs X{};
+    X.peers = h->xpeers_dev;
+    X.world = h->cfg.world;
+    X.rank = h->cfg.rank;
+    X.rec_bytes = h->rec_bytes;
+    X.parity = (uint32_t)h->iteration & 1u;
+    X.seq = (uint32_t)h->iteration + 1u;
+    return X;
+}
+
+int mmas_construct_publish(mmas_ctx* h) {
+    int st = check(h);
+    if (st) return st;
+    if (!h->xattached) return fail(MMAS_ESTATE, "attach the peer exchange buffers first");
+    CU(cudaSetDevice(h->device));
+    if ((st = launch_construct(h, false))) return st;
+    launch_pdl(publish_peers_kernel, dim3(1), dim3(256), 0, h->stream, h->best_key,
+               static_cast<const uint16_t*>(h->routes), h->ldr, h->ant_lo, h->n, h->m_local, exchange_args(h));
+    h->launches++;
+    CU(cudaGetLastError());
+    return MMAS_OK;
+}
+
+int mmas_update_exchange(mmas_ctx* h) {
+    int st = check(h);
+    if (st) return st;
+    if (!h->xattached) return fail(MMAS_ESTATE, "attach the peer exchange buffers first");
+    CU(cudaSetDevice(h->device));
+    const ExchangeArgs X = exchange_args(h);
+    {
+        PhaseScope ps(h, 1);
+        wait_peers_kernel<<<1, 32, 0, h->stream>>>(h->xbuf, X, h->xerr);
+        h->launches++;
+        CU(cudaGetLastError());
+    }
+    if ((st = launch_select(h, h->xbuf + (size_t)X.parity * X.world * X.rec_bytes, X.world))) return st;
+    if ((st = launch_update(h))) return st;
+    h->iteration++;
+    if (h->profiling) h->acc_iters++;
+    return MMAS_OK;
+}
+
+int mmas_iterate_exchange(mmas_ctx* h, int32_t iters) {
+    int st = check(h);
+    if (st) return st;
+    if (iters < 1) return fail(MMAS_EINVAL, "iters must be >= 1");
+    for (int32_t i = 0; i < iters; ++i)
+        if ((st = mmas_construct_publish(h)) || (st = mmas_update_exchange(h))) return st;
+    return MMAS_OK;
+}
+
+int mmas_exchange_status(mmas_ctx* h) {
+    int st = check(h);
+    if (st) return st;
+    if (!h->xerr) return MMAS_OK;
+    CU(cudaSetDevice(h->device));
+    uint32_t e = 0;
+    CU(cudaMemcpyAsync(&e, h->xerr, sizeof(e), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return e ? fail(MMAS_ENCCL, "peer exchange timed out waiting for a rank's record") : MMAS_OK;
 }
 
 int mmas_update(mmas_ctx* h, const void* records_dev, int32_t count) {

@@ -25,6 +25,9 @@ EXPORTED = (
     "mmas_last_error", "mmas_config_init", "mmas_create", "mmas_create_ex", "mmas_iterate",
     "mmas_record_bytes", "mmas_construct", "mmas_update", "mmas_best_tour", "mmas_best_length",
     "mmas_best_length_async", "mmas_destroy",
+    "mmas_exchange_bytes", "mmas_exchange_buffer", "mmas_exchange_ipc_handle", "mmas_exchange_open_ipc",
+    "mmas_exchange_attach", "mmas_construct_publish", "mmas_update_exchange", "mmas_iterate_exchange",
+    "mmas_exchange_status",
     "mmas_n", "mmas_iteration", "mmas_get_tours", "mmas_get_lengths", "mmas_get_pheromone",
     "mmas_get_inv_w", "mmas_get_heuristic", "mmas_get_candidates", "mmas_get_limits",
     "mmas_get_stats", "mmas_profile", "mmas_get_phase_times", "mmas_kernel_launches",
@@ -85,6 +88,15 @@ def lib():
     L.mmas_record_bytes.restype = ctypes.c_int64
     L.mmas_construct.argtypes = [V, V]
     L.mmas_update.argtypes = [V, V, ctypes.c_int32]
+    L.mmas_exchange_bytes.argtypes = [V]
+    L.mmas_exchange_bytes.restype = ctypes.c_int64
+    L.mmas_exchange_buffer.argtypes = [V, ctypes.POINTER(ctypes.c_void_p)]
+    L.mmas_exchange_ipc_handle.argtypes = [V, ctypes.c_char_p]
+    L.mmas_exchange_open_ipc.argtypes = [V, ctypes.c_char_p]
+    L.mmas_exchange_attach.argtypes = [V, ctypes.POINTER(ctypes.c_void_p)]
+    for name in ("mmas_construct_publish", "mmas_update_exchange", "mmas_exchange_status"):
+        getattr(L, name).argtypes = [V]
+    L.mmas_iterate_exchange.argtypes = [V, ctypes.c_int32]
     L.mmas_best_tour.argtypes = [V, P(ctypes.c_int32)]
     L.mmas_best_tour.restype = ctypes.c_int64
     L.mmas_best_length.argtypes = [V]
@@ -188,6 +200,38 @@ class Colony:
 
     def construct(self, record_dev_ptr: int):
         _err(lib().mmas_construct(self._h, ctypes.c_void_p(record_dev_ptr)))
+
+    # -- peer-memory exchange (include/mmas.h; R21 without a collective library) --
+    def exchange_ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _err(lib().mmas_exchange_ipc_handle(self._h, buf))
+        return buf.raw
+
+    def exchange_open_ipc(self, handles):
+        """handles: every rank's 64-byte handle in rank order."""
+        blob = b"".join(handles)
+        _err(lib().mmas_exchange_open_ipc(self._h, blob))
+
+    def exchange_buffer(self) -> int:
+        p = ctypes.c_void_p()
+        _err(lib().mmas_exchange_buffer(self._h, ctypes.byref(p)))
+        return p.value
+
+    def exchange_attach(self, buffers):
+        arr = (ctypes.c_void_p * len(buffers))(*buffers)
+        _err(lib().mmas_exchange_attach(self._h, arr))
+
+    def construct_publish(self):
+        _err(lib().mmas_construct_publish(self._h))
+
+    def update_exchange(self):
+        _err(lib().mmas_update_exchange(self._h))
+
+    def iterate_exchange(self, iters=1):
+        _err(lib().mmas_iterate_exchange(self._h, int(iters)))
+
+    def exchange_status(self):
+        _err(lib().mmas_exchange_status(self._h))
 
     def update(self, records_dev_ptr: int, count: int):
         _err(lib().mmas_update(self._h, ctypes.c_void_p(records_dev_ptr), int(count)))

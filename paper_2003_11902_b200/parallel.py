@@ -52,3 +52,33 @@ class ShardedColony:
 
     def close(self):
         self.colony.close()
+
+
+class PeerShardedColony:
+    """One rank's share of a colony whose per-iteration exchange goes through the ranks'
+    device memory instead of a collective: CUDA IPC handles of every rank's exchange buffer
+    are all-gathered once (torch.distributed, any backend), then each iteration is
+    construct + peer publish + device-side wait + update (mmas_iterate_exchange)."""
+
+    def __init__(self, coords, n_ants, cand_len, group=None, **kw):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        dev = torch.cuda.current_device()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        self.colony = mmas.Colony(coords, n_ants, cand_len, device=dev, stream=stream,
+                                  rank=self.rank, world=self.world, **kw)
+        mine = self.colony.exchange_ipc_handle()
+        handles = [None] * self.world
+        dist.all_gather_object(handles, mine, group=group)
+        self.colony.exchange_open_ipc(handles)
+        dist.barrier(group=group)
+
+    def iterate(self, iters: int = 1):
+        self.colony.iterate_exchange(iters)
+
+    def best_tour(self):
+        return self.colony.best_tour()
+
+    def close(self):
+        self.colony.close()

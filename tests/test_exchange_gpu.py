@@ -1,0 +1,86 @@
+"""The peer-memory exchange (row a7 without a collective library, include/mmas.h):
+shards publish their best record straight into every rank's device buffer and wait on
+device flags.  Checked against one unsharded context, bit for bit: in one process
+(buffers attached by pointer, every shard's construction enqueued before any update)
+and across two processes on one GPU (CUDA IPC handles, concurrent device-side waits)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_2003_11902_b200 import mmas
+from paper_2003_11902_b200.instances import make_coords
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world,m,cl", [(2, 40, 16), (3, 43, 0), (4, 3, 8)])
+def test_in_process_peer_exchange_equals_single(world, m, cl):
+    c = make_coords("uniform", 150, 17)
+    s = torch.cuda.current_stream().cuda_stream
+    ref = mmas.Colony(c, m, cl, seed=8)
+    shards = [mmas.Colony(c, m, cl, seed=8, stream=s, rank=r, world=world) for r in range(world)]
+    bufs = [sh.exchange_buffer() for sh in shards]
+    for sh in shards:
+        sh.exchange_attach(bufs)
+    for it in range(5):
+        ref.iterate(1)
+        for sh in shards:
+            sh.construct_publish()
+        for sh in shards:
+            sh.update_exchange()
+        assert np.array_equal(np.concatenate([sh.tours() for sh in shards]), ref.tours()), f"iteration {it}"
+        for sh in shards:
+            assert np.array_equal(sh.tau(), ref.tau())
+            assert sh.best_tour()[1] == ref.best_tour()[1]
+    for sh in shards:
+        sh.exchange_status()
+
+
+def _free_port():
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    p = sk.getsockname()[1]
+    sk.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2003_11902_b200.parallel import PeerShardedColony
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        col = PeerShardedColony(make_coords("uniform", 120, 5), 30, 16, seed=3)
+        col.iterate(4)
+        col.colony.exchange_status()
+        q.put((rank, col.colony.tours().tolist(), col.colony.tau().sum(dtype=np.float64), col.best_tour()[1]))
+        dist.barrier()
+        col.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_ipc_peer_exchange_equals_single():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = mmas.Colony(make_coords("uniform", 120, 5), 30, 16, seed=3)
+    ref.iterate(4)
+    tours = np.concatenate([np.array(o[1], dtype=np.int32).reshape(-1, 120) for o in out])
+    assert np.array_equal(tours, ref.tours())
+    assert all(o[2] == ref.tau().sum(dtype=np.float64) for o in out)
+    assert all(o[3] == ref.best_tour()[1] for o in out)
