@@ -223,6 +223,7 @@ def run_ours(args):
     coords = w.coords()
     stream = torch.cuda.current_stream().cuda_stream
     col = mmas.Colony(coords, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
+                      separate_update=args.separate_update,
                       local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection,
                       stream=stream, rank=rank, world=world)
     rb = col.record_bytes
@@ -306,6 +307,12 @@ def run_ours(args):
     bytes_per_launch = algorithmic_bytes_per_tour(w) * col.shard()[1]
     cons_kernel = ("construct_rwm_kernel" if w.selection else "construct_cl_kernel" if w.cand_len else
                    "construct_ct_kernel" if w.tabu else "construct_full_kernel")
+    # world == 1 with the table in shared memory: the update (row a6) runs inside the same
+    # launch (construct.cuh fused_update), so that launch also moves the update's 16 n^2 B
+    fused = bool(col.stats()["update_fused"])
+    upd_bytes = 16 * w.n * w.n
+    if fused:
+        bytes_per_launch += upd_bytes
     hbm_peak, peak_src = measured_peaks()
     achieved = bytes_per_launch / (cons_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
@@ -313,7 +320,7 @@ def run_ours(args):
                 "traffic_note": "DRAM bytes per launch (ncu capture, profiles/ncu_traffic.json); with the "
                                 "candidate table in shared memory (C1, C2: TMA-staged once per launch) or "
                                 "L2-resident rows, HBM traffic is far below the algorithmic bytes",
-                "kernel": cons_kernel,
+                "kernel": cons_kernel + (" (+ fused pheromone update)" if fused else ""),
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
                 "kernel_ms": cons_ms, "kernel_share_of_step": cons_ms / (total_ms / args.steps),
                 "algorithmic_bytes_per_launch": bytes_per_launch,
@@ -341,12 +348,18 @@ def run_ours(args):
                                  "resident at once (warps_per_sm <= 64); tools/micro_step.cu measures the "
                                  "chain alone at ~145-160 cycles/step"}
     update_ms = phases["update_ms"] / max(phases["iterations"], 1)
-    upd_bytes = 16 * w.n * w.n
-    update_roof = {"kernel": "pheromone_update_kernel", "kernel_ms": update_ms,
-                   "traffic": ncu_traffic(args.config, "pheromone_update_kernel"),
-                   "achieved_gbs": upd_bytes / (update_ms * 1e-3) / 1e9,
-                   "frac": upd_bytes / (update_ms * 1e-3) / 1e9 / hbm_peak,
-                   "algorithmic_bytes_per_launch": upd_bytes}
+    if fused:
+        update_roof = {"kernel": "fused into " + cons_kernel, "fused": True, "algorithmic_bytes_per_launch": upd_bytes,
+                       "note": "one launch per iteration: construction, grid barrier (the last block selects the "
+                               "iteration best), then every warp updates its rows from tau/heur rows TMA-prefetched "
+                               "into shared memory during the construction tail; its bytes are counted in "
+                               "roofline.algorithmic_bytes_per_launch"}
+    else:
+        update_roof = {"kernel": "pheromone_update_kernel", "kernel_ms": update_ms,
+                       "traffic": ncu_traffic(args.config, "pheromone_update_kernel"),
+                       "achieved_gbs": upd_bytes / (update_ms * 1e-3) / 1e9,
+                       "frac": upd_bytes / (update_ms * 1e-3) / 1e9 / hbm_peak,
+                       "algorithmic_bytes_per_launch": upd_bytes}
 
     # e2e through the C ABI with host buffers: create from host coords (H2D), then per step
     # iterate + read the global best back to the host (D2H), all inside the timed region.
@@ -362,6 +375,7 @@ def run_ours(args):
     best_host = torch.full((out_steps,), -1, dtype=torch.int64).pin_memory()   # per-step results
     t0 = time.perf_counter()
     c2 = mmas.Colony(pinned, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
+                     separate_update=args.separate_update,
                      local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection,
                      stream=stream, rank=rank, world=world)
     if exchange == "p2p":
@@ -421,6 +435,8 @@ def run_ours(args):
                            "tabu": "compact" if w.tabu else "bitmask",
                            "selection": "roulette wheel" if w.selection else "WRS",
                            "local_search": "2-opt" if w.local_search else "none",
+                           "iteration_launches": "one (construction + selection + update fused)" if fused else
+                                                 "construction (+ selection) then update",
                            "paper_context": PAPER_CONTEXT.get(args.config, "") + " (other hardware, context only)"},
                 "roofline": roofline, "update_roofline": update_roof,
                 "phases_ms_per_step": {"construct": cons_ms, "select": phases["select_ms"] / max(phases["iterations"], 1),
@@ -445,6 +461,8 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--separate-update", action="store_true",
+                    help="run the pheromone update as its own kernel (A/B against the fused launch)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -78,6 +78,10 @@ typedef struct mmas_config {
                               if non-NULL, else on a non-blocking stream owned by the context */
     int32_t tabu;          /* MMAS_TABU_*; default BITMASK.  COMPACT needs cand_len == 0 (R27) */
     int32_t selection;     /* MMAS_SELECT_*; default WRS (R28) */
+    int32_t separate_update; /* 1: always run the pheromone update (row a6) as its own kernel.
+                              0 (default): with world == 1, no local search, cand_len <= 32 and the
+                              candidate table in shared memory, the update runs inside the
+                              construction launch after a grid barrier (same results bit for bit) */
 } mmas_config;
 
 /* Per-context counters (cumulative since create). */
@@ -88,6 +92,9 @@ typedef struct mmas_stats {
     int32_t ants_local;       /* ants built by this context per iteration */
     int32_t first_ant;        /* global id of the first of them */
     int64_t local_search_moves; /* improving 2-opt moves applied (row a8), this shard */
+    int32_t update_fused;     /* 1: mmas_iterate runs construction + selection + update as ONE
+                                 launch (see mmas_config.separate_update) */
+    int32_t reserved_;
 } mmas_stats;
 
 /* Last error message of this thread ("" if none). */

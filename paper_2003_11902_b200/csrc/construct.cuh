@@ -283,7 +283,7 @@ __device__ __forceinline__ unsigned long long finish_ant(const ConstructArgs& A,
 // ONE atomic each (a per-ant global atomic makes ~10^3 same-address atomics queue
 // up at the end of the launch).  world == 1: the last block to finish selects the
 // iteration best with one warp (row a5; all route writes are fenced first).
-__device__ __forceinline__ void block_finish(const ConstructArgs& A, unsigned long long wbest, long long wfb,
+__device__ __forceinline__ bool block_finish(const ConstructArgs& A, unsigned long long wbest, long long wfb,
                                              int lane, int warp) {
     __shared__ unsigned long long s_best, s_fb;
     __shared__ unsigned s_last;
@@ -309,11 +309,13 @@ __device__ __forceinline__ void block_finish(const ConstructArgs& A, unsigned lo
         s_last = last;
     }
     __syncthreads();
-    if (s_last && warp == 0) {
+    const bool last = s_last != 0u;
+    if (last && warp == 0) {
         __threadfence();
         select_best_warp(A.sel, lane);
         if (lane == 0) *A.done = 0u;
     }
+    return last;
 }
 
 // Route staging: lane (s & 31) keeps route[s]; every 32 steps the warp writes a
@@ -361,6 +363,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     }
 }
 
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const unsigned int* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
     unsigned short v;
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
@@ -378,6 +389,85 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
 //   [.., +Tid)               cand_id   n x cl u16   (smem-table variant)
 //   [.., + W * 4*nwords)     tabu words (SmemTabu variant)
 extern __shared__ __align__(128) unsigned char g_smem[];
+
+// ---------------------------------------------------------------------------
+// Pheromone update fused into the construction launch (row a6; world == 1, persistent
+// shared-memory-table grid, every block resident at once).  Same arithmetic as
+// pheromone_update_kernel (update_quad), different schedule:
+//   1. a block past its construction no longer needs its candidate table, so each warp
+//      TMA-copies its first row of tau and heur into that shared memory while the rest of
+//      the grid is still constructing (the update's loads leave the critical path);
+//   2. grid barrier: the last block to finish runs the iteration-best selection (row a5,
+//      block_finish) and bumps the epoch word; the others spin on it (acquire);
+//   3. warp w updates rows w, w + W, ... from shared memory: float4 stores of tau and
+//      inv_w, the new inv_w row kept in shared memory for the candidate gather.
+// Removes the update launch and its ramp from the iteration.
+// Shared memory: [128 + 8w) mbarrier of warp w, [256 + 2w rowbytes) its tau / heur rows.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void fused_update(const UpdateArgs U, unsigned int* epoch, bool last_block, uint32_t epoch0,
+                                          int lane, int warp) {
+    const int wpb = (int)(blockDim.x >> 5);
+    const int tw = (int)gridDim.x * wpb;
+    const uint32_t rowbytes = (uint32_t)U.ld * 4u;
+    float* s_tau = reinterpret_cast<float*>(g_smem + 256 + (size_t)warp * 2 * rowbytes);
+    float* s_heur = s_tau + U.ld;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem + 128) + warp;
+    int i = (int)blockIdx.x * wpb + warp;
+    // the table's generic-proxy reads are ordered before the async-proxy writes that reuse it
+    fence_proxy_async_smem();
+    if (lane == 0) mbar_init(bar, 1);
+    __syncwarp();
+    auto fetch = [&](int row) {
+        if (lane == 0) {
+            mbar_expect_tx(bar, 2u * rowbytes);
+            bulk_g2s(smem_u32(s_tau), U.tau + (size_t)row * U.ld, rowbytes, bar);
+            bulk_g2s(smem_u32(s_heur), U.heur + (size_t)row * U.ld, rowbytes, bar);
+        }
+    };
+    uint32_t cid = 0;
+    if (i < U.n) {
+        fetch(i);
+        if (lane < U.cl) cid = __ldg(U.cand_id + (size_t)i * U.cl + lane);
+    }
+    // grid barrier (all blocks are resident: grid <= SMs, one block each)
+    __syncthreads();   // the last block's selection warp is done
+    if (threadIdx.x == 0) {
+        if (last_block) {
+            __threadfence();
+            atomicAdd(epoch, 1u);
+        }
+        while (ld_acquire_gpu(epoch) == epoch0) __nanosleep(32);
+    }
+    __syncthreads();
+    const float tmin = __ldcg(U.scal), tmax = __ldcg(U.scal + 1), delta = __ldcg(U.scal + 2);
+    const int n4 = (U.n + 3) >> 2;
+    uint32_t phase = 0;
+    for (; i < U.n; i += tw) {
+        const int si = __ldcg(U.succ + i), pi = __ldcg(U.pred + i);
+        float4* trow = reinterpret_cast<float4*>(U.tau + (size_t)i * U.ld);
+        float4* wrow = reinterpret_cast<float4*>(U.inv_w + (size_t)i * U.ld);
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        for (int q = lane; q < n4; q += 32) {
+            float4 t = reinterpret_cast<const float4*>(s_tau)[q];
+            const float4 h = reinterpret_cast<const float4*>(s_heur)[q];
+            const float4 w4 = update_quad(t, h, 4 * q, si, pi, U.rho_f, tmin, tmax, delta, U.alpha);
+            trow[q] = t;
+            wrow[q] = w4;
+            reinterpret_cast<float4*>(s_tau)[q] = w4;   // the new inv_w row, for the gather
+        }
+        __syncwarp();
+        if (lane < U.cl) U.cand_inv[(size_t)i * U.cl + lane] = s_tau[cid];
+        __syncwarp();
+        if (i + tw < U.n) {
+            fence_proxy_async_smem();
+            fetch(i + tw);
+            if (lane < U.cl) cid = __ldg(U.cand_id + (size_t)(i + tw) * U.cl + lane);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *U.iter_dev += 1u;
+}
+
 
 // ---------------------------------------------------------------------------
 // Candidate-list construction (rows a1, a2, a3, a5-local).
@@ -426,6 +516,8 @@ __global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(Cons
     const uint32_t inv_lane = s_inv + 4u * (uint32_t)lane;
     uint32_t* tabu_base = reinterpret_cast<uint32_t*>(g_smem + tab_off) + warp * nwords;
     const uint32_t iter = *A.iter_dev;
+    // grid-barrier generation of the fused update: read before this block can arrive
+    const uint32_t epoch0 = (kSmemTable && A.fuse_update) ? ld_acquire_gpu(A.epoch) : 0u;
     if (kSmemTable) {
         __syncthreads();   // the barrier is initialised before anyone waits on it
         mbar_wait(bar, 0);
@@ -682,7 +774,10 @@ __global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(Cons
         wfb += fb;
     }
     pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
-    block_finish(A, wbest, wfb, lane, warp);
+    const bool last = block_finish(A, wbest, wfb, lane, warp);
+    if constexpr (kSmemTable) {
+        if (A.fuse_update) fused_update(A.upd, A.epoch, last, epoch0, lane, warp);
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -174,6 +174,44 @@ __global__ void select_best_kernel(SelectArgs S) {
     if (threadIdx.x < 32) select_best_warp(S, threadIdx.x);
 }
 
+// pheromone update arguments (row a6; pheromone_update_kernel below)
+struct UpdateArgs {
+    float* tau;
+    float* inv_w;
+    const float* heur;
+    int n, ld, alpha;
+    float rho_f;
+    const float* scal;
+    const uint16_t* succ;
+    const uint16_t* pred;
+    const uint16_t* cand_id;
+    float* cand_inv;
+    int cl;
+    int smem_row;      // 1: the new inv_w row is staged in smem for the cand gather (ld floats fit)
+    uint32_t* iter_dev;
+};
+
+// Row a6 on one float4 of row i (columns c0 .. c0+3): evaporation, deposit along the
+// succ/pred edges of T_dep, clamp (R1, R4-R6), then 1/choice_info (R19).  Shared by the
+// update kernel and the update fused into the construction launch (bit-identical).
+__device__ __forceinline__ float4 update_quad(float4& t, float4 h, int c0, int si, int pi, float rho_f, float tmin,
+                                              float tmax, float delta, int alpha) {
+    float tv[4] = {t.x, t.y, t.z, t.w};
+    const float hv[4] = {h.x, h.y, h.z, h.w};
+    float wv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = c0 + j;
+        float v = fmaxf(__fmul_rn(rho_f, tv[j]), tmin);
+        if (c == si || c == pi) v = __fadd_rn(v, delta);
+        v = fminf(v, tmax);
+        tv[j] = v;
+        wv[j] = inv_weight(v, hv[j], alpha);
+    }
+    t = make_float4(tv[0], tv[1], tv[2], tv[3]);
+    return make_float4(wv[0], wv[1], wv[2], wv[3]);
+}
+
 struct ConstructArgs {
     const double2* __restrict__ xy;
     const float* __restrict__ inv_w;        // n x ld
@@ -199,6 +237,11 @@ struct ConstructArgs {
     const float* __restrict__ tau;   // n x ld
     const float* __restrict__ heur;  // n x ld
     int alpha;
+    // world == 1, persistent shared-memory-table grid: the pheromone update (row a6) runs in
+    // the same launch after a grid barrier (construct.cuh fused_update)
+    int fuse_update;
+    unsigned int* epoch;   // grid-barrier generation word (bumped once per fused launch)
+    UpdateArgs upd;
 };
 
 }  // namespace mmas
@@ -300,21 +343,6 @@ __global__ void wait_peers_kernel(unsigned char* own, ExchangeArgs X, uint32_t* 
 // streaming; the deposit is the row's succ/pred test, so evaporation and
 // deposit fuse into one non-conflicting pass.
 // ---------------------------------------------------------------------------
-struct UpdateArgs {
-    float* tau;
-    float* inv_w;
-    const float* heur;
-    int n, ld, alpha;
-    float rho_f;
-    const float* scal;
-    const uint16_t* succ;
-    const uint16_t* pred;
-    const uint16_t* cand_id;
-    float* cand_inv;
-    int cl;
-    int smem_row;      // 1: the new inv_w row is staged in smem for the cand gather (ld floats fit)
-    uint32_t* iter_dev;
-};
 
 __global__ void __launch_bounds__(256) pheromone_update_kernel(UpdateArgs U) {
     extern __shared__ __align__(16) float s_row[];   // new inv_w row (cl > 0: for the gather)
@@ -364,20 +392,8 @@ __global__ void __launch_bounds__(256) pheromone_update_kernel(UpdateArgs U) {
             for (int u = 0; u < 4; ++u) {
                 const int q = q0 + u * blockDim.x;
                 if (q >= n4) break;
-                float tv[4] = {t[u].x, t[u].y, t[u].z, t[u].w};
-                const float hv[4] = {h[u].x, h[u].y, h[u].z, h[u].w};
-                float wv[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int c = 4 * q + j;
-                    float v = fmaxf(__fmul_rn(U.rho_f, tv[j]), tmin);
-                    if (c == si || c == pi) v = __fadd_rn(v, delta);
-                    v = fminf(v, tmax);
-                    tv[j] = v;
-                    wv[j] = inv_weight(v, hv[j], U.alpha);
-                }
-                trow[q] = make_float4(tv[0], tv[1], tv[2], tv[3]);
-                const float4 w4 = make_float4(wv[0], wv[1], wv[2], wv[3]);
+                const float4 w4 = update_quad(t[u], h[u], 4 * q, si, pi, U.rho_f, tmin, tmax, delta, U.alpha);
+                trow[q] = t[u];
                 wrow[q] = w4;
                 if (U.cl > 0 && U.smem_row) reinterpret_cast<float4*>(s_row)[q] = w4;
             }

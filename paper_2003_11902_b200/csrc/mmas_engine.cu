@@ -114,6 +114,7 @@ struct mmas_ctx {
 
     // launch plan for construction
     bool smem_table = false;
+    bool fuse_update = false;               // world == 1: update fused into the construction launch
 
     bool reg_tabu = false;   // n <= 1024: tabu words in registers
     bool compact_tabu = false;  // cl == 0 with MMAS_TABU_COMPACT: construct_ct_kernel (R27)
@@ -219,6 +220,8 @@ SelectArgs select_args(mmas_ctx* h, const unsigned char* records, int count) {
     return S;
 }
 
+UpdateArgs update_args(mmas_ctx* h);
+
 ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = false) {
     ConstructArgs A{};
     A.fuse_select = fuse_select ? 1 : 0;
@@ -248,6 +251,8 @@ ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = f
     A.tau = h->tau;
     A.heur = h->heur;
     A.alpha = h->alpha;
+    A.epoch = h->done + 1;
+    A.upd = update_args(h);
     return A;
 }
 
@@ -369,6 +374,7 @@ int launch_construct(mmas_ctx* h, bool fuse_select) {
     }
     PhaseScope ps(h, 0);
     ConstructArgs A = construct_args(h, fuse_select);
+    A.fuse_update = fuse_select && h->fuse_update ? 1 : 0;
     if (h->cl == 0 || h->rwm) {
         launch_full(h, A);
     } else if (h->reg_tabu) {
@@ -421,8 +427,7 @@ int launch_two_opt(mmas_ctx* h, bool fuse_select) {
     return MMAS_OK;
 }
 
-int launch_update(mmas_ctx* h) {
-    PhaseScope ps(h, 2);
+UpdateArgs update_args(mmas_ctx* h) {
     UpdateArgs U{};
     U.tau = h->tau;
     U.inv_w = h->inv_w;
@@ -438,8 +443,14 @@ int launch_update(mmas_ctx* h) {
     U.cand_inv = h->cand_inv;
     U.cl = h->cl_ld;
     U.iter_dev = h->iter_dev;
-    const int threads = 256;
     U.smem_row = h->cl > 0 && sizeof(float) * (size_t)h->ld <= (size_t)h->smem_optin - 1024;
+    return U;
+}
+
+int launch_update(mmas_ctx* h) {
+    PhaseScope ps(h, 2);
+    UpdateArgs U = update_args(h);
+    const int threads = 256;
     const size_t smem = U.smem_row ? sizeof(float) * (size_t)h->ld : 0;
     launch_pdl(pheromone_update_kernel, dim3(h->n), dim3(threads), smem, h->stream, U);
     h->launches++;
@@ -510,7 +521,7 @@ int setup(mmas_ctx* h) {
         (st = dalloc(&h->succ, n)) || (st = dalloc(&h->pred, n)) || (st = dalloc(&h->gb_len, 1)) ||
         (st = dalloc(&h->ib_len, 1)) || (st = dalloc(&h->ib_ant, 1)) || (st = dalloc(&h->scal, 4)) ||
         (st = dalloc(&h->iter_dev, 1)) || (st = dalloc(&h->local_record, (size_t)h->rec_bytes)) ||
-        (st = dalloc(&h->done, 1)))
+        (st = dalloc(&h->done, 2)))
         return st;
 
     CU(cudaMemcpyAsync(h->xy, c.coords, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, h->stream));
@@ -521,7 +532,7 @@ int setup(mmas_ctx* h) {
     CU(cudaMemsetAsync(h->gb_len, 0xFF, sizeof(long long), h->stream));   // -1: empty
     CU(cudaMemsetAsync(h->ib_len, 0xFF, sizeof(long long), h->stream));
     CU(cudaMemsetAsync(h->iter_dev, 0, sizeof(uint32_t), h->stream));
-    CU(cudaMemsetAsync(h->done, 0, sizeof(unsigned int), h->stream));
+    CU(cudaMemsetAsync(h->done, 0, 2 * sizeof(unsigned int), h->stream));
     CU(cudaMemsetAsync(h->succ, 0, sizeof(uint16_t) * n, h->stream));
     CU(cudaMemsetAsync(h->pred, 0, sizeof(uint16_t) * n, h->stream));
 
@@ -640,6 +651,14 @@ int setup(mmas_ctx* h) {
             h->cons_warps = w;
             h->cons_grid = std::max(1, std::min(h->num_sms, (h->m_local + w - 1) / w));
             h->cons_smem = need;
+            // fused update (construct.cuh fused_update): one iteration = one launch.  Needs the
+            // whole grid resident (grid <= SMs, one block each), one candidate slot per lane,
+            // no exchange or local search between construction and update, and room for each
+            // warp's tau + heur rows in the block's shared memory
+            const size_t fused_need = 256 + (size_t)w * 2 * 4 * h->ld;
+            h->fuse_update = c.world == 1 && !c.local_search && h->slots == 1 && !c.separate_update &&
+                             std::max(need, fused_need) <= cons_dyn_max;
+            if (h->fuse_update) h->cons_smem = std::max(need, fused_need);
         } else {
             h->cons_warps = 4;
             h->cons_grid = std::max(1, (h->m_local + 3) / 4);
@@ -956,8 +975,9 @@ int mmas_iterate(mmas_ctx* h, int32_t iters) {
     if (h->cfg.world != 1) return fail(MMAS_ESTATE, "mmas_iterate needs world == 1; use mmas_construct/mmas_update");
     CU(cudaSetDevice(h->device));
     for (int k = 0; k < iters; ++k) {
-        if ((st = launch_construct(h, true))) return st;   // + fused iteration-best selection
-        if ((st = launch_update(h))) return st;
+        // + fused iteration-best selection (and, where eligible, the fused update)
+        if ((st = launch_construct(h, true))) return st;
+        if (!h->fuse_update && (st = launch_update(h))) return st;
         h->iteration++;
         if (h->profiling) h->acc_iters++;
     }
@@ -1084,6 +1104,7 @@ int mmas_get_stats(mmas_ctx* h, mmas_stats* out) {
     out->ants_local = h->m_local;
     out->first_ant = h->ant_lo;
     out->local_search_moves = 0;
+    out->update_fused = h->fuse_update ? 1 : 0;
     if (h->ls_moves) {
         unsigned long long mv = 0;
         CU(cudaMemcpy(&mv, h->ls_moves, sizeof(mv), cudaMemcpyDeviceToHost));

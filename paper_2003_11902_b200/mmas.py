@@ -49,14 +49,15 @@ class Config(ctypes.Structure):
         ("p_best", ctypes.c_double), ("deposit", ctypes.c_int32), ("fallback", ctypes.c_int32),
         ("local_search", ctypes.c_int32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
         ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("use_caller_stream", ctypes.c_int32),
-        ("tabu", ctypes.c_int32), ("selection", ctypes.c_int32),
+        ("tabu", ctypes.c_int32), ("selection", ctypes.c_int32), ("separate_update", ctypes.c_int32),
     ]
 
 
 class Stats(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int64), ("fallback_steps", ctypes.c_int64),
                 ("ant_steps", ctypes.c_int64), ("ants_local", ctypes.c_int32), ("first_ant", ctypes.c_int32),
-                ("local_search_moves", ctypes.c_int64)]
+                ("local_search_moves", ctypes.c_int64), ("update_fused", ctypes.c_int32),
+                ("reserved_", ctypes.c_int32)]
 
 
 class PhaseTimes(ctypes.Structure):
@@ -141,7 +142,8 @@ class Colony:
 
     def __init__(self, coords, n_ants, cand_len, alpha=1.0, beta=2.0, rho=0.5, seed=42, p_best=0.01,
                  deposit_global=False, fallback_argmax=False, local_search=False, device=-1, stream=None,
-                 rank=0, world=1, tabu=TABU_BITMASK, selection=SELECT_WRS):
+                 rank=0, world=1, tabu=TABU_BITMASK, selection=SELECT_WRS,
+                 separate_update=False):
         L = lib()
         c = np.ascontiguousarray(coords, dtype=np.float64).reshape(-1, 2)
         self.n = c.shape[0]
@@ -167,6 +169,7 @@ class Colony:
         cfg.rank, cfg.world = int(rank), int(world)
         cfg.tabu = int(tabu)
         cfg.selection = int(selection)
+        cfg.separate_update = int(bool(separate_update))
         h = ctypes.c_void_p()
         _err(L.mmas_create_ex(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h

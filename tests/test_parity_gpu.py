@@ -244,8 +244,61 @@ def test_profiling_accumulates_phase_times():
     n0 = g.kernel_launches
     g.iterate(5)
     t = g.phase_times()
+    assert g.stats()["update_fused"] == 1   # C1: the update runs inside the construction launch
+    assert t["iterations"] == 5 and t["construct_ms"] > 0 and t["update_ms"] == 0
+    assert g.kernel_launches - n0 == 5      # one launch per iteration: construct + select + update
+    s = mmas.Colony(w.coords(), w.n_ants, w.cand_len, separate_update=True)
+    s.profile(True)
+    n0 = s.kernel_launches
+    s.iterate(5)
+    t = s.phase_times()
+    assert s.stats()["update_fused"] == 0
     assert t["iterations"] == 5 and t["construct_ms"] > 0 and t["update_ms"] > 0
-    assert g.kernel_launches - n0 == 10   # construct (+ fused select) and update per iteration
+    assert s.kernel_launches - n0 == 10     # construct (+ fused select) and update per iteration
+
+
+# ---- the update fused into the construction launch (construct.cuh fused_update) --------
+FUSE_CASES = [
+    # (n, m, cl, iterations, kwargs)
+    (198, 198, 16, 4, {}),                     # C1 shape: one row per warp
+    (600, 20, 16, 3, {}),                      # 20 warps for 600 rows: 30 rows per warp (mbarrier phases)
+    (1002, 1002, 32, 3, {}),                   # the bench workload's launch configuration
+    (1025, 40, 32, 2, {}),                     # n > 1024: shared-memory tabu, ragged float4 tail
+    (130, 2400, 32, 2, {}),                    # 16 ant warps per block, several ants per warp
+    (97, 50, 8, 3, {"deposit_global": True}),
+    (64, 20, 10, 3, {"alpha": 2.0, "beta": 3.0}),
+    (5, 7, 1, 3, {}),                          # n <= 5: tau_min clamped to tau_max
+]
+
+
+@pytest.mark.parametrize("n,m,cl,iters,kw", FUSE_CASES,
+                         ids=[f"n{c[0]}-m{c[1]}-cl{c[2]}-{'-'.join(c[4])}" for c in FUSE_CASES])
+def test_fused_update_equals_separate_kernel(n, m, cl, iters, kw):
+    """One launch per iteration (grid barrier + update from TMA-prefetched rows) gives the
+    separate update kernel's results bit for bit, and both the oracle's."""
+    c = make_coords("uniform", n, 500 + n)
+    f = mmas.Colony(c, m, cl, seed=11, **kw)
+    s = mmas.Colony(c, m, cl, seed=11, separate_update=True, **kw)
+    o = oracle.Colony(c, m, cl, seed=11, **kw)
+    assert f.stats()["update_fused"] == 1 and s.stats()["update_fused"] == 0
+    for it in range(iters):
+        f.iterate(1)
+        s.iterate(1)
+        o.iterate(1)
+        compare_iteration(f, o, it)
+        assert np.array_equal(f.tau(), s.tau()) and np.array_equal(f.inv_w(), s.inv_w())
+        assert np.array_equal(f.tours(), s.tours())
+    assert f.iteration == s.iteration == iters
+
+
+def test_fused_update_not_used_where_ineligible():
+    """Exchange contexts (world > 1), local search, cl > 32 and L2-table colonies keep the
+    separate update kernel."""
+    c = make_coords("uniform", 200, 3)
+    assert mmas.Colony(c, 40, 16, rank=0, world=2).stats()["update_fused"] == 0
+    assert mmas.Colony(c, 10, 16, local_search=True).stats()["update_fused"] == 0
+    assert mmas.Colony(c, 40, 40).stats()["update_fused"] == 0
+    assert mmas.Colony(make_coords("uniform", 1500, 3), 20, 32).stats()["update_fused"] == 0
 
 
 # ---- row a8: 2-opt local search ------------------------------------------------------
