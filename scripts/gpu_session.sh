@@ -52,8 +52,10 @@ if has ncu; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:construct -s 400 -c 1 -o $OUT/prof_construct_C2 \
      python bench.py --steps 420 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_construct.log 2>&1
   digest C2 construct_cl_kernel prof_construct_C2
+  # C2 fuses the update into the construction launch; the stand-alone update kernel is
+  # captured from the A/B path (--separate-update)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:pheromone_update -s 400 -c 1 -o $OUT/prof_update_C2 \
-     python bench.py --steps 420 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_update.log 2>&1
+     python bench.py --steps 420 --warmup 3 --no-cpu-baseline --separate-update > $OUT/ncu_full_update.log 2>&1
   digest C2 pheromone_update_kernel prof_update_C2
   ls -la $OUT
 fi
