@@ -125,11 +125,14 @@ __device__ __forceinline__ void philox_rounds(uint4& c, const RoundKeys& rk) {
 // ---------------------------------------------------------------------------
 // Exact pruning of the key computations.  A city's key
 // magnitude is |det_log2(u)| * inv_w >= (1 - u) * log2(e) * inv_w, because -ln u >= 1 - u
-// and det_log2 is within 1.61 ulp of log2.  lb = (1-u) * (inv_w * kLog2eLow) in fp32, with
-// log2(e) deflated by 2^-20, stays below the fp32 magnitude for every u of the grid and
-// every inv_w (tests/test_oracle_rng.py pins the ratio), so a city with lb > thr, thr the
-// warp's best magnitude so far, can neither win nor tie: its det_log2 is not evaluated.
+// and det_log2 is within 1.61 ulp of log2.  With C = log2(e) deflated by 2^-20 (rounded
+// down), |det_log2(u)| >= (1-u) C (1+2^-24)^2/(1-2^-24) on the whole u-grid
+// (tests/test_oracle_rng.py, exhaustive).  The scans compare a = fl((1-u) inv_w) with the
+// scaled threshold T = fl_up(thr * fl_up(1/C)) >= thr / C: a > T implies
+// (1-u) inv_w C > thr / (1+2^-24), hence fl(|det_log2(u)| inv_w) > thr (1+2^-24) > thr, so
+// the city can neither win nor tie and its det_log2 is not evaluated.  One FMUL per city.
 constexpr float kLog2eLow = 1.4426935911178589f;
+constexpr float kInvLog2eLowUp = 0.6931478977203369f;   // fl_up(1 / kLog2eLow)
 
 // One 128-city chunk of the scan: lane l's cities c0 .. c0+3, nib = their visited
 // bits (bit j set = visited or beyond n).  Keys are evaluated (in increasing city order)
@@ -158,31 +161,36 @@ __device__ __forceinline__ void scan_chunk(float4 iv, int c0, uint32_t nib, uint
             if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
         }
     } else {
+        // pruned (thr = the scaled threshold T above): one predicate for "any survivor",
+        // the keys of the survivors in a rare branch
         const uint4 x = philox4x32_10(ctr_city((uint32_t)c0 >> 2, step, ant, iter), key);
         const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-        float us[4];
-        uint32_t todo = 0;
+        float om[4];
+        bool keep[4];
+        bool any = false;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            us[j] = uniform_open(xs[j]);
-            const float lb = __fmul_rn(__fsub_rn(1.0f, us[j]), __fmul_rn(ivs[j], kLog2eLow));
-            todo |= (((nib >> j) & 1u) == 0u && !(lb > thr)) ? (1u << j) : 0u;
+            om[j] = one_minus_uniform_open(xs[j]);      // 1 - u, exact on the grid
+            keep[j] = ((nib >> j) & 1u) == 0u && !(__fmul_rn(om[j], ivs[j]) > thr);
+            any |= keep[j];
         }
-        while (todo) {
-            const int j = __ffs(todo) - 1;
-            todo &= todo - 1u;
-            const float u = j == 0 ? us[0] : j == 1 ? us[1] : j == 2 ? us[2] : us[3];
-            const float v = j == 0 ? ivs[0] : j == 1 ? ivs[1] : j == 2 ? ivs[2] : ivs[3];
-            const uint32_t mag = key_magnitude(__fmul_rn(det_log2(u), v));
-            if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
+        if (any) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (keep[j]) {
+                    const uint32_t mag = key_magnitude(__fmul_rn(det_log2(__fsub_rn(1.0f, om[j])), ivs[j]));
+                    if (mag < best_mag) { best_mag = mag; best_c = (uint32_t)(c0 + j); }
+                }
+            }
         }
     }
 }
 
-// the warp's best magnitude so far as a float threshold (+inf while nothing is found)
+// the warp's best magnitude so far as the scaled pruning threshold T = fl_up(thr / C)
+// (+inf while nothing is found)
 __device__ __forceinline__ float warp_threshold(uint32_t best_mag) {
     const uint32_t b = __reduce_min_sync(kFull, best_mag);
-    return b == kNone ? __int_as_float(0x7F800000) : __uint_as_float(b);
+    return b == kNone ? __int_as_float(0x7F800000) : __fmul_ru(__uint_as_float(b), kInvLog2eLowUp);
 }
 
 // Visited bits of lane l's four cities c0 .. c0+3 (cities >= n count as visited).
@@ -848,38 +856,49 @@ __device__ __forceinline__ void ct_group(uint2 e, float4 iv, int p0, uint32_t st
     const uint4 x = philox4x32_10(ctr_city((uint32_t)p0 >> 2, step, ant, iter), key);
     const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
     const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
-    float us[4];
-    uint32_t todo = 0;
+    const uint32_t vs[4] = {e.x & 0xFFFFu, e.x >> 16, e.y & 0xFFFFu, e.y >> 16};
+    float om[4];
+    bool keep[4];
+    bool any = false;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        us[j] = uniform_open(xs[j]);
-        const float lb = __fmul_rn(__fsub_rn(1.0f, us[j]), __fmul_rn(ivs[j], kLog2eLow));
-        todo |= !(lb > thr) ? (1u << j) : 0u;
+        om[j] = one_minus_uniform_open(xs[j]);          // 1 - u, exact on the grid
+        keep[j] = !(__fmul_rn(om[j], ivs[j]) > thr);           // thr: scaled threshold T
+        any |= keep[j];
     }
-    while (todo) {
-        const int j = __ffs(todo) - 1;
-        todo &= todo - 1u;
-        const float u = j == 0 ? us[0] : j == 1 ? us[1] : j == 2 ? us[2] : us[3];
-        const float v = j == 0 ? ivs[0] : j == 1 ? ivs[1] : j == 2 ? ivs[2] : ivs[3];
-        const uint32_t vj = j == 0 ? (e.x & 0xFFFFu) : j == 1 ? (e.x >> 16) : j == 2 ? (e.y & 0xFFFFu) : (e.y >> 16);
-        const uint32_t mag = key_magnitude(__fmul_rn(det_log2(u), v));
-        // (mag, node) lexicographic minimum
-        if ((mag < best_mag) | ((mag == best_mag) & (vj < best_c))) {
-            best_mag = mag;
-            best_c = vj;
+    if (any) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (keep[j]) {
+                const uint32_t mag = key_magnitude(__fmul_rn(det_log2(__fsub_rn(1.0f, om[j])), ivs[j]));
+                // (mag, node) lexicographic minimum
+                if ((mag < best_mag) | ((mag == best_mag) & (vs[j] < best_c))) {
+                    best_mag = mag;
+                    best_c = vs[j];
+                }
+            }
         }
     }
 }
 
 // positions p0 .. p0+3 of the list: their nodes (u16 pairs) and inv_w[cur][node]
+// (kChecked: the trip may run past L; positions >= L get +inf)
+template <bool kChecked>
 __device__ __forceinline__ void ct_load(const uint16_t* ent, const float* __restrict__ row, int p0, int L, uint2& e,
                                         float4& iv) {
     const float inf = __int_as_float(0x7F800000);
     e = *reinterpret_cast<const uint2*>(ent + p0);
-    iv.x = p0 + 0 < L ? __ldg(row + (e.x & 0xFFFFu)) : inf;
-    iv.y = p0 + 1 < L ? __ldg(row + (e.x >> 16)) : inf;
-    iv.z = p0 + 2 < L ? __ldg(row + (e.y & 0xFFFFu)) : inf;
-    iv.w = p0 + 3 < L ? __ldg(row + (e.y >> 16)) : inf;
+    if (kChecked) {
+        iv.x = p0 + 0 < L ? __ldg(row + (e.x & 0xFFFFu)) : inf;
+        iv.y = p0 + 1 < L ? __ldg(row + (e.x >> 16)) : inf;
+        iv.z = p0 + 2 < L ? __ldg(row + (e.y & 0xFFFFu)) : inf;
+        iv.w = p0 + 3 < L ? __ldg(row + (e.y >> 16)) : inf;
+    } else {
+        iv.x = __ldg(row + (e.x & 0xFFFFu));
+        iv.y = __ldg(row + (e.x >> 16));
+        iv.z = __ldg(row + (e.y & 0xFFFFu));
+        iv.w = __ldg(row + (e.y >> 16));
+    }
 }
 
 // one 256-position trip: lane l's groups base+4l and base+128+4l
@@ -894,8 +913,13 @@ __device__ __forceinline__ void ct_trip(const uint2 (&e)[2], const float4 (&iv)[
 
 __device__ __forceinline__ void ct_load_trip(const uint16_t* ent, const float* __restrict__ row, int base, int lane,
                                              int L, uint2 (&e)[2], float4 (&iv)[2]) {
-    ct_load(ent, row, base + 4 * lane, L, e[0], iv[0]);
-    ct_load(ent, row, base + 128 + 4 * lane, L, e[1], iv[1]);
+    if (base + 256 <= L) {   // a full trip (warp-uniform): no per-position bounds
+        ct_load<false>(ent, row, base + 4 * lane, L, e[0], iv[0]);
+        ct_load<false>(ent, row, base + 128 + 4 * lane, L, e[1], iv[1]);
+    } else {
+        ct_load<true>(ent, row, base + 4 * lane, L, e[0], iv[0]);
+        ct_load<true>(ent, row, base + 128 + 4 * lane, L, e[1], iv[1]);
+    }
 }
 
 // CT mark(u), by one lane; L = list length before the mark.

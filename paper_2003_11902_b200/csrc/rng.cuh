@@ -46,6 +46,13 @@ __device__ __forceinline__ float uniform_open(uint32_t x) {
     return __fsub_rn(__uint_as_float(0x3F800000u | (x >> 9)), 0.99999994039535522461f);
 }
 
+// 1 - u for the same x, exactly (1 - u = (2^24 - 2j - 1) 2^-24 has 24 significant bits):
+// 1 + (2^23 - 1 - j) 2^-23 = 2 - (j+1) 2^-23 from the bits 0x3FFFFFFF - j, minus (1 - 2^-24).
+// (The pruned scans need 1 - u for every city and u itself only for the few survivors.)
+__device__ __forceinline__ float one_minus_uniform_open(uint32_t x) {
+    return __fsub_rn(__uint_as_float(0x3FFFFFFFu - (x >> 9)), 0.99999994039535522461f);
+}
+
 // det_log2 (R14): u = 2^e * m, m in [sqrt(1/2), sqrt(2)), f = m - 1 (exact),
 // log2 u = e + f * P(f), P of degree 8 (coefficients frozen in DESIGN.md).
 // Valid for normal u > 0, which covers every value uniform_open() produces.

@@ -84,6 +84,35 @@ def test_start_node_uniform():
     assert chisquare(counts).pvalue > 1e-3
 
 
+def _f32_round_up(x):
+    """float64 array -> the smallest float32 >= x (x finite, positive)."""
+    f = x.astype(np.float32)
+    low = f.astype(np.float64) < x
+    f[low] = np.nextafter(f[low], np.float32(np.inf))
+    return f
+
+
+def test_scaled_pruning_threshold_never_prunes_a_tie_or_winner():
+    """The GPU scans compare a = fl(fl(1-u) inv) with T = fl_up(thr * K), K = fl_up(1/C)
+    (construct.cuh warp_threshold), pruning when a > T.  Safe iff a city whose magnitude
+    mag = fl(|det_log2(u)| inv) is <= thr is never pruned; T is monotone in thr, so the
+    worst case is thr = mag: a <= fl_up(mag * K) must hold for every u of the grid (all
+    2^23, exhaustive) and every inv (a spread of 64 magnitudes per u block)."""
+    C = np.float32(1.4426935911178589)
+    K = np.float32(0.6931478977203369)
+    assert float(K) >= 1.0 / float(C)
+    j = np.arange(1 << 23, dtype=np.float64)
+    u = ((2.0 * j + 1.0) / 2.0 ** 24).astype(np.float32)
+    om = np.float32(1.0) - u
+    D = np.abs(oracle.det_log2_many(u))
+    rng = np.random.default_rng(1)
+    for inv in (10.0 ** rng.uniform(-3, 12, size=64)).astype(np.float32):
+        mag = (D * inv).astype(np.float32)                      # fl(|det_log2(u)| inv)
+        a = (om * inv).astype(np.float32)                       # fl(fl(1-u) inv)
+        T = _f32_round_up(mag.astype(np.float64) * float(K))    # fl_up(mag K)
+        assert np.all(a <= T), float(inv)
+
+
 def test_pruning_lower_bound_holds_on_the_whole_grid():
     """The exact key pruning of the GPU scans skips det_log2
     when lb = fl(fl(1-u) * fl(inv * C)) > thr, C = log2(e)(1 - 2^-20) rounded down.  That is
