@@ -137,7 +137,11 @@ constexpr float kInvLog2eLowUp = 0.6931478977203369f;   // fl_up(1 / kLog2eLow)
 // One 128-city chunk of the scan: lane l's cities c0 .. c0+3, nib = their visited
 // bits (bit j set = visited or beyond n).  Keys are evaluated (in increasing city order)
 // only for the unvisited cities whose lower bound does not exceed thr.
-template <bool kArgmax, bool kPrune>
+// kPrune: per-lane survivor branch (full-row scans: 16+ warps per SM hide its latency);
+// kWarpPrune (with kPrune): the warp skips a group's logs only when no lane has a survivor,
+// and otherwise evaluates all four logs branch-free (ILP 4: the fallback scans of C3 / C5
+// run at a few warps per SM, where a serial per-city branch costs more than it saves)
+template <bool kArgmax, bool kPrune, bool kWarpPrune = false>
 __device__ __forceinline__ void scan_chunk(float4 iv, int c0, uint32_t nib, uint32_t step, uint32_t ant,
                                            uint32_t iter, PhiloxKey key, uint32_t& best_mag, uint32_t& best_c,
                                            float thr) {
@@ -174,7 +178,17 @@ __device__ __forceinline__ void scan_chunk(float4 iv, int c0, uint32_t nib, uint
             keep[j] = ((nib >> j) & 1u) == 0u && !(__fmul_rn(om[j], ivs[j]) > thr);
             any |= keep[j];
         }
-        if (any) {
+        if (kWarpPrune) {
+            if (__any_sync(kFull, any)) {
+                uint32_t mag[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    mag[j] = keep[j] ? key_magnitude(__fmul_rn(det_log2(__fsub_rn(1.0f, om[j])), ivs[j])) : kNone;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (mag[j] < best_mag) { best_mag = mag[j]; best_c = (uint32_t)(c0 + j); }
+            }
+        } else if (any) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (keep[j]) {
@@ -215,12 +229,19 @@ __device__ __forceinline__ uint32_t chunk_nibble(const Tabu& tabu, int c0, int n
 // ---------------------------------------------------------------------------
 // kPrefetch (the full-row path, where the scan is the whole step and 16+ warps per SM hide the
 // serial pruned key chains): next trip loaded one trip ahead + exact pruning of the keys.
-template <bool kArgmax, bool kPrefetch = false, class Tabu>
+// kLagPrune (candidate-list fallback of the L2-table kernel at high occupancy, C3): pruned
+// keys with the threshold of the trip before last -- still exact (an older threshold is
+// larger, so it prunes less), but the warp reduction after trip i is only needed at trip
+// i + 2, so the trips do not serialise on it.  At a few warps per SM (C5) the branch-free
+// scan is faster (its eight independent log chains per trip are the ILP those warps lack).
+template <bool kArgmax, bool kPrefetch = false, bool kLagPrune = false, class Tabu>
 __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, const Tabu& tabu, int n,
                                                uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
                                                int lane, uint32_t& best_mag, uint32_t& best_c) {
     // pruning threshold (full-row path only: kPrefetch; unused by the argmax flag)
-    float thr = kPrefetch && !kArgmax ? warp_threshold(best_mag) : 0.f;
+    constexpr bool kLag = kLagPrune && !kArgmax && !kPrefetch;
+    float thr = (kPrefetch || kLag) && !kArgmax ? warp_threshold(best_mag) : 0.f;
+    float thr_next = thr;
     auto load_trip = [&](int base, uint32_t& na, uint32_t& nb, float4& iva, float4& ivb) {
         const int ca = base + 4 * lane, cb = ca + 128;
         na = chunk_nibble(tabu, ca, n);
@@ -256,8 +277,12 @@ __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, co
             load_trip(base, na, nb, iva, ivb);
             if (!__any_sync(kFull, (na & nb) != 0xFu)) continue;
             const int ca = base + 4 * lane;
-            scan_chunk<kArgmax, false>(iva, ca, na, step, ant, iter, key, best_mag, best_c, thr);
-            scan_chunk<kArgmax, false>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c, thr);
+            scan_chunk<kArgmax, kLag, true>(iva, ca, na, step, ant, iter, key, best_mag, best_c, thr);
+            scan_chunk<kArgmax, kLag, true>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c, thr);
+            if (kLag) {
+                thr = thr_next;
+                thr_next = warp_threshold(best_mag);
+            }
         }
     }
 }
@@ -695,6 +720,9 @@ __global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(Cons
                 uint32_t fm = kNone, fc = kNone;
                 if (A.fallback_argmax)
                     scan_unvisited<true>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm, fc);
+                else if (!kSmemTable && A.prune_fallback)
+                    scan_unvisited<false, false, !kSmemTable>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm,
+                                                              fc);
                 else
                     scan_unvisited<false>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm, fc);
                 nxt = warp_select(fm, fc);

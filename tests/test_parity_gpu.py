@@ -129,6 +129,16 @@ def test_clustered_instance_with_fallbacks():
     assert g.stats()["fallback_steps"] > 0
 
 
+def test_pruned_fallback_scan_bit_exact():
+    """The L2-table kernel at >= 16 ant warps per SM takes the pruned (lagged-threshold)
+    fallback scan (construct.cuh scan_unvisited kLagPrune): table too large for shared
+    memory (n = 1300, cl padded to 32 slots), 2400 ants, cl = 4 on a clustered instance so
+    most steps fall back."""
+    c = make_coords("fl3795", 1300, 21)
+    g, o = lockstep(c, 2400, 4, 1, seed=13)
+    assert g.stats()["fallback_steps"] > 100000
+
+
 def test_fallback_counter_matches_oracle():
     c = make_coords("d198", 198, 198)
     g = mmas.Colony(c, 120, 4, seed=3)
