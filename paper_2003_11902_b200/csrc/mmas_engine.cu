@@ -131,6 +131,9 @@ struct mmas_ctx {
     // row a8: 2-opt local search (local_search != 0)
     int ls_k = 0, ls_nwords = 0, ls_coop_smem_max = 0;
     uint16_t* ls_nn = nullptr;         // n x ls_k neighbour lists
+    int32_t* ls_nnd = nullptr;         // n x ls_k: d(a, nn[a][k])
+    short2* ls_xys = nullptr;          // integral coordinates (ls_int_xy), else null
+    bool ls_int_xy = false;
     uint16_t *ls_pos = nullptr, *ls_queue = nullptr;
     uint32_t* ls_inq = nullptr;
     unsigned long long* ls_moves = nullptr;
@@ -403,6 +406,8 @@ int launch_two_opt(mmas_ctx* h, bool fuse_select) {
     TwoOptArgs T{};
     T.xy = h->xy;
     T.nn = h->ls_nn;
+    T.nnd = h->ls_nnd;
+    T.xys = h->ls_xys;
     T.n = h->n;
     T.K = h->ls_k;
     T.ldr = h->ldr;
@@ -418,12 +423,19 @@ int launch_two_opt(mmas_ctx* h, bool fuse_select) {
     if (per_ant <= (size_t)h->ls_coop_smem_max) {
         // one block of kLsWarps warps per ant (speculative parallel FIFO, two_opt_coop_kernel)
         T.warps_per_block = kLsWarps;
-        launch_pdl(two_opt_coop_kernel, dim3(std::max(1, h->m_local)), dim3(kLsWarps * 32), per_ant, h->stream, T,
-                   construct_args(h, fuse_select));
+        if (h->ls_int_xy)
+            launch_pdl(two_opt_coop_kernel<true>, dim3(std::max(1, h->m_local)), dim3(kLsWarps * 32), per_ant,
+                       h->stream, T, construct_args(h, fuse_select));
+        else
+            launch_pdl(two_opt_coop_kernel<false>, dim3(std::max(1, h->m_local)), dim3(kLsWarps * 32), per_ant,
+                       h->stream, T, construct_args(h, fuse_select));
     } else {
         T.warps_per_block = 4;
         const int grid = std::max(1, (h->m_local + 3) / 4);
-        launch_pdl(two_opt_kernel, dim3(grid), dim3(128), 0, h->stream, T, construct_args(h, fuse_select));
+        if (h->ls_int_xy)
+            launch_pdl(two_opt_kernel<true>, dim3(grid), dim3(128), 0, h->stream, T, construct_args(h, fuse_select));
+        else
+            launch_pdl(two_opt_kernel<false>, dim3(grid), dim3(128), 0, h->stream, T, construct_args(h, fuse_select));
     }
     h->launches++;
     CU(cudaGetLastError());
@@ -468,7 +480,7 @@ void free_ctx(mmas_ctx* h) {
     void* ptrs[] = {h->xy, h->heur, h->tau, h->inv_w, h->cand_inv, h->cand_id, h->routes, h->lengths,
                     h->best_key, h->fallback_count, h->ib_route, h->gb_route, h->succ, h->pred, h->gb_len,
                     h->ib_len, h->ib_ant, h->scal, h->iter_dev, h->local_record, h->done,
-                    h->ls_nn, h->ls_pos, h->ls_queue, h->ls_inq, h->ls_moves};
+                    h->ls_nn, h->ls_nnd, h->ls_xys, h->ls_pos, h->ls_queue, h->ls_inq, h->ls_moves};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : h->xopened) cudaIpcCloseMemHandle(p);
@@ -580,10 +592,31 @@ int setup(mmas_ctx* h) {
         std::vector<uint16_t> nnl;
         candidate_lists(c.coords, n, h->ls_k, nnl);
         const size_t ma = (size_t)std::max(h->m_local, 1);
-        if ((st = dalloc(&h->ls_nn, nnl.size())) || (st = dalloc(&h->ls_pos, ma * h->ldr)) ||
+        // neighbour distances (exact R12 values; the 2-opt evaluation reads d(a, c) from here)
+        std::vector<int32_t> nnd(nnl.size());
+        for (int i = 0; i < n; ++i)
+            for (int k = 0; k < h->ls_k; ++k) nnd[(size_t)i * h->ls_k + k] = host_dist(c.coords, i, nnl[(size_t)i * h->ls_k + k]);
+        // integral coordinates with |x|, |y| <= 16383: the 2-opt kernels compute distances in
+        // 32-bit integer arithmetic (two_opt.cuh euc2d_int; identical results)
+        h->ls_int_xy = true;
+        std::vector<short2> xys((size_t)n);
+        for (int i = 0; i < n && h->ls_int_xy; ++i) {
+            const double x = c.coords[2 * i], y = c.coords[2 * i + 1];
+            if (x != std::floor(x) || y != std::floor(y) || std::fabs(x) > 16383.0 || std::fabs(y) > 16383.0)
+                h->ls_int_xy = false;
+            else
+                xys[(size_t)i] = make_short2((short)x, (short)y);
+        }
+        if ((st = dalloc(&h->ls_nn, nnl.size())) || (st = dalloc(&h->ls_nnd, nnd.size())) ||
+            (st = dalloc(&h->ls_pos, ma * h->ldr)) ||
             (st = dalloc(&h->ls_queue, ma * h->ldr)) || (st = dalloc(&h->ls_inq, ma * h->ls_nwords)) ||
             (st = dalloc(&h->ls_moves, 1)))
             return st;
+        if (h->ls_int_xy) {
+            if ((st = dalloc(&h->ls_xys, (size_t)n))) return st;
+            CU(cudaMemcpyAsync(h->ls_xys, xys.data(), sizeof(short2) * n, cudaMemcpyHostToDevice, h->stream));
+        }
+        CU(cudaMemcpyAsync(h->ls_nnd, nnd.data(), sizeof(int32_t) * nnd.size(), cudaMemcpyHostToDevice, h->stream));
         CU(cudaMemcpyAsync(h->ls_nn, nnl.data(), sizeof(uint16_t) * nnl.size(), cudaMemcpyHostToDevice, h->stream));
         CU(cudaMemsetAsync(h->ls_moves, 0, sizeof(unsigned long long), h->stream));
         CU(cudaStreamSynchronize(h->stream));
@@ -695,10 +728,15 @@ int setup(mmas_ctx* h) {
         allow_max_smem(construct_ct_kernel, h->smem_optin);
     }
     {
-        cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, two_opt_coop_kernel);
-        h->ls_coop_smem_max = h->smem_optin - (int)fa.sharedSizeBytes;   // dynamic = opt-in limit - static
-        cudaFuncSetAttribute(two_opt_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->ls_coop_smem_max);
+        cudaFuncAttributes fa{}, fb{};
+        cudaFuncGetAttributes(&fa, two_opt_coop_kernel<true>);
+        cudaFuncGetAttributes(&fb, two_opt_coop_kernel<false>);
+        // dynamic = opt-in limit - static (both instantiations)
+        h->ls_coop_smem_max = h->smem_optin - (int)std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
+        cudaFuncSetAttribute(two_opt_coop_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             h->ls_coop_smem_max);
+        cudaFuncSetAttribute(two_opt_coop_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             h->ls_coop_smem_max);
     }
     allow_max_smem(pheromone_update_kernel, h->smem_optin);
     CU(cudaGetLastError());

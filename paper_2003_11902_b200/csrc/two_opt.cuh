@@ -16,6 +16,8 @@ namespace mmas {
 
 struct TwoOptArgs {
     const double2* __restrict__ xy;
+    const short2* __restrict__ xys;    // integral coordinates, |x|, |y| <= 16383 (kIntXY kernels), else null
+    const int32_t* __restrict__ nnd;   // n x K: d(a, nn[a][k]) (setup, exact R12 distances)
     const uint16_t* __restrict__ nn;   // n x K neighbour lists (R10 order)
     int n, K, ldr, m_local, warps_per_block, nwords;
     uint16_t* routes;                  // m_local x ldr (in: constructed routes; out: improved)
@@ -23,6 +25,47 @@ struct TwoOptArgs {
     uint16_t* queue;                   // m_local x ldr scratch
     uint32_t* inq;                     // m_local x nwords scratch ("don't-look bit" clear <=> queued)
     unsigned long long* moves;         // total applied moves (stats)
+};
+
+// ---- coordinates and EUC_2D distances of the local search --------------------------
+// kIntXY: every coordinate is an integer with |x|, |y| <= 16383 (checked at setup), so
+// S = dx^2 + dy^2 < 2^31 is exact in 32 bits and nint(sqrt(S)) -- the R12 distance, which
+// the double formula computes exactly for such S (sqrt(S) is never within 2^-30 of a
+// half-integer) -- comes from an approximate sqrt rounded to the nearest integer k0
+// (|error| << 1/2 except next to a half-integer) and one integer correction:
+// (2k-1)^2 <= 4S < (2k+1)^2  <=>  k^2 - k < S <= k^2 + k   (4S is even, (2k+-1)^2 odd).
+// No fp64 (DSQRT is a ~20-instruction subroutine with a long DFMA chain).  Pinned against
+// the double formula in tests/test_capi.py (exhaustive S <= 2^22, random S < 2^31, and the
+// near-half-integer cases k^2 + k, k^2 + k + 1).
+__device__ __forceinline__ int32_t euc2d_int(short2 p, short2 q) {
+    const int dx = (int)p.x - (int)q.x, dy = (int)p.y - (int)q.y;
+    const uint32_t S = (uint32_t)(dx * dx) + (uint32_t)(dy * dy);
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(__uint2float_rn(S)));
+    uint32_t k = (uint32_t)__float2int_rn(r);
+    const uint32_t kk = k * k;
+    if (kk + k < S) ++k;
+    else if (k > 0u && kk - k >= S) --k;
+    return (int32_t)k;
+}
+
+template <bool kInt>
+struct Pts;
+template <>
+struct Pts<false> {
+    using P = double2;
+    const double2* __restrict__ p;
+    __device__ __forceinline__ explicit Pts(const TwoOptArgs& T) : p(T.xy) {}
+    __device__ __forceinline__ P at(int i) const { return __ldg(p + i); }
+    __device__ __forceinline__ static int64_t dist(P a, P b) { return euc2d(a, b); }
+};
+template <>
+struct Pts<true> {
+    using P = short2;
+    const short2* __restrict__ p;
+    __device__ __forceinline__ explicit Pts(const TwoOptArgs& T) : p(T.xys) {}
+    __device__ __forceinline__ P at(int i) const { return __ldg(p + i); }
+    __device__ __forceinline__ static int64_t dist(P a, P b) { return euc2d_int(a, b); }
 };
 
 __device__ __forceinline__ int wrap_inc(int i, int n) { return i + 1 == n ? 0 : i + 1; }
@@ -55,9 +98,12 @@ __device__ __forceinline__ void warp_reverse(uint16_t* route, uint16_t* pos, int
 }
 
 // Local search of one route (the whole warp).  Returns the number of applied moves.
+template <bool kInt>
 __device__ __forceinline__ long long two_opt_route(const TwoOptArgs& T, uint16_t* route, uint16_t* pos,
                                                    uint16_t* queue, uint32_t* inq, int lane) {
     const int n = T.n, K = T.K;
+    const Pts<kInt> X(T);
+    using P = typename Pts<kInt>::P;
     for (int i = lane; i < n; i += 32) pos[route[i]] = (uint16_t)i;
     long long moves = 0, sweep_moves;
     do {
@@ -71,7 +117,8 @@ __device__ __forceinline__ long long two_opt_route(const TwoOptArgs& T, uint16_t
         // coordinates) is loaded one pop AHEAD, behind the current pop's work
         int a = queue[0];
         int c = lane < K ? T.nn[(size_t)a * K + lane] : a;
-        double2 xa = __ldg(T.xy + a), xc = __ldg(T.xy + c);
+        int64_t dac = lane < K ? __ldg(T.nnd + (size_t)a * K + lane) : 0;
+        P xa = X.at(a), xc = X.at(c);
         while (count > 0) {
             head = wrap_inc(head, n);
             --count;
@@ -82,22 +129,28 @@ __device__ __forceinline__ long long two_opt_route(const TwoOptArgs& T, uint16_t
             const int sa = route[wrap_inc(pa, n)];      // successor of a
             const int pr = route[wrap_dec(pa, n)];      // predecessor of a
             const int c2 = lane < K ? T.nn[(size_t)a2 * K + lane] : a2;
-            const double2 xa2 = __ldg(T.xy + a2);
-            const int64_t d_as = euc2d(xa, __ldg(T.xy + sa));
-            const int64_t d_ap = euc2d(xa, __ldg(T.xy + pr));
+            const int64_t dac2 = lane < K ? __ldg(T.nnd + (size_t)a2 * K + lane) : 0;
+            const P xa2 = X.at(a2);
+            const P xs = X.at(sa), xp = X.at(pr);
+            const int64_t d_as = X.dist(xa, xs);
+            const int64_t d_ap = X.dist(xa, xp);
             // lane k: the k-th nearest neighbour c of a, in both directions
             bool imp_s = false, imp_p = false;
             int sc = 0, pc = 0;
-            const double2 xc2 = __ldg(T.xy + c2);
+            const P xc2 = X.at(c2);
             if (lane < K) {
-                const int64_t d_ac = euc2d(xa, xc);
+                const int64_t d_ac = dac;
                 const int qc = pos[c];
                 sc = route[wrap_inc(qc, n)];
                 pc = route[wrap_dec(qc, n)];
-                if (d_ac < d_as && c != sa && sc != a)   // Bentley pruning + degenerate moves
-                    imp_s = d_ac + euc2d(__ldg(T.xy + sa), __ldg(T.xy + sc)) - d_as - euc2d(xc, __ldg(T.xy + sc)) < 0;
-                if (d_ac < d_ap && c != pr && pc != a)
-                    imp_p = d_ac + euc2d(__ldg(T.xy + pr), __ldg(T.xy + pc)) - d_ap - euc2d(xc, __ldg(T.xy + pc)) < 0;
+                if (d_ac < d_as && c != sa && sc != a) {   // Bentley pruning + degenerate moves
+                    const P xsc = X.at(sc);
+                    imp_s = d_ac + X.dist(xs, xsc) - d_as - X.dist(xc, xsc) < 0;
+                }
+                if (d_ac < d_ap && c != pr && pc != a) {
+                    const P xpc = X.at(pc);
+                    imp_p = d_ac + X.dist(xp, xpc) - d_ap - X.dist(xc, xpc) < 0;
+                }
             }
             // the pruning is a prefix of k (lists are sorted by d(a, .)), so "first improving
             // in (direction, k) order" is the lowest improving lane of the successor direction,
@@ -142,13 +195,15 @@ __device__ __forceinline__ long long two_opt_route(const TwoOptArgs& T, uint16_t
             if (ahead) {
                 a = a2;
                 c = c2;
+                dac = dac2;
                 xa = xa2;
                 xc = xc2;
             } else if (count > 0) {   // the queue had run empty: the next pop was just enqueued
                 a = queue[head];
                 c = lane < K ? T.nn[(size_t)a * K + lane] : a;
-                xa = __ldg(T.xy + a);
-                xc = __ldg(T.xy + c);
+                dac = lane < K ? __ldg(T.nnd + (size_t)a * K + lane) : 0;
+                xa = X.at(a);
+                xc = X.at(c);
             }
         }
         moves += sweep_moves;
@@ -163,6 +218,7 @@ namespace mmas {
 // Row a8 over every ant of the shard, then the per-ant length and the block-level
 // iteration-best bookkeeping (row a5) on the IMPROVED routes (R26: the local-search
 // output replaces the ant's tour).
+template <bool kInt>
 __global__ void __launch_bounds__(128) two_opt_kernel(TwoOptArgs T, ConstructArgs A) {
     pdl_wait();
     const int lane = threadIdx.x & 31;
@@ -171,7 +227,7 @@ __global__ void __launch_bounds__(128) two_opt_kernel(TwoOptArgs T, ConstructArg
     long long moves = 0;
     for (int al = blockIdx.x * T.warps_per_block + warp; al < T.m_local; al += gridDim.x * T.warps_per_block) {
         uint16_t* route = T.routes + (size_t)al * T.ldr;
-        moves += two_opt_route(T, route, T.pos + (size_t)al * T.ldr, T.queue + (size_t)al * T.ldr,
+        moves += two_opt_route<kInt>(T, route, T.pos + (size_t)al * T.ldr, T.queue + (size_t)al * T.ldr,
                                T.inq + (size_t)al * T.nwords, lane);
         __syncwarp();
         wbest = min(wbest, finish_ant(A, route, al, (uint32_t)(A.ant_lo + al), lane));
@@ -206,28 +262,39 @@ struct MoveEval {
 };
 
 // Evaluate node a on the current route (one warp).  Lane k: the k-th neighbour.
+// d(a, c) comes from the setup's neighbour-distance table (loaded with the neighbour id).
+template <bool kInt>
 __device__ __forceinline__ MoveEval eval_node(const TwoOptArgs& T, const uint16_t* route, const uint16_t* pos,
                                               int a, int lane) {
     const int n = T.n, K = T.K;
+    const Pts<kInt> X(T);
+    using P = typename Pts<kInt>::P;
+    int c = a, sc = 0, pc = 0;
+    int64_t d_ac = 0;
+    if (lane < K) {
+        c = T.nn[(size_t)a * K + lane];
+        d_ac = __ldg(T.nnd + (size_t)a * K + lane);
+    }
     const int pa = pos[a];
     const int sa = route[wrap_inc(pa, n)];
     const int pr = route[wrap_dec(pa, n)];
-    const double2 xa = __ldg(T.xy + a);
-    int c = a, sc = 0, pc = 0;
-    if (lane < K) c = T.nn[(size_t)a * K + lane];
-    const double2 xc = __ldg(T.xy + c);
-    const int64_t d_as = euc2d(xa, __ldg(T.xy + sa));
-    const int64_t d_ap = euc2d(xa, __ldg(T.xy + pr));
+    const P xs = X.at(sa), xp = X.at(pr), xa = X.at(a);
+    const P xc = X.at(c);
+    const int64_t d_as = X.dist(xa, xs);
+    const int64_t d_ap = X.dist(xa, xp);
     bool imp_s = false, imp_p = false;
     if (lane < K) {
-        const int64_t d_ac = euc2d(xa, xc);
         const int qc = pos[c];
         sc = route[wrap_inc(qc, n)];
         pc = route[wrap_dec(qc, n)];
-        if (d_ac < d_as && c != sa && sc != a)   // Bentley pruning + degenerate moves
-            imp_s = d_ac + euc2d(__ldg(T.xy + sa), __ldg(T.xy + sc)) - d_as - euc2d(xc, __ldg(T.xy + sc)) < 0;
-        if (d_ac < d_ap && c != pr && pc != a)
-            imp_p = d_ac + euc2d(__ldg(T.xy + pr), __ldg(T.xy + pc)) - d_ap - euc2d(xc, __ldg(T.xy + pc)) < 0;
+        if (d_ac < d_as && c != sa && sc != a) {   // Bentley pruning + degenerate moves
+            const P xsc = X.at(sc);
+            imp_s = d_ac + X.dist(xs, xsc) - d_as - X.dist(xc, xsc) < 0;
+        }
+        if (d_ac < d_ap && c != pr && pc != a) {
+            const P xpc = X.at(pc);
+            imp_p = d_ac + X.dist(xp, xpc) - d_ap - X.dist(xc, xpc) < 0;
+        }
     }
     const uint32_t ms = __ballot_sync(kFull, imp_s);
     const uint32_t mp = __ballot_sync(kFull, imp_p);
@@ -243,6 +310,7 @@ __device__ __forceinline__ MoveEval eval_node(const TwoOptArgs& T, const uint16_
     return m;
 }
 
+template <bool kInt>
 __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs T, ConstructArgs A) {
     pdl_wait();
     extern __shared__ __align__(16) uint16_t ls_smem[];
@@ -282,7 +350,7 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
                 if (warp < count) {
                     int q = head + warp;
                     if (q >= n) q -= n;
-                    const MoveEval m = eval_node(T, s_route, s_pos, (int)queue[q], lane);
+                    const MoveEval m = eval_node<kInt>(T, s_route, s_pos, (int)queue[q], lane);
                     if (lane == 0) s_eval[warp] = m;
                 }
                 __syncthreads();

@@ -327,6 +327,16 @@ def test_two_opt_bit_exact(n, m, cl, iters):
     lockstep(make_coords("uniform", n, 3000 + n), m, cl, iters, seed=11 + n, local_search=True, rho=0.7)
 
 
+@pytest.mark.parametrize("shift,scale", [(0.25, 1.0), (0.0, 3.0)], ids=["fractional", "beyond-16383"])
+def test_two_opt_bit_exact_double_distance_path(shift, scale):
+    """Coordinates that are not integers, or exceed |x| <= 16383, take the 2-opt kernels'
+    double EUC_2D path (two_opt.cuh Pts<false>); integral ones the 32-bit path."""
+    c = make_coords("uniform", 150, 77) * scale + shift
+    if scale > 1:
+        c[:, 0] += 20000.0
+    lockstep(c, 30, 16, 2, seed=5, local_search=True, rho=0.7)
+
+
 def test_c5_sampled_ants_with_two_opt():
     """d18512-shaped with cl 32 + 2-opt (C5) at full size: iteration-0 routes of sampled
     ants after local search, computed one by one by the oracle."""
