@@ -256,8 +256,7 @@ def run_ours(args):
         if world == 1:
             col.iterate(1)
         elif exchange == "p2p":
-            col.construct_publish()
-            col.update_exchange()
+            col.iterate_exchange(1)   # one launch per iteration where eligible (include/mmas.h)
         else:
             col.construct(local.data_ptr())
             if backend == "nccl":
@@ -309,7 +308,7 @@ def run_ours(args):
                    "construct_ct_kernel" if w.tabu else "construct_full_kernel")
     # world == 1 with the table in shared memory: the update (row a6) runs inside the same
     # launch (construct.cuh fused_update), so that launch also moves the update's 16 n^2 B
-    fused = bool(col.stats()["update_fused"])
+    fused = bool(col.stats()["update_fused"]) and (world == 1 or exchange == "p2p")
     upd_bytes = 16 * w.n * w.n
     if fused:
         bytes_per_launch += upd_bytes
@@ -384,8 +383,7 @@ def run_ours(args):
         if world == 1:
             c2.iterate(1)
         elif exchange == "p2p":
-            c2.construct_publish()
-            c2.update_exchange()
+            c2.iterate_exchange(1)
         else:
             c2.construct(local.data_ptr())
             if backend == "nccl":

@@ -150,7 +150,13 @@ int mmas_update(mmas_ctx *h, const void *records_dev, int32_t count);
  * Then each iteration is mmas_construct_publish(h) (construction; the shard's best record
  * is written into slot `rank` of every buffer and a flag raised in each) followed by
  * mmas_update_exchange(h) (waits on the device until every rank's flag of this iteration
- * is up, selects, updates); mmas_iterate_exchange(h, iters) does both.  The wait is
+ * is up, selects, updates); mmas_iterate_exchange(h, iters) does both -- as ONE launch
+ * per iteration where the context is eligible (mmas_stats.update_fused: candidate table in
+ * shared memory, cand_len <= 32, no local search, ants on this rank): the grid's last block
+ * publishes, waits for the peers' flags and selects, then every block updates.  That
+ * launch spins on the device until every peer has published, so the ranks' launches must
+ * be able to run concurrently (one process per GPU, or separate streams / processes);
+ * ranks sharing ONE stream must use the split calls.  The wait is
  * bounded (~2^34 GPU cycles): a lost peer sets an error that mmas_exchange_status(h)
  * reports as MMAS_ENCCL.  Iteration t uses buffer half t & 1, so ranks stay lockstep
  * without further synchronisation.  All calls are asynchronous except the wiring and

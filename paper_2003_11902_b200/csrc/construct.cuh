@@ -312,6 +312,54 @@ __device__ __forceinline__ unsigned long long finish_ant(const ConstructArgs& A,
     return ((unsigned long long)len << 24) | ant;   // iteration-best key (R8)
 }
 
+// Row a7 inside the fused launch (world > 1; called by every thread of the grid's last
+// block): the same steps as publish_peers_kernel + wait_peers_kernel + select_best_kernel
+// of the split path -- this shard's best record (key, route) into slot `rank` of every
+// peer's buffer, a system-wide fence, the flags; then a bounded wait for every peer's flag
+// of this iteration and the selection over the gathered records (the local key reset).
+__device__ __forceinline__ void exchange_select_block(const ConstructArgs& A, int lane, int warp) {
+    const ExchangeArgs& X = A.X;
+    __shared__ unsigned long long s_key;
+    if (threadIdx.x == 0) s_key = A.m_local > 0 ? __ldcg(A.best_key) : ~0ull;   // an empty shard never wins
+    __syncthreads();
+    const unsigned long long key = s_key;
+    const int al = (int)(key & 0xFFFFFFu) - A.ant_lo;
+    for (int p = 0; p < X.world; ++p) {
+        unsigned char* rec = xrecord(X.peers[p], X, (int)X.parity, X.rank);
+        if (A.m_local > 0) {
+            uint16_t* dst = reinterpret_cast<uint16_t*>(rec + 8);
+            for (int k = threadIdx.x; k < A.n; k += blockDim.x) dst[k] = A.routes[(size_t)al * A.ldr + k];
+        }
+        if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned long long*>(rec) = key;
+    }
+    __threadfence_system();   // records visible to every peer before any flag
+    __syncthreads();
+    if ((int)threadIdx.x < X.world) *(volatile uint32_t*)xflag(X.peers[threadIdx.x], X, (int)X.parity, X.rank) = X.seq;
+    if (warp == 0) {
+        if (lane < X.world) {
+            volatile uint32_t* f = xflag(A.xown, X, (int)X.parity, lane);
+            const long long t0 = clock64();
+            while (*f != X.seq) {
+                if (clock64() - t0 > (1ll << 34)) {
+                    atomicExch(A.xerr, 1u);
+                    break;
+                }
+                __nanosleep(200);
+            }
+        }
+        __syncwarp();
+        __threadfence();
+        SelectArgs S = A.sel;
+        S.records = A.xown + (size_t)X.parity * X.world * X.rec_bytes;
+        S.count = X.world;
+        select_best_warp(S, lane);
+        if (lane == 0) {
+            *A.done = 0u;
+            if (A.m_local > 0) *A.best_key = ~0ull;
+        }
+    }
+}
+
 // Block epilogue: the block's best key and fallback count reach global memory with
 // ONE atomic each (a per-ant global atomic makes ~10^3 same-address atomics queue
 // up at the end of the launch).  world == 1: the last block to finish selects the
@@ -343,7 +391,11 @@ __device__ __forceinline__ bool block_finish(const ConstructArgs& A, unsigned lo
     }
     __syncthreads();
     const bool last = s_last != 0u;
-    if (last && warp == 0) {
+    if (last && A.xchg) {
+        // world > 1 inside the fused launch: the whole last block publishes, waits, selects
+        __threadfence();
+        exchange_select_block(A, lane, warp);
+    } else if (last && warp == 0) {
         __threadfence();
         select_best_warp(A.sel, lane);
         if (lane == 0) *A.done = 0u;

@@ -174,6 +174,20 @@ __global__ void select_best_kernel(SelectArgs S) {
     if (threadIdx.x < 32) select_best_warp(S, threadIdx.x);
 }
 
+// peer-memory exchange (row a7; see publish_peers_kernel below)
+struct ExchangeArgs {
+    unsigned char* const* peers;   // device array: every rank's exchange buffer (peer-mapped)
+    int world, rank, rec_bytes;
+    uint32_t parity, seq;
+};
+
+__device__ __forceinline__ unsigned char* xrecord(unsigned char* buf, const ExchangeArgs& X, int p, int r) {
+    return buf + ((size_t)p * X.world + r) * X.rec_bytes;
+}
+__device__ __forceinline__ uint32_t* xflag(unsigned char* buf, const ExchangeArgs& X, int p, int r) {
+    return reinterpret_cast<uint32_t*>(buf + (size_t)2 * X.world * X.rec_bytes) + p * X.world + r;
+}
+
 // pheromone update arguments (row a6; pheromone_update_kernel below)
 struct UpdateArgs {
     float* tau;
@@ -243,6 +257,12 @@ struct ConstructArgs {
     int fuse_update;
     unsigned int* epoch;   // grid-barrier generation word (bumped once per fused launch)
     UpdateArgs upd;
+    // world > 1, fused launch (mmas_iterate_exchange): the last block publishes this shard's
+    // record to every peer, waits for theirs and selects over them (block_finish)
+    int xchg;
+    ExchangeArgs X;
+    unsigned char* xown;   // this rank's exchange buffer
+    uint32_t* xerr;        // set when a peer's flag does not arrive (bounded wait)
 };
 
 }  // namespace mmas
@@ -278,18 +298,6 @@ __global__ void publish_kernel(unsigned long long* local_key, const uint16_t* ro
 // a rank publishes iteration t + 2 only after its update t + 1, which waited for every
 // rank's record of t + 1, published after that rank had finished reading iteration t.
 // ---------------------------------------------------------------------------
-struct ExchangeArgs {
-    unsigned char* const* peers;   // device array: every rank's exchange buffer (peer-mapped)
-    int world, rank, rec_bytes;
-    uint32_t parity, seq;
-};
-__device__ __forceinline__ unsigned char* xrecord(unsigned char* buf, const ExchangeArgs& X, int p, int r) {
-    return buf + ((size_t)p * X.world + r) * X.rec_bytes;
-}
-__device__ __forceinline__ uint32_t* xflag(unsigned char* buf, const ExchangeArgs& X, int p, int r) {
-    return reinterpret_cast<uint32_t*>(buf + (size_t)2 * X.world * X.rec_bytes) + p * X.world + r;
-}
-
 // One block: this shard's best record (key = len << 24 | global ant, route) to every peer.
 __global__ void publish_peers_kernel(unsigned long long* local_key, const uint16_t* routes, int ldr, int ant_lo,
                                      int n, int m_local, ExchangeArgs X) {

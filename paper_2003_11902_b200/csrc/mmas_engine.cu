@@ -115,6 +115,7 @@ struct mmas_ctx {
     // launch plan for construction
     bool smem_table = false;
     bool fuse_update = false;               // world == 1: update fused into the construction launch
+    bool fuse_peers = false;                // world > 1: mmas_iterate_exchange as one launch per iteration
 
     bool reg_tabu = false;   // n <= 1024: tabu words in registers
     bool compact_tabu = false;  // cl == 0 with MMAS_TABU_COMPACT: construct_ct_kernel (R27)
@@ -259,6 +260,7 @@ ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = f
     A.alpha = h->alpha;
     A.epoch = h->done + 1;
     A.upd = update_args(h);
+    A.xchg = 0;
     return A;
 }
 
@@ -360,7 +362,7 @@ void launch_full(mmas_ctx* h, const ConstructArgs& A) {
 
 // Construction (rows a1-a4) -- and, with local search on, the 2-opt pass (row a8) that
 // then owns the tour lengths and the iteration-best bookkeeping (row a5).
-int launch_construct(mmas_ctx* h, bool fuse_select) {
+int launch_construct(mmas_ctx* h, bool fuse_select, const ExchangeArgs* xfused = nullptr) {
     if (h->m_local == 0) return MMAS_OK;
     if (h->cfg.local_search) {
         {
@@ -379,8 +381,14 @@ int launch_construct(mmas_ctx* h, bool fuse_select) {
         return launch_two_opt(h, fuse_select);
     }
     PhaseScope ps(h, 0);
-    ConstructArgs A = construct_args(h, fuse_select);
-    A.fuse_update = fuse_select && h->fuse_update ? 1 : 0;
+    ConstructArgs A = construct_args(h, fuse_select || xfused != nullptr);
+    A.fuse_update = (fuse_select && h->fuse_update) || xfused ? 1 : 0;
+    if (xfused) {
+        A.xchg = 1;
+        A.X = *xfused;
+        A.xown = h->xbuf;
+        A.xerr = h->xerr;
+    }
     if (h->cl == 0 || h->rwm) {
         launch_full(h, A);
     } else if (h->reg_tabu) {
@@ -693,9 +701,11 @@ int setup(mmas_ctx* h) {
             // no exchange or local search between construction and update, and room for each
             // warp's tau + heur rows in the block's shared memory
             const size_t fused_need = 256 + (size_t)w * 2 * 4 * h->ld;
-            h->fuse_update = c.world == 1 && !c.local_search && h->slots == 1 && !c.separate_update &&
-                             std::max(need, fused_need) <= cons_dyn_max;
-            if (h->fuse_update) h->cons_smem = std::max(need, fused_need);
+            const bool fusable = !c.local_search && h->slots == 1 && !c.separate_update &&
+                                 std::max(need, fused_need) <= cons_dyn_max;
+            h->fuse_update = fusable && c.world == 1;
+            h->fuse_peers = fusable && c.world > 1 && h->m_local > 0;
+            if (fusable) h->cons_smem = std::max(need, fused_need);
         } else {
             h->cons_warps = 4;
             h->cons_grid = std::max(1, (h->m_local + 3) / 4);
@@ -982,8 +992,20 @@ int mmas_iterate_exchange(mmas_ctx* h, int32_t iters) {
     int st = check(h);
     if (st) return st;
     if (iters < 1) return fail(MMAS_EINVAL, "iters must be >= 1");
-    for (int32_t i = 0; i < iters; ++i)
-        if ((st = mmas_construct_publish(h)) || (st = mmas_update_exchange(h))) return st;
+    if (!h->xattached) return fail(MMAS_ESTATE, "attach the peer exchange buffers first");
+    CU(cudaSetDevice(h->device));
+    for (int32_t i = 0; i < iters; ++i) {
+        if (h->fuse_peers) {
+            // ONE launch: construction, the last block's publish + wait + select, grid
+            // barrier, update (construct.cuh exchange_select_block / fused_update)
+            const ExchangeArgs X = exchange_args(h);
+            if ((st = launch_construct(h, false, &X))) return st;
+            h->iteration++;
+            if (h->profiling) h->acc_iters++;
+        } else if ((st = mmas_construct_publish(h)) || (st = mmas_update_exchange(h))) {
+            return st;
+        }
+    }
     return MMAS_OK;
 }
 
@@ -1146,7 +1168,7 @@ int mmas_get_stats(mmas_ctx* h, mmas_stats* out) {
     out->ants_local = h->m_local;
     out->first_ant = h->ant_lo;
     out->local_search_moves = 0;
-    out->update_fused = h->fuse_update ? 1 : 0;
+    out->update_fused = (h->fuse_update || h->fuse_peers) ? 1 : 0;
     if (h->ls_moves) {
         unsigned long long mv = 0;
         CU(cudaMemcpy(&mv, h->ls_moves, sizeof(mv), cudaMemcpyDeviceToHost));

@@ -40,6 +40,35 @@ def test_in_process_peer_exchange_equals_single(world, m, cl):
         sh.exchange_status()
 
 
+@pytest.mark.parametrize("world,m,cl", [(2, 40, 16), (3, 43, 8)])
+def test_in_process_fused_exchange_iteration_equals_single(world, m, cl):
+    """mmas_iterate_exchange as ONE launch per iteration (construct.cuh
+    exchange_select_block: the grid's last block publishes, waits on the device flags and
+    selects; then the fused update).  The shards run on their own streams so their
+    launches overlap on the one GPU (each grid is a few small blocks), as they would on
+    separate GPUs."""
+    c = make_coords("uniform", 150, 19)
+    ref = mmas.Colony(c, m, cl, seed=6)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    shards = [mmas.Colony(c, m, cl, seed=6, stream=streams[r].cuda_stream, rank=r, world=world)
+              for r in range(world)]
+    assert all(sh.stats()["update_fused"] == 1 for sh in shards)
+    bufs = [sh.exchange_buffer() for sh in shards]
+    for sh in shards:
+        sh.exchange_attach(bufs)
+    for it in range(4):
+        ref.iterate(1)
+        for sh in shards:
+            sh.iterate_exchange(1)
+        for sh in shards:
+            sh.sync()
+            sh.exchange_status()
+        assert np.array_equal(np.concatenate([sh.tours() for sh in shards]), ref.tours()), f"iteration {it}"
+        for sh in shards:
+            assert np.array_equal(sh.tau(), ref.tau()) and np.array_equal(sh.inv_w(), ref.inv_w())
+            assert sh.best_tour()[1] == ref.best_tour()[1]
+
+
 def _free_port():
     sk = socket.socket()
     sk.bind(("127.0.0.1", 0))

@@ -302,10 +302,11 @@ def test_fused_update_equals_separate_kernel(n, m, cl, iters, kw):
 
 
 def test_fused_update_not_used_where_ineligible():
-    """Exchange contexts (world > 1), local search, cl > 32 and L2-table colonies keep the
-    separate update kernel."""
+    """Local search, cl > 32, L2-table colonies and empty shards keep the separate update
+    kernel (world > 1 shards with ants fuse mmas_iterate_exchange, test_exchange_gpu.py)."""
     c = make_coords("uniform", 200, 3)
-    assert mmas.Colony(c, 40, 16, rank=0, world=2).stats()["update_fused"] == 0
+    assert mmas.Colony(c, 40, 16, rank=0, world=2).stats()["update_fused"] == 1
+    assert mmas.Colony(c, 3, 16, rank=0, world=4).stats()["update_fused"] == 0   # no ants on rank 0
     assert mmas.Colony(c, 10, 16, local_search=True).stats()["update_fused"] == 0
     assert mmas.Colony(c, 40, 40).stats()["update_fused"] == 0
     assert mmas.Colony(make_coords("uniform", 1500, 3), 20, 32).stats()["update_fused"] == 0
