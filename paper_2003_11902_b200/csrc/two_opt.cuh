@@ -259,7 +259,15 @@ constexpr int kLsWarps = 8;
 
 struct MoveEval {
     int found, dir, b, c, d;
+    int i, j;   // the forward segment to reverse (before the shorter-side choice), read during
+                // the evaluation so the apply step needs no position reads (and no barrier)
 };
+// Shared-memory form (16 B: found, b | c << 16, d, i | j << 16).  The size matters: three
+// 76.4 KB blocks per SM (C5) leave only ~350 B of static shared memory per block.
+__device__ __forceinline__ uint4 pack_eval(const MoveEval& m) {
+    return make_uint4((uint32_t)m.found, (uint32_t)m.b | ((uint32_t)m.c << 16), (uint32_t)m.d,
+                      (uint32_t)m.i | ((uint32_t)m.j << 16));
+}
 
 // Evaluate node a on the current route (one warp).  Lane k: the k-th neighbour.
 // d(a, c) comes from the setup's neighbour-distance table (loaded with the neighbour id).
@@ -298,7 +306,7 @@ __device__ __forceinline__ MoveEval eval_node(const TwoOptArgs& T, const uint16_
     }
     const uint32_t ms = __ballot_sync(kFull, imp_s);
     const uint32_t mp = __ballot_sync(kFull, imp_p);
-    MoveEval m{0, 0, 0, 0, 0};
+    MoveEval m{0, 0, 0, 0, 0, 0, 0};
     if (ms | mp) {
         m.found = 1;
         m.dir = ms ? 0 : 1;
@@ -306,6 +314,10 @@ __device__ __forceinline__ MoveEval eval_node(const TwoOptArgs& T, const uint16_
         m.c = __shfl_sync(kFull, c, kk);
         m.d = __shfl_sync(kFull, m.dir == 0 ? sc : pc, kk);
         m.b = m.dir == 0 ? sa : pr;
+        const int qk = __shfl_sync(kFull, lane < K ? (int)pos[c] : 0, kk);
+        // dir 0: reverse b .. c = pos[a]+1 .. pos[c];  dir 1: reverse a .. d = pos[a] .. pos[c]-1
+        m.i = m.dir == 0 ? wrap_inc(pa, n) : pa;
+        m.j = m.dir == 0 ? qk : wrap_dec(qk, n);
     }
     return m;
 }
@@ -314,7 +326,7 @@ template <bool kInt>
 __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs T, ConstructArgs A) {
     pdl_wait();
     extern __shared__ __align__(16) uint16_t ls_smem[];
-    __shared__ MoveEval s_eval[kLsWarps];
+    __shared__ uint4 s_eval[kLsWarps];
     __shared__ int s_ctl[4];   // head, count, sweep_moves, winner
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -351,14 +363,14 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
                     int q = head + warp;
                     if (q >= n) q -= n;
                     const MoveEval m = eval_node<kInt>(T, s_route, s_pos, (int)queue[q], lane);
-                    if (lane == 0) s_eval[warp] = m;
+                    if (lane == 0) s_eval[warp] = pack_eval(m);
                 }
                 __syncthreads();
                 // take the results in queue order up to the first improving one
                 const int avail = min(count, kLsWarps);
                 uint32_t fmask = 0;
 #pragma unroll
-                for (int w = 0; w < kLsWarps; ++w) fmask |= (w < avail && s_eval[w].found) ? 1u << w : 0u;
+                for (int w = 0; w < kLsWarps; ++w) fmask |= (w < avail && s_eval[w].x) ? 1u << w : 0u;
                 const int win = fmask ? __ffs(fmask) - 1 : -1;
                 const int retired = win >= 0 ? win + 1 : avail;
                 if (warp == 0 && lane < retired) {
@@ -371,14 +383,15 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
                 if (nhead >= n) nhead -= n;
                 int ncount = count - retired;
                 if (win >= 0) {
-                    const MoveEval m = s_eval[win];
+                    const uint4 pe = s_eval[win];
+                    const int mb = (int)(pe.y & 0xFFFFu), mc = (int)(pe.y >> 16), md = (int)pe.z;
                     int q = head + win;
                     if (q >= n) q -= n;
                     const int a = queue[q];
-                    // reverse (all lanes of all warps; disjoint pairs)
-                    int i = m.dir == 0 ? s_pos[m.b] : s_pos[a];
-                    int j = m.dir == 0 ? s_pos[m.c] : s_pos[m.d];
-                    __syncthreads();   // every thread has read the positions before they change
+                    // reverse (all lanes of all warps; disjoint pairs); the segment's positions
+                    // come with the evaluation, so no thread reads pos before it changes
+                    int i = (int)(pe.w & 0xFFFFu);
+                    int j = (int)(pe.w >> 16);
                     int len = j - i;
                     if (len < 0) len += n;
                     len += 1;
@@ -401,7 +414,7 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
                     }
                     // enqueue a, b, c, d in that order (thread 0; the bits of a .. d)
                     if (tid == 0) {
-                        const int ends[4] = {a, m.b, m.c, m.d};
+                        const int ends[4] = {a, mb, mc, md};
                         __threadfence_block();
                         for (int e = 0; e < 4; ++e) {
                             const int v = ends[e];
