@@ -655,6 +655,35 @@ __global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(Cons
                 if (j == 3 && h == 1) Ln[q][3] = det_log2(uniform_open(nx[q].w));
             }
         };
+        // Quarter slices for the speculative step, which has four latency windows (table
+        // loads, tabu shuffle, and the two reductions): Philox rounds 0-1 | 1-3 | 3-4 | 4-5,
+        // 5-6 | 6-8 | 8-9 | 9-10, then each log split in two (det_log2_a / det_log2_b).
+        Log2Part lp[kSlots];
+        auto slice_q = [&](auto J, auto Q) {
+            constexpr int j = decltype(J)::value;
+            constexpr int k = decltype(Q)::value;
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q) {
+                if (j == 0 && k == 0) philox_rounds<0, 1>(nx[q], rk);
+                if (j == 0 && k == 1) philox_rounds<1, 3>(nx[q], rk);
+                if (j == 0 && k == 2) philox_rounds<3, 4>(nx[q], rk);
+                if (j == 0 && k == 3) philox_rounds<4, 5>(nx[q], rk);
+                if (j == 1 && k == 0) philox_rounds<5, 6>(nx[q], rk);
+                if (j == 1 && k == 1) philox_rounds<6, 8>(nx[q], rk);
+                if (j == 1 && k == 2) philox_rounds<8, 9>(nx[q], rk);
+                if (j == 1 && k == 3) philox_rounds<9, 10>(nx[q], rk);
+                if (j >= 2) {
+                    const uint32_t w = (j == 2) ? (k < 2 ? nx[q].x : nx[q].y) : (k < 2 ? nx[q].z : nx[q].w);
+                    const int slot = 2 * (j - 2) + (k >> 1);
+                    if ((k & 1) == 0) lp[q] = det_log2_a(uniform_open(w));
+                    else Ln[q][slot] = det_log2_b(lp[q]);
+                }
+            }
+        };
+        using Q0 = std::integral_constant<int, 0>;
+        using Q1 = std::integral_constant<int, 1>;
+        using Q2 = std::integral_constant<int, 2>;
+        using Q3 = std::integral_constant<int, 3>;
         using H0 = std::integral_constant<int, 0>;
         using H1 = std::integral_constant<int, 1>;
         using I0 = std::integral_constant<int, 0>;
@@ -746,9 +775,11 @@ __global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(Cons
 #pragma unroll
             for (int q = 0; q < kSlots; ++q) Lv[q] = L[q][j];
             uint32_t bm, bc;
-            evaluate(Lv, [&] { slice_half(J, H0{}); }, [&] { slice_half(J, H1{}); }, bm, bc);
+            evaluate(Lv, [&] { slice_q(J, Q0{}); }, [&] { slice_q(J, Q1{}); }, bm, bc);
             const uint32_t best = __reduce_min_sync(kFull, bm);
+            slice_q(J, Q2{});
             const uint32_t nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
+            slice_q(J, Q3{});
             // every lane holds a real candidate (a visited one has bit 31 set), so nxt is a city
             // id < n even when best >= 2^31 (then it is undone by the caller)
             __builtin_assume(nxt < 65536u);

@@ -80,6 +80,40 @@ __device__ __forceinline__ float det_log2(float u) {
     return __fmaf_rn(f, p, ef);
 }
 
+// det_log2 in two parts (the same operations in the same order, so bit-identical): the
+// construction kernels place the halves in different latency windows of a step.
+struct Log2Part {
+    float f, p, ef;
+};
+__device__ __forceinline__ Log2Part det_log2_a(float u) {
+    const uint32_t b = __float_as_uint(u);
+    const uint32_t mant = b & 0x007FFFFFu;
+    int e = (int)(b >> 23) - 127;
+    uint32_t mb = mant | 0x3F800000u;
+    if (mant > 0x003504F3u) {
+        mb = mant | 0x3F000000u;
+        e += 1;
+    }
+    Log2Part r;
+    r.f = __fsub_rn(__uint_as_float(mb), 1.0f);
+    float p = 0.12583690881729126f;
+    p = __fmaf_rn(p, r.f, -0.20726971328258514f);
+    p = __fmaf_rn(p, r.f, 0.21571563184261322f);
+    p = __fmaf_rn(p, r.f, -0.23894482851028442f);
+    p = __fmaf_rn(p, r.f, 0.28791624307632446f);
+    r.p = p;
+    r.ef = __fsub_rn(__int_as_float(0x4B400000 + e), 12582912.0f);
+    return r;
+}
+__device__ __forceinline__ float det_log2_b(const Log2Part& r) {
+    float p = r.p;
+    p = __fmaf_rn(p, r.f, -0.3607036769390106f);
+    p = __fmaf_rn(p, r.f, 0.48091062903404236f);
+    p = __fmaf_rn(p, r.f, -0.7213473320007324f);
+    p = __fmaf_rn(p, r.f, 1.4426950216293335f);
+    return __fmaf_rn(r.f, p, r.ef);
+}
+
 // Counter layouts (R13).  x2 = global ant id, x3 = global iteration.
 __device__ __forceinline__ uint4 ctr_start(uint32_t ant, uint32_t iter) {
     return make_uint4(0x80000000u, 0u, ant, iter);
