@@ -134,6 +134,7 @@ struct mmas_ctx {
     uint16_t* ls_nn = nullptr;         // n x ls_k neighbour lists
     int32_t* ls_nnd = nullptr;         // n x ls_k: d(a, nn[a][k])
     short2* ls_xys = nullptr;          // integral coordinates (ls_int_xy), else null
+    uint32_t* ls_nnp = nullptr;        // ls_int_xy: packed neighbour id | distance << 16
     bool ls_int_xy = false;
     uint16_t *ls_pos = nullptr, *ls_queue = nullptr;
     uint32_t* ls_inq = nullptr;
@@ -416,6 +417,7 @@ int launch_two_opt(mmas_ctx* h, bool fuse_select) {
     T.nn = h->ls_nn;
     T.nnd = h->ls_nnd;
     T.xys = h->ls_xys;
+    T.nnp = h->ls_nnp;
     T.n = h->n;
     T.K = h->ls_k;
     T.ldr = h->ldr;
@@ -488,7 +490,7 @@ void free_ctx(mmas_ctx* h) {
     void* ptrs[] = {h->xy, h->heur, h->tau, h->inv_w, h->cand_inv, h->cand_id, h->routes, h->lengths,
                     h->best_key, h->fallback_count, h->ib_route, h->gb_route, h->succ, h->pred, h->gb_len,
                     h->ib_len, h->ib_ant, h->scal, h->iter_dev, h->local_record, h->done,
-                    h->ls_nn, h->ls_nnd, h->ls_xys, h->ls_pos, h->ls_queue, h->ls_inq, h->ls_moves};
+                    h->ls_nn, h->ls_nnd, h->ls_xys, h->ls_nnp, h->ls_pos, h->ls_queue, h->ls_inq, h->ls_moves};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : h->xopened) cudaIpcCloseMemHandle(p);
@@ -621,8 +623,13 @@ int setup(mmas_ctx* h) {
             (st = dalloc(&h->ls_moves, 1)))
             return st;
         if (h->ls_int_xy) {
-            if ((st = dalloc(&h->ls_xys, (size_t)n))) return st;
+            std::vector<uint32_t> nnp(nnl.size());
+            for (size_t e = 0; e < nnl.size(); ++e) nnp[e] = (uint32_t)nnl[e] | ((uint32_t)nnd[e] << 16);
+            if ((st = dalloc(&h->ls_xys, (size_t)n)) || (st = dalloc(&h->ls_nnp, nnp.size()))) return st;
             CU(cudaMemcpyAsync(h->ls_xys, xys.data(), sizeof(short2) * n, cudaMemcpyHostToDevice, h->stream));
+            CU(cudaMemcpyAsync(h->ls_nnp, nnp.data(), sizeof(uint32_t) * nnp.size(), cudaMemcpyHostToDevice,
+                               h->stream));
+            CU(cudaStreamSynchronize(h->stream));   // the host vectors go out of scope
         }
         CU(cudaMemcpyAsync(h->ls_nnd, nnd.data(), sizeof(int32_t) * nnd.size(), cudaMemcpyHostToDevice, h->stream));
         CU(cudaMemcpyAsync(h->ls_nn, nnl.data(), sizeof(uint16_t) * nnl.size(), cudaMemcpyHostToDevice, h->stream));

@@ -18,6 +18,7 @@ struct TwoOptArgs {
     const double2* __restrict__ xy;
     const short2* __restrict__ xys;    // integral coordinates, |x|, |y| <= 16383 (kIntXY kernels), else null
     const int32_t* __restrict__ nnd;   // n x K: d(a, nn[a][k]) (setup, exact R12 distances)
+    const uint32_t* __restrict__ nnp;  // kIntXY: n x K packed nn[a][k] | d(a, nn[a][k]) << 16 (d < 46339)
     const uint16_t* __restrict__ nn;   // n x K neighbour lists (R10 order)
     int n, K, ldr, m_local, warps_per_block, nwords;
     uint16_t* routes;                  // m_local x ldr (in: constructed routes; out: improved)
@@ -68,6 +69,19 @@ struct Pts<true> {
     __device__ __forceinline__ static int64_t dist(P a, P b) { return euc2d_int(a, b); }
 };
 
+// neighbour k of a and d(a, it): one 4-byte load of the packed table (integer path), else two
+template <bool kInt>
+__device__ __forceinline__ void load_nbr(const TwoOptArgs& T, int a, int k, int& c, int64_t& d) {
+    if (kInt) {
+        const uint32_t v = __ldg(T.nnp + (size_t)a * T.K + k);
+        c = (int)(v & 0xFFFFu);
+        d = (int64_t)(v >> 16);
+    } else {
+        c = T.nn[(size_t)a * T.K + k];
+        d = __ldg(T.nnd + (size_t)a * T.K + k);
+    }
+}
+
 __device__ __forceinline__ int wrap_inc(int i, int n) { return i + 1 == n ? 0 : i + 1; }
 __device__ __forceinline__ int wrap_dec(int i, int n) { return i == 0 ? n - 1 : i - 1; }
 
@@ -116,8 +130,9 @@ __device__ __forceinline__ long long two_opt_route(const TwoOptArgs& T, uint16_t
         // the static data of a popped node (its neighbour list entry per lane and the
         // coordinates) is loaded one pop AHEAD, behind the current pop's work
         int a = queue[0];
-        int c = lane < K ? T.nn[(size_t)a * K + lane] : a;
-        int64_t dac = lane < K ? __ldg(T.nnd + (size_t)a * K + lane) : 0;
+        int c = a;
+        int64_t dac = 0;
+        if (lane < K) load_nbr<kInt>(T, a, lane, c, dac);
         P xa = X.at(a), xc = X.at(c);
         while (count > 0) {
             head = wrap_inc(head, n);
@@ -128,8 +143,9 @@ __device__ __forceinline__ long long two_opt_route(const TwoOptArgs& T, uint16_t
             const int pa = pos[a];
             const int sa = route[wrap_inc(pa, n)];      // successor of a
             const int pr = route[wrap_dec(pa, n)];      // predecessor of a
-            const int c2 = lane < K ? T.nn[(size_t)a2 * K + lane] : a2;
-            const int64_t dac2 = lane < K ? __ldg(T.nnd + (size_t)a2 * K + lane) : 0;
+            int c2 = a2;
+            int64_t dac2 = 0;
+            if (lane < K) load_nbr<kInt>(T, a2, lane, c2, dac2);
             const P xa2 = X.at(a2);
             const P xs = X.at(sa), xp = X.at(pr);
             const int64_t d_as = X.dist(xa, xs);
@@ -200,8 +216,9 @@ __device__ __forceinline__ long long two_opt_route(const TwoOptArgs& T, uint16_t
                 xc = xc2;
             } else if (count > 0) {   // the queue had run empty: the next pop was just enqueued
                 a = queue[head];
-                c = lane < K ? T.nn[(size_t)a * K + lane] : a;
-                dac = lane < K ? __ldg(T.nnd + (size_t)a * K + lane) : 0;
+                c = a;
+                dac = 0;
+                if (lane < K) load_nbr<kInt>(T, a, lane, c, dac);
                 xa = X.at(a);
                 xc = X.at(c);
             }
@@ -279,10 +296,7 @@ __device__ __forceinline__ MoveEval eval_node(const TwoOptArgs& T, const uint16_
     using P = typename Pts<kInt>::P;
     int c = a, sc = 0, pc = 0;
     int64_t d_ac = 0;
-    if (lane < K) {
-        c = T.nn[(size_t)a * K + lane];
-        d_ac = __ldg(T.nnd + (size_t)a * K + lane);
-    }
+    if (lane < K) load_nbr<kInt>(T, a, lane, c, d_ac);
     const int pa = pos[a];
     const int sa = route[wrap_inc(pa, n)];
     const int pr = route[wrap_dec(pa, n)];
