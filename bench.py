@@ -44,6 +44,16 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def onchip_peaks():
+    """Measured L2 / shared-memory read bandwidth (tools/onchip_peaks.cu, committed in
+    profiles/onchip_peaks.json); None if absent."""
+    p = os.path.join(ROOT, "profiles", "onchip_peaks.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
 class ClockSampler:
     """NVML sampling of SM clock and throttle reasons during the timed region."""
 
@@ -326,6 +336,20 @@ def run_ours(args):
                 "note": "algorithmic bytes per tour: see algorithmic_bytes_per_tour() and DESIGN.md Sec. 5; the "
                         "construction kernels are issue/latency-bound (ALU + the per-step dependent chain), so "
                         "the issue and chain views below are the ones that bound them (SURVEY 8(d))"}
+    # (1b) the on-chip resource the candidate rows actually come from: shared memory (table
+    # staged per launch: C1, C2) or L2 (the rest), against the measured read bandwidth
+    pk = onchip_peaks()
+    if pk:
+        smem_table = bool(w.cand_len) and not w.selection and w.n * 32 * 6 <= 200 * 1024
+        res = "smem" if smem_table else "l2"
+        peak_on = pk["smem_read_gbs" if smem_table else "l2_read_gbs"]
+        cand_bytes = algorithmic_bytes_per_tour(w) * col.shard()[1]
+        ach_on = cand_bytes / (cons_ms * 1e-3) / 1e9
+        roofline["onchip"] = {"resource": res, "achieved": ach_on, "peak": peak_on, "unit": "GB/s",
+                              "frac": ach_on / peak_on,
+                              "peak_source": "measured: profiles/onchip_peaks.json (tools/onchip_peaks.cu)",
+                              "note": "the construction's algorithmic candidate/row bytes over the launch time "
+                                      "against the measured read bandwidth of the resource they are read from"}
     # (2) issue roofline: warp instructions per launch (ncu capture of the same launch configuration)
     # over the live kernel time, against 4 schedulers x SMs x the SM clock sampled during the run
     sm_mhz = clk.summary().get("sm_mhz") or 0.0
