@@ -40,17 +40,17 @@ def test_in_process_peer_exchange_equals_single(world, m, cl):
         sh.exchange_status()
 
 
-@pytest.mark.parametrize("world,m,cl", [(2, 40, 16), (3, 43, 8)])
-def test_in_process_fused_exchange_iteration_equals_single(world, m, cl):
+@pytest.mark.parametrize("world,m,cl,kw", [(2, 40, 16, {}), (3, 43, 8, {}), (2, 30, 8, {"deposit_global": True})])
+def test_in_process_fused_exchange_iteration_equals_single(world, m, cl, kw):
     """mmas_iterate_exchange as ONE launch per iteration (construct.cuh
     exchange_select_block: the grid's last block publishes, waits on the device flags and
     selects; then the fused update).  The shards run on their own streams so their
     launches overlap on the one GPU (each grid is a few small blocks), as they would on
     separate GPUs."""
     c = make_coords("uniform", 150, 19)
-    ref = mmas.Colony(c, m, cl, seed=6)
+    ref = mmas.Colony(c, m, cl, seed=6, **kw)
     streams = [torch.cuda.Stream() for _ in range(world)]
-    shards = [mmas.Colony(c, m, cl, seed=6, stream=streams[r].cuda_stream, rank=r, world=world)
+    shards = [mmas.Colony(c, m, cl, seed=6, stream=streams[r].cuda_stream, rank=r, world=world, **kw)
               for r in range(world)]
     assert all(sh.stats()["update_fused"] == 1 for sh in shards)
     bufs = [sh.exchange_buffer() for sh in shards]

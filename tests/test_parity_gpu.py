@@ -276,6 +276,8 @@ FUSE_CASES = [
     (1025, 40, 32, 2, {}),                     # n > 1024: shared-memory tabu, ragged float4 tail
     (130, 2400, 32, 2, {}),                    # 16 ant warps per block, several ants per warp
     (97, 50, 8, 3, {"deposit_global": True}),
+    (97, 50, 8, 3, {"fallback_argmax": True}),
+    (90, 25, 12, 3, {"rho": 0.9, "p_best": 0.05}),
     (64, 20, 10, 3, {"alpha": 2.0, "beta": 3.0}),
     (5, 7, 1, 3, {}),                          # n <= 5: tau_min clamped to tau_max
 ]
