@@ -524,6 +524,7 @@ __device__ __noinline__ void fused_update(const UpdateArgs U, unsigned int* epoc
         while (ld_acquire_gpu(epoch) == epoch0) __nanosleep(32);
     }
     __syncthreads();
+    trace_mark(4);
     const float tmin = __ldcg(U.scal), tmax = __ldcg(U.scal + 1), delta = __ldcg(U.scal + 2);
     const int n4 = (U.n + 3) >> 2;
     uint32_t phase = 0;
@@ -565,6 +566,7 @@ __device__ __noinline__ void fused_update(const UpdateArgs U, unsigned int* epoc
 template <int kSlots, bool kSmemTable, bool kRegTabu, bool kFull32, bool kWide = false>
 __global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(ConstructArgs A) {
     pdl_wait();
+    trace_mark(0);
     static_assert(!kFull32 || kSlots == 1, "kFull32: cl == 32, one slot per lane");
     static_assert(!kWide || (kFull32 && kSmemTable), "kWide: one-slot shared-memory-table variant only");
     using Tabu = typename std::conditional<kRegTabu, RegTabuX<kFull32>, SmemTabu>::type;
@@ -607,6 +609,7 @@ __global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(Cons
         __syncthreads();   // the barrier is initialised before anyone waits on it
         mbar_wait(bar, 0);
     }
+    trace_mark(1);
     unsigned long long wbest = ~0ull;
     long long wfb = 0;
 
@@ -893,10 +896,13 @@ __global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(Cons
         wfb += fb;
     }
     pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
+    trace_mark(2);
     const bool last = block_finish(A, wbest, wfb, lane, warp);
+    trace_mark(3);
     if constexpr (kSmemTable) {
         if (A.fuse_update) fused_update(A.upd, A.epoch, last, epoch0, lane, warp);
     }
+    trace_mark(5);
 }
 
 // ---------------------------------------------------------------------------

@@ -30,6 +30,22 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
+// Phase timestamps of construct_cl_kernel (tools/trace_phases.py; only with -DMMAS_TRACE):
+// per block [entry, table staged, warp 0's ants done, block_finish done (the last block:
+// + selection), barrier released, end], %globaltimer ns, thread 0.  No code otherwise.
+#ifdef MMAS_TRACE
+__device__ unsigned long long g_trace[1024 * 8];
+__device__ __forceinline__ void trace_mark(int k) {
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+        g_trace[blockIdx.x * 8 + k] = t;
+    }
+}
+#else
+__device__ __forceinline__ void trace_mark(int) {}
+#endif
+
 // TSPLIB EUC_2D (R12): (int)(sqrt(dx*dx + dy*dy) + 0.5) in double.
 __device__ __forceinline__ int32_t euc2d(double2 p, double2 q) {
     const double dx = __dsub_rn(p.x, q.x);

@@ -1261,3 +1261,17 @@ int mmas_sync(mmas_ctx* h) {
 }
 
 }  // extern "C"
+
+// Debug: copy the construct_cl_kernel phase timestamps (a -DMMAS_TRACE build; see
+// tools/trace_phases.py).  Not part of the documented ABI; MMAS_ESTATE otherwise.
+extern "C" int mmas_debug_trace(unsigned long long* out, int count) {
+#ifdef MMAS_TRACE
+    if (!out || count < 0 || count > 1024 * 8) return MMAS_EINVAL;
+    if (cudaMemcpyFromSymbol(out, mmas::g_trace, sizeof(unsigned long long) * count) != cudaSuccess) return MMAS_ECUDA;
+    return MMAS_OK;
+#else
+    (void)out;
+    (void)count;
+    return MMAS_ESTATE;
+#endif
+}

@@ -12,7 +12,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmmas.so")
+# MMAS_LIB: an alternative in-tree build of the same library (e.g. the -DMMAS_TRACE build
+# tools/trace_phases.py makes); the CUDA path is the only path either way
+LIB_PATH = os.environ.get("MMAS_LIB") or os.path.join(_HERE, "libmmas.so")
 
 MMAS_OK, MMAS_EINVAL, MMAS_ENOMEM, MMAS_ECUDA, MMAS_ENCCL, MMAS_ESTATE = 0, -1, -2, -3, -4, -5
 DEPOSIT_ITERATION_BEST, DEPOSIT_GLOBAL_BEST = 0, 1
