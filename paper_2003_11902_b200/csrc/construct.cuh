@@ -395,10 +395,10 @@ __device__ __forceinline__ bool block_finish(const ConstructArgs& A, unsigned lo
         // world > 1 inside the fused launch: the whole last block publishes, waits, selects
         __threadfence();
         exchange_select_block(A, lane, warp);
-    } else if (last && warp == 0) {
+    } else if (last) {
         __threadfence();
-        select_best_warp(A.sel, lane);
-        if (lane == 0) *A.done = 0u;
+        select_best_block(A.sel);
+        if (threadIdx.x == 0) *A.done = 0u;
     }
     return last;
 }

@@ -185,6 +185,52 @@ __device__ __noinline__ void select_best_warp(const SelectArgs S, int lane) {
     }
 }
 
+// Row a5 by a whole block (the fused launch's last block): thread 0 reads the key and sets
+// gb / limits / Delta exactly as select_best_warp does; every thread then copies and links
+// a share of the deposit route (succ / pred), so one warp does not issue ~2n scattered
+// stores in sequence.  Called by every thread of the block.
+__device__ __noinline__ void select_best_block(const SelectArgs S) {
+    __shared__ const uint16_t* s_src;
+    __shared__ int s_improved;
+    const int n = S.n;
+    if (threadIdx.x == 0) {
+        const unsigned long long key = __ldcg(S.local_key);
+        const long long gbl = __ldcg(S.gb_len);
+        const uint16_t* src = S.routes + (size_t)((int)(key & 0xFFFFFFu) - S.ant_lo) * S.ldr;
+        const long long len = (long long)(key >> 24);
+        const int improved = (gbl < 0 || len < gbl);   // strictly shorter (R8)
+        if (improved) {
+            *S.gb_len = len;
+            // R2: tau_max = 1/((1-rho) C_gb), tau_min = tau_max * F, clamped <= tau_max
+            const double tx = __ddiv_rn(1.0, __dmul_rn(__dsub_rn(1.0, S.rho), (double)len));
+            double tn = __dmul_rn(tx, S.factor);
+            if (tn > tx) tn = tx;
+            S.scal[0] = __double2float_rn(tn);
+            S.scal[1] = __double2float_rn(tx);
+        }
+        const long long dep = S.deposit_global ? (improved ? len : gbl) : len;
+        S.scal[2] = __double2float_rn(__ddiv_rn(1.0, (double)dep));   // R6
+        *S.ib_len = len;
+        *S.ib_ant = (int)(key & 0xFFFFFFu);
+        *S.local_key = ~0ull;
+        s_src = src;
+        s_improved = improved;
+    }
+    __syncthreads();
+    const uint16_t* src = s_src;
+    const int improved = s_improved;
+    const uint16_t* dep = (!S.deposit_global || improved) ? src : S.gb_route;
+    // gb <- ib first when the deposit route is the old gb (deposit_global && !improved never
+    // copies, so dep is never overwritten while it is read)
+    for (int k = (int)threadIdx.x; k < n; k += (int)blockDim.x) {
+        const uint16_t i = __ldcg(dep + k);
+        const uint16_t j = __ldcg(dep + (k + 1 < n ? k + 1 : 0));
+        if (improved) S.gb_route[k] = __ldcg(src + k);
+        S.succ[i] = j;
+        S.pred[j] = i;
+    }
+}
+
 __global__ void select_best_kernel(SelectArgs S) {
     pdl_wait();
     if (threadIdx.x < 32) select_best_warp(S, threadIdx.x);
