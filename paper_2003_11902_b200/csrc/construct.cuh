@@ -234,7 +234,8 @@ __device__ __forceinline__ uint32_t chunk_nibble(const Tabu& tabu, int c0, int n
 // larger, so it prunes less), but the warp reduction after trip i is only needed at trip
 // i + 2, so the trips do not serialise on it.  At a few warps per SM (C5) the branch-free
 // scan is faster (its eight independent log chains per trip are the ILP those warps lack).
-template <bool kArgmax, bool kPrefetch = false, bool kLagPrune = false, class Tabu>
+// kRowSmem: `row` is a copy of the inv_w row in shared memory (plain loads, no __ldg)
+template <bool kArgmax, bool kPrefetch = false, bool kLagPrune = false, bool kRowSmem = false, class Tabu>
 __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, const Tabu& tabu, int n,
                                                uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
                                                int lane, uint32_t& best_mag, uint32_t& best_c) {
@@ -246,8 +247,13 @@ __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, co
         const int ca = base + 4 * lane, cb = ca + 128;
         na = chunk_nibble(tabu, ca, n);
         nb = chunk_nibble(tabu, cb, n);
-        iva = na != 0xFu ? __ldg(reinterpret_cast<const float4*>(row + ca)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        ivb = nb != 0xFu ? __ldg(reinterpret_cast<const float4*>(row + cb)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (kRowSmem) {
+            iva = na != 0xFu ? reinterpret_cast<const float4*>(row)[ca >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
+            ivb = nb != 0xFu ? reinterpret_cast<const float4*>(row)[cb >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            iva = na != 0xFu ? __ldg(reinterpret_cast<const float4*>(row + ca)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            ivb = nb != 0xFu ? __ldg(reinterpret_cast<const float4*>(row + cb)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     };
     if constexpr (kPrefetch) {
         // the next trip's visited bits and inv_w float4s are loaded one trip ahead
@@ -475,6 +481,45 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
 //   [.., + W * 4*nwords)     tabu words (SmemTabu variant)
 extern __shared__ __align__(128) unsigned char g_smem[];
 
+// ---- fallback row staging (L2-table kernel, C3 / C5) ---------------------------------
+// One inv_w-row buffer per block in shared memory (ConstructArgs::fb_row_off), used by one
+// warp at a time: a warp that falls back (R9) and finds it free takes it (smem flag), copies
+// the row in with one cp.async.bulk, waits on the block's mbarrier (its phase kept next to
+// the flag) and scans from shared memory; a warp that finds it taken scans from global.
+// Layout in the [0, 128) header: mbarrier at 0 (unused by this kernel's table path), flag
+// at 64, phase at 68.
+__device__ __forceinline__ bool stage_fallback_row(const ConstructArgs& A, const float* row, int lane) {
+    uint32_t* flag = reinterpret_cast<uint32_t*>(g_smem + 64);
+    uint32_t* phase = reinterpret_cast<uint32_t*>(g_smem + 68);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
+    uint32_t got = 0, ph = 0;
+    if (lane == 0) {
+        got = atomicCAS(flag, 0u, 1u) == 0u;
+        if (got) {
+            ph = *reinterpret_cast<volatile uint32_t*>(phase);
+            fence_proxy_async_smem();   // earlier generic reads of the buffer before the copy
+            const uint32_t bytes = (uint32_t)(((size_t)A.n * 4 + 15) & ~(size_t)15);
+            mbar_expect_tx(bar, bytes);
+            bulk_g2s(smem_u32(g_smem + A.fb_row_off), row, bytes, bar);
+        }
+    }
+    got = __shfl_sync(kFull, got, 0);
+    if (!got) return false;
+    ph = __shfl_sync(kFull, ph, 0);
+    mbar_wait(bar, ph);
+    return true;
+}
+__device__ __forceinline__ void release_fallback_row(int lane) {
+    __syncwarp();   // every lane is done reading the buffer
+    if (lane == 0) {
+        uint32_t* phase = reinterpret_cast<uint32_t*>(g_smem + 68);
+        *reinterpret_cast<volatile uint32_t*>(phase) ^= 1u;
+        __threadfence_block();
+        atomicExch(reinterpret_cast<uint32_t*>(g_smem + 64), 0u);
+    }
+}
+
+
 // ---------------------------------------------------------------------------
 // Pheromone update fused into the construction launch (row a6; world == 1, persistent
 // shared-memory-table grid, every block resident at once).  Same arithmetic as
@@ -564,11 +609,15 @@ __device__ __noinline__ void fused_update(const UpdateArgs U, unsigned int* epoc
 // kWide: up to 16 ant warps per block (large colonies with the shared-memory table; the
 // register budget drops to 128), else up to 8
 template <int kSlots, bool kSmemTable, bool kRegTabu, bool kFull32, bool kWide = false>
-__global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(ConstructArgs A) {
+// L2-table variants run 4-warp blocks and need 4 blocks per SM (128 registers) when the
+// colony fills the SMs (C3's 3795 ants: 25 warps per SM); with kWide (few ant warps per SM,
+// C5) the register budget is left to the compiler
+__global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmemTable || kWide) ? 1 : 4)
+    construct_cl_kernel(ConstructArgs A) {
     pdl_wait();
     trace_mark(0);
     static_assert(!kFull32 || kSlots == 1, "kFull32: cl == 32, one slot per lane");
-    static_assert(!kWide || (kFull32 && kSmemTable), "kWide: one-slot shared-memory-table variant only");
+    static_assert(!kWide || kFull32, "kWide: one-slot variants only");
     using Tabu = typename std::conditional<kRegTabu, RegTabuX<kFull32>, SmemTabu>::type;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -605,6 +654,14 @@ __global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(Cons
     const uint32_t iter = *A.iter_dev;
     // grid-barrier generation of the fused update: read before this block can arrive
     const uint32_t epoch0 = (kSmemTable && A.fuse_update) ? ld_acquire_gpu(A.epoch) : 0u;
+    if (!kSmemTable && A.fb_row_off) {
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            *reinterpret_cast<uint32_t*>(g_smem + 64) = 0u;
+            *reinterpret_cast<uint32_t*>(g_smem + 68) = 0u;
+        }
+        __syncthreads();
+    }
     if (kSmemTable) {
         __syncthreads();   // the barrier is initialised before anyone waits on it
         mbar_wait(bar, 0);
@@ -806,7 +863,18 @@ __global__ void __launch_bounds__(kWide ? 512 : 256, 1) construct_cl_kernel(Cons
                 uint32_t fm = kNone, fc = kNone;
                 if (A.fallback_argmax)
                     scan_unvisited<true>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm, fc);
-                else if (!kSmemTable && A.prune_fallback)
+                else if (!kSmemTable && A.fb_row_off && stage_fallback_row(A, row, lane)) {
+                    // the row came into the block's shared buffer by one TMA copy: the scan reads
+                    // it there instead of paying one L2/HBM latency per trip
+                    const float* srow = reinterpret_cast<const float*>(g_smem + A.fb_row_off);
+                    if (A.prune_fallback)
+                        scan_unvisited<false, false, true, true>(srow, tabu, n, (uint32_t)s, ant, iter, A.key, lane,
+                                                                 fm, fc);
+                    else
+                        scan_unvisited<false, false, false, true>(srow, tabu, n, (uint32_t)s, ant, iter, A.key,
+                                                                  lane, fm, fc);
+                    release_fallback_row(lane);
+                } else if (!kSmemTable && A.prune_fallback)
                     scan_unvisited<false, false, !kSmemTable>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm,
                                                               fc);
                 else

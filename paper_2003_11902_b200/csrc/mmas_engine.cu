@@ -123,6 +123,7 @@ struct mmas_ctx {
     int slots = 1;
     int cons_warps = 4, cons_grid = 1;
     size_t cons_smem = 0;
+    uint32_t fb_row_off = 0;                // L2-table kernel: fallback row buffer in smem
     uint32_t tb_inv = 0, tb_id = 0;
 
     // host mirrors
@@ -249,6 +250,7 @@ ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = f
     // pruned fallback scans where 16+ ant warps per SM hide their reduction latency (C3:
     // 5.78 -> 5.34 ms); the branch-free scan at fewer (C5: 29.4 vs 33.0 ms pruned)
     A.prune_fallback = h->m_local >= 16 * h->num_sms;
+    A.fb_row_off = h->fb_row_off;
     A.warps_per_block = h->cons_warps;
     A.table_bytes_inv = h->tb_inv;
     A.table_bytes_id = h->tb_id;
@@ -316,6 +318,12 @@ void launch_cl(mmas_ctx* h, const ConstructArgs& A) {
                 launch_cl_f<1, T, R, true, true>(h, A);
                 return;
             }
+        } else {
+            // L2 table, fewer than 16 ant warps per SM: the uncapped-register instantiation
+            if (h->m_local < 16 * h->num_sms) {
+                launch_cl_f<1, T, R, true, true>(h, A);
+                return;
+            }
         }
         launch_cl_f<1, T, R, true>(h, A);
     } else {
@@ -341,6 +349,7 @@ template <bool R>
 void set_cl_attrs(int bytes) {
     set_smem_attr<1, true, R, true>(bytes); set_smem_attr<1, false, R, true>(bytes);
     set_smem_attr<1, true, R, true, true>(bytes);
+    set_smem_attr<1, false, R, true, true>(bytes);
     set_smem_attr<2, true, R, false>(bytes); set_smem_attr<2, false, R, false>(bytes);
     set_smem_attr<4, true, R, false>(bytes); set_smem_attr<4, false, R, false>(bytes);
 }
@@ -717,6 +726,18 @@ int setup(mmas_ctx* h) {
             h->cons_warps = 4;
             h->cons_grid = std::max(1, (h->m_local + 3) / 4);
             h->cons_smem = 128 + 16 + 4 * per_warp;
+            // one inv_w row per block for the R9 fallback scans (construct.cuh stage_fallback_row),
+            // when it leaves room for at least two blocks per SM
+            const size_t off = (h->cons_smem + 127) & ~(size_t)127;
+            const size_t with_row = off + (size_t)round_up(n * 4, 16);
+            // only where inv_w is not L2-resident (C5: its rows come from HBM; C3's L2-resident
+            // rows measured 1.5 % slower with the staging)
+            const bool hbm_rows = 4.0 * (double)n * h->ld > 0.75 * (double)h->l2_bytes ||
+                                  std::getenv("MMAS_FB_ROW") != nullptr;   // (tests force it on small n)
+            if (hbm_rows && 2 * (with_row + 1024) <= (size_t)h->smem_optin && !std::getenv("MMAS_NO_FB_ROW")) {
+                h->fb_row_off = (uint32_t)off;
+                h->cons_smem = with_row;
+            }
         }
     } else if (h->cfg.tabu == MMAS_TABU_COMPACT) {
         // CT entries: n u16 per ant warp, padded to 256 positions (one scan trip)

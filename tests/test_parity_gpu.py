@@ -139,6 +139,18 @@ def test_pruned_fallback_scan_bit_exact():
     assert g.stats()["fallback_steps"] > 100000
 
 
+@pytest.mark.parametrize("m", [40, 2400], ids=["few-warps-uncapped", "16-warps-pruned"])
+def test_staged_fallback_rows_bit_exact(m, monkeypatch):
+    """Fallback scans over an inv_w row staged into the block's shared memory by one TMA copy
+    (construct.cuh stage_fallback_row; on by default only where inv_w is not L2-resident,
+    forced here with MMAS_FB_ROW): L2-table kernel (n = 1300), cl = 4 on a clustered
+    instance, both the low-occupancy (uncapped registers) and the pruned 16-warp variants."""
+    monkeypatch.setenv("MMAS_FB_ROW", "1")
+    c = make_coords("fl3795", 1300, 23)
+    g, o = lockstep(c, m, 4, 2, seed=17)
+    assert g.stats()["fallback_steps"] > 1000
+
+
 def test_fallback_counter_matches_oracle():
     c = make_coords("d198", 198, 198)
     g = mmas.Colony(c, 120, 4, seed=3)
