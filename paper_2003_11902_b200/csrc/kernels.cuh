@@ -298,8 +298,8 @@ struct ConstructArgs {
     int n, ld, cl, ldr;
     int ant_lo, m_local;
     int fallback_argmax;
-    int prune_fallback;
-    uint32_t fb_row_off;         // L2-table kernel: shared-memory offset of the fallback row buffer (0 = none)          // L2-table kernel: pruned (lagged-threshold) fallback scans
+    int prune_fallback;          // L2-table kernel: pruned (lagged-threshold) fallback scans
+    uint32_t fb_row_off;         // L2-table kernel: shared-memory offset of the fallback row buffer (0 = none)
     int warps_per_block;
     uint32_t table_bytes_inv, table_bytes_id;  // smem-table variant: padded table sizes
     uint16_t* __restrict__ routes;          // m_local x ldr
