@@ -234,8 +234,7 @@ __device__ __forceinline__ uint32_t chunk_nibble(const Tabu& tabu, int c0, int n
 // larger, so it prunes less), but the warp reduction after trip i is only needed at trip
 // i + 2, so the trips do not serialise on it.  At a few warps per SM (C5) the branch-free
 // scan is faster (its eight independent log chains per trip are the ILP those warps lack).
-// kRowSmem: `row` is a copy of the inv_w row in shared memory (plain loads, no __ldg)
-template <bool kArgmax, bool kPrefetch = false, bool kLagPrune = false, bool kRowSmem = false, class Tabu>
+template <bool kArgmax, bool kPrefetch = false, bool kLagPrune = false, class Tabu>
 __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, const Tabu& tabu, int n,
                                                uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
                                                int lane, uint32_t& best_mag, uint32_t& best_c) {
@@ -247,13 +246,8 @@ __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, co
         const int ca = base + 4 * lane, cb = ca + 128;
         na = chunk_nibble(tabu, ca, n);
         nb = chunk_nibble(tabu, cb, n);
-        if constexpr (kRowSmem) {
-            iva = na != 0xFu ? reinterpret_cast<const float4*>(row)[ca >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
-            ivb = nb != 0xFu ? reinterpret_cast<const float4*>(row)[cb >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
-        } else {
-            iva = na != 0xFu ? __ldg(reinterpret_cast<const float4*>(row + ca)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            ivb = nb != 0xFu ? __ldg(reinterpret_cast<const float4*>(row + cb)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        iva = na != 0xFu ? __ldg(reinterpret_cast<const float4*>(row + ca)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        ivb = nb != 0xFu ? __ldg(reinterpret_cast<const float4*>(row + cb)) : make_float4(0.f, 0.f, 0.f, 0.f);
     };
     if constexpr (kPrefetch) {
         // the next trip's visited bits and inv_w float4s are loaded one trip ahead
@@ -481,43 +475,95 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
 //   [.., + W * 4*nwords)     tabu words (SmemTabu variant)
 extern __shared__ __align__(128) unsigned char g_smem[];
 
-// ---- fallback row staging (L2-table kernel, C3 / C5) ---------------------------------
-// One inv_w-row buffer per block in shared memory (ConstructArgs::fb_row_off), used by one
-// warp at a time: a warp that falls back (R9) and finds it free takes it (smem flag), copies
-// the row in with one cp.async.bulk, waits on the block's mbarrier (its phase kept next to
-// the flag) and scans from shared memory; a warp that finds it taken scans from global.
-// Layout in the [0, 128) header: mbarrier at 0 (unused by this kernel's table path), flag
-// at 64, phase at 68.
-__device__ __forceinline__ bool stage_fallback_row(const ConstructArgs& A, const float* row, int lane) {
-    uint32_t* flag = reinterpret_cast<uint32_t*>(g_smem + 64);
-    uint32_t* phase = reinterpret_cast<uint32_t*>(g_smem + 68);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
-    uint32_t got = 0, ph = 0;
-    if (lane == 0) {
-        got = atomicCAS(flag, 0u, 1u) == 0u;
-        if (got) {
-            ph = *reinterpret_cast<volatile uint32_t*>(phase);
-            fence_proxy_async_smem();   // earlier generic reads of the buffer before the copy
-            const uint32_t bytes = (uint32_t)(((size_t)A.n * 4 + 15) & ~(size_t)15);
-            mbar_expect_tx(bar, bytes);
-            bulk_g2s(smem_u32(g_smem + A.fb_row_off), row, bytes, bar);
+// Fallback scan over an HBM-resident row (C5), streamed through shared memory: per warp
+// kFbBufs 8 KB chunk buffers (2048 cities = 8 trips) filled by cp.async.bulk, the next
+// chunks in flight while the current one is scanned; chunks whose 2048 cities are all
+// visited are neither copied nor scanned.  Cities are visited in the same order as
+// scan_unvisited (chunks ascending, trips ascending), so the per-lane (key, city) results
+// are identical.  Shared memory: the warp's mbarriers at 8 (kFbBufs warp + b), its phase
+// bits at 96 + 4 warp, its buffers at fb_off + (kFbBufs warp + b) 8 KB (4 warps per block).
+constexpr int kFbChunk = 2048;   // floats per chunk (8 KB)
+constexpr int kFbBufs = 2;       // chunks in flight per warp (3 measured the same on C5)
+template <class Tabu>
+__device__ __forceinline__ void scan_unvisited_staged(const float* __restrict__ row, const Tabu& tabu, int n, int ld,
+                                                      uint32_t fb_off, uint32_t step, uint32_t ant, uint32_t iter,
+                                                      PhiloxKey key, int lane, int warp, uint32_t& best_mag,
+                                                      uint32_t& best_c) {
+    const int nchunks = (n + kFbChunk - 1) / kFbChunk;   // <= 32 (n < 65536)
+    uint32_t need = 0;
+    for (int c = 0; c < nchunks; ++c) {
+        bool full = true;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int wi = c * (kFbChunk / 32) + 2 * lane + k;
+            if (wi * 32 < n) {
+                uint32_t wd = tabu.word(wi);
+                const int rem = n - wi * 32;
+                if (rem < 32) wd |= ~((1u << rem) - 1u);   // cities >= n count as visited
+                full = full && wd == 0xFFFFFFFFu;
+            }
+        }
+        if (!__all_sync(kFull, full)) need |= 1u << c;
+    }
+    uint64_t* bars = reinterpret_cast<uint64_t*>(g_smem) + kFbBufs * warp;
+    uint32_t* phw = reinterpret_cast<uint32_t*>(g_smem + 96) + warp;
+    float* bufs = reinterpret_cast<float*>(g_smem + fb_off) + (size_t)warp * kFbBufs * kFbChunk;
+    uint32_t ph = *reinterpret_cast<volatile uint32_t*>(phw);
+    __syncwarp();
+    auto issue = [&](int c, int b) {
+        if (lane == 0) {
+            fence_proxy_async_smem();   // the buffer's earlier generic reads before the copy
+            const uint32_t bytes = (uint32_t)min(kFbChunk, ld - c * kFbChunk) * 4u;   // ld: multiple of 32
+            mbar_expect_tx(bars + b, bytes);
+            bulk_g2s(smem_u32(bufs + (size_t)b * kFbChunk), row + (size_t)c * kFbChunk, bytes, bars + b);
+        }
+    };
+    int cq[kFbBufs];
+#pragma unroll
+    for (int b = 0; b < kFbBufs; ++b) {
+        cq[b] = -1;
+        if (need) {
+            cq[b] = __ffs(need) - 1;
+            need &= need - 1u;
+            issue(cq[b], b);
         }
     }
-    got = __shfl_sync(kFull, got, 0);
-    if (!got) return false;
-    ph = __shfl_sync(kFull, ph, 0);
-    mbar_wait(bar, ph);
-    return true;
-}
-__device__ __forceinline__ void release_fallback_row(int lane) {
-    __syncwarp();   // every lane is done reading the buffer
-    if (lane == 0) {
-        uint32_t* phase = reinterpret_cast<uint32_t*>(g_smem + 68);
-        *reinterpret_cast<volatile uint32_t*>(phase) ^= 1u;
-        __threadfence_block();
-        atomicExch(reinterpret_cast<uint32_t*>(g_smem + 64), 0u);
+    for (int b = 0;;) {
+        int c = cq[0];
+#pragma unroll
+        for (int k = 1; k < kFbBufs; ++k)
+            if (b == k) c = cq[k];
+        if (c < 0) break;
+        mbar_wait(bars + b, (ph >> b) & 1u);
+        ph ^= 1u << b;
+        const float4* buf = reinterpret_cast<const float4*>(bufs + (size_t)b * kFbChunk);
+        const int end = min(n, (c + 1) * kFbChunk);
+        for (int base = c * kFbChunk; base < end; base += 256) {
+            const int ca = base + 4 * lane, cb = ca + 128;
+            const uint32_t na = chunk_nibble(tabu, ca, n), nb = chunk_nibble(tabu, cb, n);
+            if (!__any_sync(kFull, (na & nb) != 0xFu)) continue;
+            const float4 iva = na != 0xFu ? buf[(ca - c * kFbChunk) >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 ivb = nb != 0xFu ? buf[(cb - c * kFbChunk) >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
+            scan_chunk<false, false>(iva, ca, na, step, ant, iter, key, best_mag, best_c, 0.f);
+            scan_chunk<false, false>(ivb, cb, nb, step, ant, iter, key, best_mag, best_c, 0.f);
+        }
+        __syncwarp();   // every lane is done with this buffer before it is refilled
+        int nc = -1;
+        if (need) {
+            nc = __ffs(need) - 1;
+            need &= need - 1u;
+            issue(nc, b);
+        }
+#pragma unroll
+        for (int k = 0; k < kFbBufs; ++k)
+            if (b == k) cq[k] = nc;
+        b = b + 1 == kFbBufs ? 0 : b + 1;
     }
+    if (lane == 0) *reinterpret_cast<volatile uint32_t*>(phw) = ph;
+    __syncwarp();
 }
+
+
 
 
 // ---------------------------------------------------------------------------
@@ -654,12 +700,9 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
     const uint32_t iter = *A.iter_dev;
     // grid-barrier generation of the fused update: read before this block can arrive
     const uint32_t epoch0 = (kSmemTable && A.fuse_update) ? ld_acquire_gpu(A.epoch) : 0u;
-    if (!kSmemTable && A.fb_row_off) {
-        if (threadIdx.x == 0) {
-            mbar_init(bar, 1);
-            *reinterpret_cast<uint32_t*>(g_smem + 64) = 0u;
-            *reinterpret_cast<uint32_t*>(g_smem + 68) = 0u;
-        }
+    if (!kSmemTable && A.fb_row_off) {   // the fallback chunk pipelines (scan_unvisited_staged)
+        if (threadIdx.x < 4 * kFbBufs) mbar_init(reinterpret_cast<uint64_t*>(g_smem) + threadIdx.x, 1);
+        if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(g_smem + 96)[threadIdx.x] = 0u;
         __syncthreads();
     }
     if (kSmemTable) {
@@ -863,17 +906,9 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
                 uint32_t fm = kNone, fc = kNone;
                 if (A.fallback_argmax)
                     scan_unvisited<true>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm, fc);
-                else if (!kSmemTable && A.fb_row_off && stage_fallback_row(A, row, lane)) {
-                    // the row came into the block's shared buffer by one TMA copy: the scan reads
-                    // it there instead of paying one L2/HBM latency per trip
-                    const float* srow = reinterpret_cast<const float*>(g_smem + A.fb_row_off);
-                    if (A.prune_fallback)
-                        scan_unvisited<false, false, true, true>(srow, tabu, n, (uint32_t)s, ant, iter, A.key, lane,
-                                                                 fm, fc);
-                    else
-                        scan_unvisited<false, false, false, true>(srow, tabu, n, (uint32_t)s, ant, iter, A.key,
-                                                                  lane, fm, fc);
-                    release_fallback_row(lane);
+                else if (!kSmemTable && A.fb_row_off) {
+                    scan_unvisited_staged(row, tabu, n, A.ld, A.fb_row_off, (uint32_t)s, ant, iter, A.key, lane,
+                                          warp, fm, fc);
                 } else if (!kSmemTable && A.prune_fallback)
                     scan_unvisited<false, false, !kSmemTable>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm,
                                                               fc);

@@ -726,10 +726,10 @@ int setup(mmas_ctx* h) {
             h->cons_warps = 4;
             h->cons_grid = std::max(1, (h->m_local + 3) / 4);
             h->cons_smem = 128 + 16 + 4 * per_warp;
-            // one inv_w row per block for the R9 fallback scans (construct.cuh stage_fallback_row),
-            // when it leaves room for at least two blocks per SM
+            // per warp kFbBufs 8 KB chunk buffers for the R9 fallback scans over HBM-resident rows
+            // (construct.cuh scan_unvisited_staged), when they leave room for two blocks per SM
             const size_t off = (h->cons_smem + 127) & ~(size_t)127;
-            const size_t with_row = off + (size_t)round_up(n * 4, 16);
+            const size_t with_row = off + (size_t)h->cons_warps * kFbBufs * 4 * kFbChunk;
             // only where inv_w is not L2-resident (C5: its rows come from HBM; C3's L2-resident
             // rows measured 1.5 % slower with the staging)
             const bool hbm_rows = 4.0 * (double)n * h->ld > 0.75 * (double)h->l2_bytes ||
