@@ -510,6 +510,7 @@ __device__ __forceinline__ void scan_unvisited_staged(const float* __restrict__ 
     float* bufs = reinterpret_cast<float*>(g_smem + fb_off) + (size_t)warp * kFbBufs * kFbChunk;
     uint32_t ph = *reinterpret_cast<volatile uint32_t*>(phw);
     __syncwarp();
+    float thr = warp_threshold(best_mag);
     auto issue = [&](int c, int b) {
         if (lane == 0) {
             fence_proxy_async_smem();   // the buffer's earlier generic reads before the copy
@@ -544,8 +545,9 @@ __device__ __forceinline__ void scan_unvisited_staged(const float* __restrict__ 
             if (!__any_sync(kFull, (na & nb) != 0xFu)) continue;
             const float4 iva = na != 0xFu ? buf[(ca - c * kFbChunk) >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
             const float4 ivb = nb != 0xFu ? buf[(cb - c * kFbChunk) >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
-            scan_chunk<false, false>(iva, ca, na, step, ant, iter, key, best_mag, best_c, 0.f);
-            scan_chunk<false, false>(ivb, cb, nb, step, ant, iter, key, best_mag, best_c, 0.f);
+            scan_chunk<false, true>(iva, ca, na, step, ant, iter, key, best_mag, best_c, thr);
+            scan_chunk<false, true>(ivb, cb, nb, step, ant, iter, key, best_mag, best_c, thr);
+            thr = warp_threshold(best_mag);
         }
         __syncwarp();   // every lane is done with this buffer before it is refilled
         int nc = -1;
