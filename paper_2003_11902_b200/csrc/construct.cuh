@@ -229,19 +229,18 @@ __device__ __forceinline__ uint32_t chunk_nibble(const Tabu& tabu, int c0, int n
 // ---------------------------------------------------------------------------
 // kPrefetch (the full-row path, where the scan is the whole step and 16+ warps per SM hide the
 // serial pruned key chains): next trip loaded one trip ahead + exact pruning of the keys.
-// kLagPrune (candidate-list fallback of the L2-table kernel at high occupancy, C3): pruned
-// keys with the threshold of the trip before last -- still exact (an older threshold is
-// larger, so it prunes less), but the warp reduction after trip i is only needed at trip
-// i + 2, so the trips do not serialise on it.  At a few warps per SM (C5) the branch-free
-// scan is faster (its eight independent log chains per trip are the ILP those warps lack).
-template <bool kArgmax, bool kPrefetch = false, bool kLagPrune = false, class Tabu>
+// kPruneFb (candidate-list fallback of the L2-table kernel at >= 16 ant warps per SM, C3):
+// exact key pruning against the warp's threshold refreshed every trip, per-lane survivor
+// branch (a threshold lagged by a trip, or warp-uniform skipping, measured slower: the
+// other warps hide the reduction).  At a few warps per SM with rows loaded from global the
+// branch-free scan is faster (C5 streams its rows through shared memory instead).
+template <bool kArgmax, bool kPrefetch = false, bool kPruneFb = false, class Tabu>
 __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, const Tabu& tabu, int n,
                                                uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
                                                int lane, uint32_t& best_mag, uint32_t& best_c) {
     // pruning threshold (full-row path only: kPrefetch; unused by the argmax flag)
-    constexpr bool kLag = kLagPrune && !kArgmax && !kPrefetch;
+    constexpr bool kLag = kPruneFb && !kArgmax && !kPrefetch;
     float thr = (kPrefetch || kLag) && !kArgmax ? warp_threshold(best_mag) : 0.f;
-    float thr_next = thr;
     auto load_trip = [&](int base, uint32_t& na, uint32_t& nb, float4& iva, float4& ivb) {
         const int ca = base + 4 * lane, cb = ca + 128;
         na = chunk_nibble(tabu, ca, n);
@@ -277,12 +276,9 @@ __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, co
             load_trip(base, na, nb, iva, ivb);
             if (!__any_sync(kFull, (na & nb) != 0xFu)) continue;
             const int ca = base + 4 * lane;
-            scan_chunk<kArgmax, kLag, true>(iva, ca, na, step, ant, iter, key, best_mag, best_c, thr);
-            scan_chunk<kArgmax, kLag, true>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c, thr);
-            if (kLag) {
-                thr = thr_next;
-                thr_next = warp_threshold(best_mag);
-            }
+            scan_chunk<kArgmax, kLag, false>(iva, ca, na, step, ant, iter, key, best_mag, best_c, thr);
+            scan_chunk<kArgmax, kLag, false>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c, thr);
+            if (kLag) thr = warp_threshold(best_mag);
         }
     }
 }
