@@ -396,13 +396,28 @@ def run_ours(args):
     pinned = torch.from_numpy(coords.copy()).pin_memory().numpy()
     out_steps = args.steps
     best_host = torch.full((out_steps,), -1, dtype=torch.int64).pin_memory()   # per-step results
+
+    def e2e_colony():
+        c = mmas.Colony(pinned, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
+                        separate_update=args.separate_update,
+                        local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection,
+                        stream=stream, rank=rank, world=world)
+        if exchange == "p2p":
+            wire_p2p(c)
+        return c
+
+    # untimed warm-up of the same path (create, a few iterations, read-back, destroy)
+    cw = e2e_colony()
+    for _ in range(min(3, args.warmup)):
+        cw.iterate(1) if world == 1 else (cw.iterate_exchange(1) if exchange == "p2p" else None)
+    cw.sync()
+    cw.close()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    c2 = mmas.Colony(pinned, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
-                     separate_update=args.separate_update,
-                     local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection,
-                     stream=stream, rank=rank, world=world)
-    if exchange == "p2p":
-        wire_p2p(c2)
+    c2 = e2e_colony()
+    t_created = time.perf_counter()
     for k in range(out_steps):
         if world == 1:
             c2.iterate(1)
@@ -420,6 +435,7 @@ def run_ours(args):
         # the step's result (global best length, 8 B) copied to pinned host memory on the
         # stream: no per-step host round trip; the host reads them after the final sync
         c2.best_length_async(best_host.data_ptr() + 8 * k)
+    t_enqueued = time.perf_counter()
     _, final_len = c2.best_tour()
     el = time.perf_counter() - t0
     c2.close()
@@ -431,6 +447,7 @@ def run_ours(args):
         el = float(te.item())
     e2e = {"value": m_total * out_steps / el, "unit": UNIT,
            "h2d_bytes_per_step": 16 * w.n / out_steps, "d2h_bytes_per_step": 8 + 2 * w.n / out_steps,
+           "seconds": {"total": el, "create": t_created - t0, "steps_enqueued": t_enqueued - t_created},
            "note": "timed on every rank, max over ranks: mmas_create from pinned host coords (H2D), per "
                    "step mmas_iterate(1) (N = 1) or mmas_construct + all-gather + mmas_update (N > 1) + "
                    "mmas_best_length_async (8-byte D2H of the step's global best into pinned host memory, "
