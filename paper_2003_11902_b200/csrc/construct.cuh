@@ -368,7 +368,8 @@ __device__ __forceinline__ bool block_finish(const ConstructArgs& A, unsigned lo
         s_best = ~0ull;
         s_fb = 0ull;
     }
-    __threadfence();
+    // (no per-thread fence: the block's route / length writes are ordered before the block
+    // barriers, and thread 0's fence before its arrival is cumulative over them)
     __syncthreads();
     if (lane == 0) {
         atomicMin(&s_best, wbest);
@@ -380,8 +381,9 @@ __device__ __forceinline__ bool block_finish(const ConstructArgs& A, unsigned lo
         if (s_fb) atomicAdd(A.fallback_count, s_fb);
         unsigned last = 0;
         if (A.fuse_select) {
-            __threadfence();
+            __threadfence();   // release: this block's routes / lengths before its arrival
             last = atomicAdd(A.done, 1u) == gridDim.x - 1u;
+            if (last) __threadfence();   // acquire: every block's; bar.sync passes it to the block
         }
         s_last = last;
     }
@@ -389,10 +391,8 @@ __device__ __forceinline__ bool block_finish(const ConstructArgs& A, unsigned lo
     const bool last = s_last != 0u;
     if (last && A.xchg) {
         // world > 1 inside the fused launch: the whole last block publishes, waits, selects
-        __threadfence();
         exchange_select_block(A, lane, warp);
     } else if (last) {
-        __threadfence();
         select_best_block(A.sel);
         if (threadIdx.x == 0) *A.done = 0u;
     }
