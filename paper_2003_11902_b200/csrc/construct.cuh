@@ -328,9 +328,13 @@ __device__ __forceinline__ void exchange_select_block(const ConstructArgs& A, in
         }
         if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned long long*>(rec) = key;
     }
-    __threadfence_system();   // records visible to every peer before any flag
     __syncthreads();
-    if ((int)threadIdx.x < X.world) *(volatile uint32_t*)xflag(X.peers[threadIdx.x], X, (int)X.parity, X.rank) = X.seq;
+    // one system-scope fence (cumulative over the block barrier) by the thread that then
+    // raises the flags: records visible to every peer before any flag
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int p = 0; p < X.world; ++p) *(volatile uint32_t*)xflag(X.peers[p], X, (int)X.parity, X.rank) = X.seq;
+    }
     if (warp == 0) {
         if (lane < X.world) {
             volatile uint32_t* f = xflag(A.xown, X, (int)X.parity, lane);

@@ -377,11 +377,12 @@ __global__ void publish_peers_kernel(unsigned long long* local_key, const uint16
         }
         if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned long long*>(rec) = key;
     }
-    __threadfence_system();   // records visible to every peer before any flag
     __syncthreads();
-    if (threadIdx.x < X.world) {
-        volatile uint32_t* f = xflag(X.peers[threadIdx.x], X, (int)X.parity, X.rank);
-        *f = X.seq;
+    // one system-scope fence (cumulative over the block barrier) by the thread that then
+    // raises the flags: records visible to every peer before any flag
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int p = 0; p < X.world; ++p) *(volatile uint32_t*)xflag(X.peers[p], X, (int)X.parity, X.rank) = X.seq;
     }
     if (threadIdx.x == 0 && m_local > 0) *local_key = ~0ull;
 }
