@@ -96,6 +96,38 @@ def test_choice_info_example():
     assert oracle.heur(0, 2.0) == 1.0          # R11: eta = 1/max(d, 1)
 
 
+def test_pow_alpha_fixed_values():
+    """R17 (integer alpha by repeated multiplication; Eq. (1) P:228-231 raises tau to alpha):
+    with tau a power of two every product is exact, so inv_w = 1/(tau^alpha * eta) has a
+    closed form; an off-by-one in the multiplication loop changes it by a factor tau."""
+    # tau = 0.5, eta = 1: alpha 2 -> 4, alpha 3 -> 8, alpha 8 -> 256
+    assert oracle.inv_w(np.float32(0.5), 1.0, 2) == 4.0
+    assert oracle.inv_w(np.float32(0.5), 1.0, 3) == 8.0
+    assert oracle.inv_w(np.float32(0.5), 1.0, 8) == 256.0
+    # tau = 3 (exact powers 9, 27), eta = 1/4: 1/(9/4) and 1/(27/4) correctly rounded
+    assert oracle.inv_w(np.float32(3.0), 0.25, 2) == np.float32(4.0 / 9.0)
+    assert oracle.inv_w(np.float32(3.0), 0.25, 3) == np.float32(4.0 / 27.0)
+    # a non-representable tau: tau^alpha within 2 ulp (alpha-1 roundings) of the exact power
+    t = np.float32(0.013)
+    for a in (2, 3):
+        exact = 1.0 / (float(t) ** a * 0.5)
+        got = oracle.inv_w(t, 0.5, a)
+        assert abs(got - exact) <= 3 * np.spacing(np.float32(exact)), (a, got, exact)
+
+
+def test_heur_fixed_values_beta_3_and_non_integer():
+    """R18: eta^beta = 1/max(d,1)^beta, integer beta by repeated double
+    multiplication, otherwise libm pow -- closed forms at beta = 3 and beta = 2.5."""
+    assert oracle.heur(10, 3.0) == np.float32(1e-3)
+    assert oracle.heur(7, 3.0) == np.float32(1.0 / 343.0)
+    assert oracle.heur(1000, 3.0) == np.float32(1e-9)
+    assert oracle.heur(4, 2.5) == np.float32(1.0 / 32.0)      # 4^2.5 = 32
+    assert oracle.heur(9, 2.5) == np.float32(1.0 / 243.0)     # 9^2.5 = 243
+    assert oracle.heur(100, 0.5) == np.float32(0.1)           # 100^0.5 = 10
+    assert oracle.heur(16, 1.25) == np.float32(1.0 / 32.0)    # 16^1.25 = 32
+    assert oracle.heur(0, 2.5) == 1.0                         # R11
+
+
 # ---- pheromone update (row a6) --------------------------------------------------
 def test_update_worked_examples():
     n = 5

@@ -115,3 +115,58 @@ def test_rwm_with_candidate_lists_falls_back():
 def test_rejects_bad_selection():
     with pytest.raises(ValueError):
         oracle.Colony(make_coords("uniform", 10, 1), 5, 3, selection=2)
+
+
+def _hillis_steele(s):
+    """The inclusive scan of R28 (pre[t] += pre[t-d], d = 1, 2, 4, 8, 16) in fp32 -- used
+    here only to certify that the input below is adversarial, not to compute a result."""
+    p = s.astype(np.float32).copy()
+    d = 1
+    while d < 32:
+        q = p.copy()
+        q[d:] = p[d:] + p[:-d]
+        p, d = q, 2 * d
+    return p
+
+
+def _adversarial_zero_chunk():
+    """32 one-item chunks, item 4 of weight 0 (a visited node), whose scanned prefix
+    rounds one ulp ABOVE its predecessor's, and a u whose r = fl(u * total) lands exactly
+    on the predecessor's prefix: the rule 'first t with pre[t] > r' alone picks item 4."""
+    rng = np.random.default_rng(0)
+    for _ in range(100000):
+        w = rng.random(32).astype(np.float32)
+        w[4] = np.float32(0.0)
+        p = _hillis_steele(w)
+        if not p[4] > p[3]:
+            continue
+        total = p[31]
+        u0 = np.float32(p[3] / total)
+        for k in range(-64, 65):
+            u = u0
+            for _ in range(abs(k)):
+                u = np.nextafter(u, np.float32(2.0 if k > 0 else -1.0), dtype=np.float32)
+            if np.float32(u * total) == p[3]:
+                return w, u, p
+    raise AssertionError("no adversarial input found")
+
+
+def test_prwm_zero_sum_chunk_never_wins():
+    """Eq. (1): a visited node (weight 0) has probability 0.  With the
+    Hillis-Steele association (R28) a zero-sum chunk's prefix can round above its
+    predecessor's; r on that predecessor's prefix must still not select the zero chunk
+    (this input fails under the rule without the positive-sum test of commit c5400dc)."""
+    w, u, p = _adversarial_zero_chunk()
+    assert p[4] > p[3] and w[4] == 0.0                  # the input is adversarial:
+    r = np.float32(u * p[31])
+    assert next(t for t in range(32) if p[t] > r) == 4   # the prefix rule alone picks item 4
+    got = oracle.prwm(w, float(u))
+    assert got != 4 and w[got] > 0
+    assert got == 5                                      # the next item whose prefix exceeds r
+    # chunked over 64 items (chunk size 2, both items of chunk 4 visited): same story
+    w2 = np.repeat(w, 2) / np.float32(2.0)
+    w2[8:10] = 0.0
+    p2 = _hillis_steele(np.add.reduceat(w2, np.arange(0, 64, 2)))
+    if p2[4] > p2[3]:
+        got2 = oracle.prwm(w2, float(u))
+        assert w2[got2] > 0
