@@ -163,41 +163,6 @@ def test_fallback_counter_matches_oracle():
     assert tot > 0 and g.stats()["fallback_steps"] == tot
 
 
-def test_c2_full_size_iterations_bit_exact():
-    """pr1002-shaped, 1002 ants, cl 32 -- the bench workload, in its launch configuration."""
-    w = CONFIGS["C2"]
-    lockstep(w.coords(), w.n_ants, w.cand_len, 3, seed=w.mmas_seed, rho=w.rho)
-
-
-@pytest.mark.parametrize("cfg,samples", [("C3", 10), ("C4", 4)])
-def test_full_size_sampled_ants(cfg, samples):
-    """C3 (clustered, cl + fallback) and C4 (full row) at full size: iteration 0
-    routes of sampled ants (the oracle computes them one by one), plus properties
-    of every route and of the update that hold at any size."""
-    w = CONFIGS[cfg]
-    c = w.coords()
-    g = mmas.Colony(c, w.n_ants, w.cand_len, seed=w.mmas_seed, rho=w.rho)
-    o = oracle.Colony(c, w.n_ants, w.cand_len, seed=w.mmas_seed, rho=w.rho, nthreads=8)
-    if w.cand_len:
-        assert np.array_equal(g.cand(), o.cand())
-    assert g.limits() == o.limits()
-    g.iterate(1)
-    T, L = g.tours(), g.lengths()
-    rng = np.random.default_rng(0)
-    picks = sorted(set([0, w.n_ants - 1] + list(rng.integers(0, w.n_ants, size=samples))))
-    for a in picks:
-        r, l, _ = o.construct_ant(int(a))
-        assert np.array_equal(T[a], r), f"ant {a}"
-        assert L[a] == l
-    assert np.all(np.sort(T, axis=1) == np.arange(w.n))        # every route a permutation
-    gb, gl = g.best_tour()
-    assert gl == L.min() and oracle.tour_length(c, gb) == gl
-    tmin, tmax = g.limits()
-    assert tmax == np.float32(1.0 / ((1.0 - w.rho) * gl))
-    tau = g.tau()
-    assert tau.min() >= tmin and tau.max() <= tmax
-
-
 # ---- identities of the contract -----------------------------------------------------
 def test_resume_identity():
     """R20: iterate(2); iterate(3) == iterate(5)."""
@@ -227,29 +192,42 @@ def test_split_calls_equal_iterate():
 
 
 @pytest.mark.parametrize("world,m", [(2, 43), (3, 43), (5, 43), (4, 3)])
-def test_sharded_colony_identical_to_single(world, m):
-    """R21: ants sharded over `world` contexts (one GPU here; one per GPU in
-    production) with their records gathered give bit-identical tours and trails;
-    (4, 3) leaves rank 0 without ants (its record never wins)."""
+def test_sharded_colony_equals_oracle(world, m):
+    """R21 / Alg. 1 select_shortest: ants sharded over `world` contexts (one
+    GPU here; one per GPU in production) with their records gathered give the oracle's
+    unsharded colony bit for bit -- every route, length, the global best, limits, tau and
+    inv_w on every replica; (4, 3) leaves rank 0 without ants (its record never wins)."""
     import torch
     c = make_coords("uniform", 140, 12)
     cl = 16
     s = torch.cuda.current_stream().cuda_stream
-    ref = mmas.Colony(c, m, cl, seed=4)
+    o = oracle.Colony(c, m, cl, seed=4)
     shards = [mmas.Colony(c, m, cl, seed=4, stream=s, rank=r, world=world) for r in range(world)]
     rb = shards[0].record_bytes
     recs = torch.zeros(world * rb, dtype=torch.uint8, device="cuda")
-    for _ in range(4):
-        ref.iterate(1)
+    for it in range(4):
+        o.iterate(1)
         for r, sh in enumerate(shards):
             sh.construct(recs.data_ptr() + r * rb)
         for sh in shards:
             sh.update(recs.data_ptr(), world)
-        T = np.concatenate([sh.tours() for sh in shards])
-        assert np.array_equal(T, ref.tours())
-        for sh in shards:
-            assert np.array_equal(sh.tau(), ref.tau())
-            assert sh.best_tour()[1] == ref.best_tour()[1]
+        compare_shards(shards, o, it)
+
+
+def compare_shards(shards, o, it):
+    """Every shard's routes/lengths against the oracle's ants of that shard; every
+    replica's limits, global best, tau and inv_w against the oracle's."""
+    ot, ol = o.tours(), o.lengths()
+    for sh in shards:
+        first, count = sh.shard()
+        assert np.array_equal(sh.tours(), ot[first:first + count]), f"iteration {it}: rank {sh.rank} routes"
+        assert np.array_equal(sh.lengths(), ol[first:first + count]), f"iteration {it}: rank {sh.rank} lengths"
+        assert sh.limits() == o.limits(), f"iteration {it}: rank {sh.rank} limits"
+        gb, gl = sh.best_tour()
+        ob, obl = o.best_tour()
+        assert gl == obl and np.array_equal(gb, ob), f"iteration {it}: rank {sh.rank} global best"
+        assert_matrix(sh.tau(), o.tau(), f"rank {sh.rank} tau after iteration {it}")
+        assert_matrix(sh.inv_w(), o.inv_w(), f"rank {sh.rank} inv_w after iteration {it}")
 
 
 def test_best_tour_before_first_iteration_is_estate():
@@ -350,24 +328,6 @@ def test_two_opt_bit_exact_double_distance_path(shift, scale):
     if scale > 1:
         c[:, 0] += 20000.0
     lockstep(c, 30, 16, 2, seed=5, local_search=True, rho=0.7)
-
-
-def test_c5_sampled_ants_with_two_opt():
-    """d18512-shaped with cl 32 + 2-opt (C5) at full size: iteration-0 routes of sampled
-    ants after local search, computed one by one by the oracle."""
-    w = CONFIGS["C5"]
-    c = w.coords()
-    g = mmas.Colony(c, w.n_ants, w.cand_len, seed=w.mmas_seed, rho=w.rho, local_search=True)
-    o = oracle.Colony(c, w.n_ants, w.cand_len, seed=w.mmas_seed, rho=w.rho, local_search=True, nthreads=8)
-    assert g.limits() == o.limits()
-    g.iterate(1)
-    T, L = g.tours(), g.lengths()
-    for a in (0, 417, w.n_ants - 1):
-        r, l, _ = o.construct_ant(a)
-        assert np.array_equal(T[a], r), f"ant {a}"
-        assert L[a] == l
-    assert np.all(np.sort(T, axis=1) == np.arange(w.n))
-    assert g.stats()["local_search_moves"] > 0
 
 
 # ---- maximum size (u16 ids: n = 65535) --------------------------------------------
