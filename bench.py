@@ -109,21 +109,36 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": sorted(self.reasons)}
 
 
-def ncu_entry(config, kernel):
+def ncu_entry(config, kernel, iteration=None):
     """Per-launch numbers of the committed ncu --set full capture (profiles/ncu_traffic.json,
-    written by scripts/ncu_json.py), or None."""
+    written by scripts/ncu_json.py) of this config and kernel, from the capture whose
+    iteration is nearest `iteration` (keys "C2@10", "C2@400": the fallback rate -- and so the
+    instruction count -- depends on the iteration), else the un-keyed one; (entry, key) or
+    (None, None)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f)[config][kernel]
-    except (OSError, KeyError, ValueError):
-        return None
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None, None
+    keyed = []
+    for k, v in d.items():
+        if k.startswith(config + "@") and isinstance(v, dict) and kernel in v:
+            try:
+                keyed.append((int(k.split("@", 1)[1]), k))
+            except ValueError:
+                pass
+    if keyed and iteration is not None:
+        _, k = min(keyed, key=lambda t: abs(t[0] - iteration))
+        return d[k][kernel], k
+    if config in d and kernel in d[config]:
+        return d[config][kernel], config
+    return None, None
 
 
-def ncu_traffic(config, kernel):
+def ncu_traffic(ent):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) or None."""
-    d = ncu_entry(config, kernel)
-    return None if d is None else d["dram_bytes_read"] + d["dram_bytes_write"]
+    return None if ent is None else ent["dram_bytes_read"] + ent["dram_bytes_write"]
 
 
 # the paper's construction-only numbers for the same instance shape (other hardware: context)
@@ -158,6 +173,21 @@ def algorithmic_bytes_per_tour(w):
     return (w.n - 1) * w.n // 2 * 4
 
 
+def workload_config(w, args, world):
+    """The `config` object of the JSON line -- the workload only, identical for both arms
+    (--impl ours / reference) at the same N; how our arm ran it goes to `run`."""
+    m_total = w.n_ants * world if args.scaling == "weak" else w.n_ants
+    return {"workload": f"{w.name} ({args.config}): n={w.n}, {w.n_ants} ants"
+                        + (" per GPU" if args.scaling == "weak" else " in total")
+                        + (f" per colony x {w.colonies} colonies" if w.colonies > 1 else "")
+                        + f", cl={w.cand_len}, rho={w.rho}, alpha=1, beta=2",
+            "n": w.n, "n_ants": w.n_ants, "global_ants": m_total, "cand_len": w.cand_len, "colonies": w.colonies,
+            "scaling": args.scaling, "tabu": "compact" if w.tabu else "bitmask",
+            "selection": "roulette wheel" if w.selection else "WRS",
+            "local_search": "2-opt" if w.local_search else "none",
+            "l2": "flushed between timed steps (256 MiB write, outside the step events)"}
+
+
 def cpu_baseline_leg(w, budget_s=12.0):
     """The oracle as it stands on this host's cores, bounded to ~budget_s of CPU work."""
     import oracle
@@ -184,24 +214,34 @@ def run_reference(args):
     w = CONFIGS[args.config]
     import oracle
     cores = os.cpu_count() or 1
-    col = oracle.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, nthreads=cores,
-                        local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    m_total = w.n_ants * world if args.scaling == "weak" else w.n_ants
+    # the same colony (all N ranks' ants; k independent colonies seeded seed + c, R29) on the host
+    cols = [oracle.Colony(w.coords(), m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed + c, nthreads=cores,
+                          local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection)
+            for c in range(w.colonies)]
+
+    def step():
+        for col in cols:
+            col.iterate(1)
     for _ in range(args.warmup if args.warmup < 3 else 1):
-        col.iterate(1)
-    # bounded: each step is one full oracle iteration; cap the number of timed steps
+        step()
+    # bounded: each step is one full oracle iteration of every colony; cap the timed steps
     t_probe = time.perf_counter()
-    col.iterate(1)
+    step()
     t_iter = time.perf_counter() - t_probe
     steps = int(max(1, min(args.steps, 90.0 // max(t_iter, 1e-3))))
     t0 = time.perf_counter()
-    col.iterate(steps)
+    for _ in range(steps):
+        step()
     el = time.perf_counter() - t0
-    value = w.n_ants * steps / el
-    sample = f"{steps} of the requested {args.steps} steps (full {w.n_ants}-ant oracle iterations of {w.name})"
+    value = m_total * w.colonies * steps / el
+    sample = (f"{steps} of the requested {args.steps} steps (full {m_total}-ant oracle iterations of {w.name}"
+              + (f", x {w.colonies} colonies" if w.colonies > 1 else "") + ")")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": steps, "warmup": args.warmup, "ms_per_step": el / steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": w.name, "n": w.n, "n_ants": w.n_ants, "cand_len": w.cand_len},
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(w, args, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -229,13 +269,14 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     w = CONFIGS[args.config]
-    m_total = w.n_ants * world                      # weak scaling: n_ants per GPU
+    # weak (default): n_ants per GPU; strong: n_ants in total, split over the ranks (R21)
+    m_total = w.n_ants * world if args.scaling == "weak" else w.n_ants
     coords = w.coords()
     stream = torch.cuda.current_stream().cuda_stream
     col = mmas.Colony(coords, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
                       separate_update=args.separate_update,
                       local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection,
-                      stream=stream, rank=rank, world=world)
+                      stream=stream, rank=rank, world=world, colonies=w.colonies)
     rb = col.record_bytes
     local = torch.zeros(rb, dtype=torch.uint8, device="cuda")
     gathered = torch.zeros(world * rb, dtype=torch.uint8, device="cuda")
@@ -308,24 +349,27 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    tours = m_total * args.steps
+    K = w.colonies                                  # concurrent colonies (R29): K tours per ant slot
+    tours = m_total * K * args.steps
+    mid_iter = args.warmup + args.steps // 2   # the ncu capture nearest the timed window
     value = tours / (total_ms * 1e-3)
 
     # roofline of the dominant kernel (construction), live CUDA-event time on its stream
     cons_ms = phases["construct_ms"] / max(phases["iterations"], 1)
-    bytes_per_launch = algorithmic_bytes_per_tour(w) * col.shard()[1]
+    bytes_per_launch = algorithmic_bytes_per_tour(w) * col.shard()[1] * K
     cons_kernel = ("construct_rwm_kernel" if w.selection else "construct_cl_kernel" if w.cand_len else
                    "construct_ct_kernel" if w.tabu else "construct_full_kernel")
     # world == 1 with the table in shared memory: the update (row a6) runs inside the same
     # launch (construct.cuh fused_update), so that launch also moves the update's 16 n^2 B
     fused = bool(col.stats()["update_fused"]) and (world == 1 or exchange == "p2p")
-    upd_bytes = 16 * w.n * w.n
+    upd_bytes = 16 * w.n * w.n * K
     if fused:
         bytes_per_launch += upd_bytes
     hbm_peak, peak_src = measured_peaks()
     achieved = bytes_per_launch / (cons_ms * 1e-3) / 1e9
+    ent, ent_key = ncu_entry(args.config, cons_kernel, mid_iter)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": ncu_traffic(args.config, cons_kernel),
+                "traffic": ncu_traffic(ent), "ncu_capture": ent_key,
                 "traffic_note": "DRAM bytes per launch (ncu capture, profiles/ncu_traffic.json); with the "
                                 "candidate table in shared memory (C1, C2: TMA-staged once per launch) or "
                                 "L2-resident rows, HBM traffic is far below the algorithmic bytes",
@@ -338,12 +382,12 @@ def run_ours(args):
                         "the issue and chain views below are the ones that bound them (SURVEY 8(d))"}
     # (1b) the on-chip resource the candidate rows actually come from: shared memory (table
     # staged per launch: C1, C2) or L2 (the rest), against the measured read bandwidth
-    pk = onchip_peaks()
+    pk = onchip_peaks() or {}
     if pk:
         smem_table = bool(w.cand_len) and not w.selection and w.n * 32 * 6 <= 200 * 1024
         res = "smem" if smem_table else "l2"
         peak_on = pk["smem_read_gbs" if smem_table else "l2_read_gbs"]
-        cand_bytes = algorithmic_bytes_per_tour(w) * col.shard()[1]
+        cand_bytes = algorithmic_bytes_per_tour(w) * col.shard()[1] * K
         ach_on = cand_bytes / (cons_ms * 1e-3) / 1e9
         roofline["onchip"] = {"resource": res, "achieved": ach_on, "peak": peak_on, "unit": "GB/s",
                               "frac": ach_on / peak_on,
@@ -354,16 +398,27 @@ def run_ours(args):
     # over the live kernel time, against 4 schedulers x SMs x the SM clock sampled during the run
     sm_mhz = clk.summary().get("sm_mhz") or 0.0
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    ent = ncu_entry(args.config, cons_kernel)
+    if ent and ent.get("l2_bytes") is not None:
+        # measured L2 traffic of the same-regime capture over the live kernel time (north_star:
+        # "achieved L2 and HBM GB/s"); the read sectors are the candidate / row loads that miss L1
+        l2_ach = ent["l2_bytes"] / (cons_ms * 1e-3) / 1e9
+        roofline["l2_measured"] = {"bytes_per_launch": ent["l2_bytes"],
+                                   "read_sectors": ent.get("l2_sectors_read"),
+                                   "achieved": l2_ach, "unit": "GB/s",
+                                   "peak": pk.get("l2_read_gbs"),
+                                   "frac": l2_ach / pk["l2_read_gbs"] if pk.get("l2_read_gbs") else None,
+                                   "capture": ent_key,
+                                   "note": "lts__t_bytes.sum of the ncu capture (same config, nearest iteration) / "
+                                           "live kernel time, against the measured L2 read bandwidth"}
     if ent and ent.get("inst_executed") and sm_mhz:
         ach = ent["inst_executed"] / (cons_ms * 1e-3) / 1e9
-        pk = 4 * nsm * sm_mhz * 1e6 / 1e9
-        roofline["issue"] = {"achieved": ach, "peak": pk, "unit": "Ginst/s (warp)", "frac": ach / pk,
-                             "inst_per_launch": ent["inst_executed"],
+        ipk = 4 * nsm * sm_mhz * 1e6 / 1e9
+        roofline["issue"] = {"achieved": ach, "peak": ipk, "unit": "Ginst/s (warp)", "frac": ach / ipk,
+                             "inst_per_launch": ent["inst_executed"], "capture": ent_key,
                              "note": "smsp__inst_executed.sum of one captured launch / live kernel time; "
                                      "peak = 4 issue slots x %d SMs x %.0f MHz" % (nsm, sm_mhz)}
     # (3) chain model: every ant's n-1 dependent steps; time per step of one resident warp
-    warps_per_sm = col.shard()[1] / nsm
+    warps_per_sm = col.shard()[1] * K / nsm
     roofline["chain"] = {"ns_per_step": cons_ms * 1e6 / (w.n - 1),
                          "cycles_per_step": cons_ms * 1e-3 * sm_mhz * 1e6 / (w.n - 1) if sm_mhz else None,
                          "ant_warps_per_sm": warps_per_sm,
@@ -379,7 +434,7 @@ def run_ours(args):
                                "roofline.algorithmic_bytes_per_launch"}
     else:
         update_roof = {"kernel": "pheromone_update_kernel", "kernel_ms": update_ms,
-                       "traffic": ncu_traffic(args.config, "pheromone_update_kernel"),
+                       "traffic": ncu_traffic(ncu_entry(args.config, "pheromone_update_kernel", mid_iter)[0]),
                        "achieved_gbs": upd_bytes / (update_ms * 1e-3) / 1e9,
                        "frac": upd_bytes / (update_ms * 1e-3) / 1e9 / hbm_peak,
                        "algorithmic_bytes_per_launch": upd_bytes}
@@ -401,7 +456,7 @@ def run_ours(args):
         c = mmas.Colony(pinned, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
                         separate_update=args.separate_update,
                         local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection,
-                        stream=stream, rank=rank, world=world)
+                        stream=stream, rank=rank, world=world, colonies=w.colonies)
         if exchange == "p2p":
             wire_p2p(c)
         return c
@@ -445,7 +500,7 @@ def run_ours(args):
         te = torch.tensor([el], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         el = float(te.item())
-    e2e = {"value": m_total * out_steps / el, "unit": UNIT,
+    e2e = {"value": m_total * K * out_steps / el, "unit": UNIT,
            "h2d_bytes_per_step": 16 * w.n / out_steps, "d2h_bytes_per_step": 8 + 2 * w.n / out_steps,
            "seconds": {"total": el, "create": t_created - t0, "steps_enqueued": t_enqueued - t_created},
            "note": "timed on every rank, max over ranks: mmas_create from pinned host coords (H2D), per "
@@ -462,28 +517,23 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"{w.name} ({args.config}): n={w.n}, {w.n_ants} ants per GPU, "
-                                       f"cl={w.cand_len}, rho={w.rho}, alpha=1, beta=2",
-                           "n": w.n, "ants_per_gpu": w.n_ants, "global_ants": m_total, "cand_len": w.cand_len,
-                           "parallelism": f"ant-sharded x{world}" if world > 1 else "single GPU",
-                           "exchange": {"p2p": "peer memory: CUDA IPC buffers, P2P record stores + device flags",
-                                        "collective": f"{backend} all-gather of the records",
-                                        "none": "none (one GPU)"}[exchange],
-                           "l2": "flushed between timed steps (256 MiB write, outside the step events)",
-                           "tabu": "compact" if w.tabu else "bitmask",
-                           "selection": "roulette wheel" if w.selection else "WRS",
-                           "local_search": "2-opt" if w.local_search else "none",
-                           "iteration_launches": "one (construction + selection + update fused)" if fused else
-                                                 "construction (+ selection) then update",
-                           "paper_context": PAPER_CONTEXT.get(args.config, "") + " (other hardware, context only)"},
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": workload_config(w, args, world),
+                "run": {"parallelism": f"ant-sharded x{world}" if world > 1 else "single GPU",
+                        "exchange": {"p2p": "peer memory: CUDA IPC buffers, P2P record stores + device flags",
+                                     "collective": f"{backend} all-gather of the records",
+                                     "none": "none (one GPU)"}[exchange],
+                        "timed_iterations": [args.warmup, args.warmup + args.steps - 1],
+                        "iteration_launches": "one (construction + selection + update fused)" if fused else
+                                              "construction (+ selection) then update",
+                        "paper_context": PAPER_CONTEXT.get(args.config, "") + " (other hardware, context only)"},
                 "roofline": roofline, "update_roofline": update_roof,
                 "phases_ms_per_step": {"construct": cons_ms, "select": phases["select_ms"] / max(phases["iterations"], 1),
                                        "update": update_ms,
                                        "local_search": phases["local_search_ms"] / max(phases["iterations"], 1)},
-                "construction_only_tours_per_s": w.n_ants / (cons_ms * 1e-3),
+                "construction_only_tours_per_s": w.n_ants * K / (cons_ms * 1e-3),
                 "gpu_launches": gpu_launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
-                "fallback_steps_per_tour": col.stats()["fallback_steps"] / max(col.stats()["iterations"], 1) / col.shard()[1],
+                "fallback_steps_per_tour": col.stats()["fallback_steps"] / max(col.stats()["iterations"], 1) / col.shard()[1] / K,
                 "local_search_moves_per_tour": col.stats()["local_search_moves"] / max(col.stats()["iterations"], 1) / col.shard()[1]}
         print(json.dumps(line), flush=True)
     col.close()
@@ -500,6 +550,8 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: n_ants per GPU (default); strong: n_ants in total, split over the GPUs")
     ap.add_argument("--separate-update", action="store_true",
                     help="run the pheromone update as its own kernel (A/B against the fused launch)")
     args = ap.parse_args()

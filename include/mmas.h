@@ -36,8 +36,11 @@ typedef enum mmas_status {
     MMAS_EINVAL = -1, /* invalid argument */
     MMAS_ENOMEM = -2, /* device or host allocation failed */
     MMAS_ECUDA = -3,  /* a CUDA runtime call or kernel failed */
-    MMAS_ENCCL = -4,  /* reserved: collective failure (exchange is done by the caller) */
-    MMAS_ESTATE = -5  /* call not valid in the current state (e.g. no global best yet) */
+    MMAS_ENCCL = -4,  /* reserved (no collective runs inside the library; the caller's all-gather
+                         or the peer-memory exchange below carries row a7) */
+    MMAS_ESTATE = -5, /* call not valid in the current state (e.g. no global best yet) */
+    MMAS_ETIMEDOUT = -6 /* a bounded device-side wait gave up (a peer's exchange flag, or the fused
+                         launch's grid barrier); see mmas_device_status */
 } mmas_status;
 
 enum { MMAS_DEPOSIT_ITERATION_BEST = 0, MMAS_DEPOSIT_GLOBAL_BEST = 1 }; /* Alg.1 l.288 / P:332-333 (R7) */
@@ -54,6 +57,15 @@ enum { MMAS_TABU_BITMASK = 0, MMAS_TABU_COMPACT = 1 };
  * a warp-wide chunked prefix-sum wheel over choice_info = tau^alpha * eta^beta, one
  * uniform per step.  Both follow Eq. (1); they draw different random numbers. */
 enum { MMAS_SELECT_WRS = 0, MMAS_SELECT_RWM = 1 };
+/* Pheromone storage (the paper's O(n^2) pheromone memory limit, P:1945-1947,
+ * and its future work "replacement of the pheromone memory with a more space-efficient
+ * alternative").  DENSE (default): tau, eta^beta and 1/choice_info as n x n fp32
+ * matrices.  LEAN: no n x n matrix -- the candidate trails (n x cl), one background trail that
+ * every never-deposited trail equals, and per row at most 2 (L + 1) other trails
+ * (L = ceil(ln(tau_min/tau_max) / ln rho)); the fallback scans recompute eta^beta from the
+ * coordinates.  Exactly the same results as DENSE (R30).  LEAN needs cand_len >= 1, integer
+ * beta, WRS selection and fallback, colonies <= 1. */
+enum { MMAS_PHEROMONE_DENSE = 0, MMAS_PHEROMONE_LEAN = 1 };
 
 /* Full configuration (mmas_config_init() fills the defaults). */
 typedef struct mmas_config {
@@ -82,6 +94,15 @@ typedef struct mmas_config {
                               0 (default): with world == 1, no local search, cand_len <= 32 and the
                               candidate table in shared memory, the update runs inside the
                               construction launch after a grid barrier (same results bit for bit) */
+    int32_t colonies;      /* k concurrent independent colonies in this context (the
+                              paper's repeated runs P:1143-1145 and colony-size study P:1568-1619).
+                              Colony c is a complete MMAS run of n_ants ants with Philox key
+                              seed + c (R29): its own trails, choice_info, routes, global best and
+                              limits; coordinates, eta^beta and candidate lists are shared.  Every
+                              launch runs all k (grid.y = colony).  0 or 1 = one colony (default);
+                              k > 1 needs world == 1 and mmas_iterate (not the split / exchange
+                              calls).  Introspection reports the colony chosen by mmas_select_colony */
+    int32_t pheromone;     /* MMAS_PHEROMONE_*; default DENSE */
 } mmas_config;
 
 /* Per-context counters (cumulative since create). */
@@ -155,12 +176,17 @@ int mmas_update(mmas_ctx *h, const void *records_dev, int32_t count);
  * shared memory, cand_len <= 32, no local search, ants on this rank): the grid's last block
  * publishes, waits for the peers' flags and selects, then every block updates.  That
  * launch spins on the device until every peer has published, so the ranks' launches must
- * be able to run concurrently (one process per GPU, or separate streams / processes);
- * ranks sharing ONE stream must use the split calls.  The wait is
- * bounded (~2^34 GPU cycles): a lost peer sets an error that mmas_exchange_status(h)
- * reports as MMAS_ENCCL.  Iteration t uses buffer half t & 1, so ranks stay lockstep
- * without further synchronisation.  All calls are asynchronous except the wiring and
- * mmas_exchange_status. */
+ * run concurrently: one process (or context) per GPU.  Ranks that share ONE GPU must use
+ * the split calls (mmas_construct_publish / mmas_update_exchange, or mmas_construct ->
+ * all-gather -> mmas_update): a fused grid holds its SMs while it waits, and two of them
+ * on one device may not both fit.  mmas_exchange_attach enables peer access to every
+ * buffer on another device (MMAS_ECUDA if the devices cannot access each other).
+ * Every device-side wait is bounded (~2^34 GPU cycles): a lost peer sets the context's
+ * error word, the selection and update are skipped from then on (the replica keeps the
+ * trails of the last complete iteration instead of diverging), and mmas_device_status(h) reports
+ * MMAS_ETIMEDOUT.  Iteration t uses buffer half t & 1, so ranks stay lockstep without
+ * further synchronisation.  All calls are asynchronous except the wiring and
+ * mmas_device_status / mmas_exchange_status. */
 int64_t mmas_exchange_bytes(const mmas_ctx *h);
 int mmas_exchange_buffer(mmas_ctx *h, void **buffer_dev);
 int mmas_exchange_ipc_handle(mmas_ctx *h, void *handle_out);
@@ -169,7 +195,13 @@ int mmas_exchange_attach(mmas_ctx *h, void *const *peer_buffers);
 int mmas_construct_publish(mmas_ctx *h);
 int mmas_update_exchange(mmas_ctx *h);
 int mmas_iterate_exchange(mmas_ctx *h, int32_t iters);
-int mmas_exchange_status(mmas_ctx *h);
+int mmas_exchange_status(mmas_ctx *h);   /* = mmas_device_status */
+
+/* Synchronises the context's stream and reports a device-side failure: MMAS_ETIMEDOUT when a
+ * bounded device wait gave up (a peer's exchange flag, or the one-launch iteration's grid
+ * barrier, whose blocks must all be resident at once -- checked at create, see
+ * mmas_stats.update_fused), else MMAS_OK.  The error is sticky. */
+int mmas_device_status(mmas_ctx *h);
 
 /* Synchronises the context's stream and copies the global best route (n city
  * ids, starting at its route[0]) into tour_out (host, n int32, caller-owned).
@@ -191,7 +223,15 @@ int mmas_best_length_async(mmas_ctx *h, int64_t *host_dst);
 /* Frees every device and host resource.  NULL is a no-op. */
 void mmas_destroy(mmas_ctx *h);
 
-/* ---- introspection (synchronous; caller-allocated host buffers) ---- */
+/* ---- introspection (synchronous; caller-allocated host buffers) ----
+ * With the LEAN pheromone, get_pheromone / get_inv_w / get_heuristic expand the dense n x n
+ * view on the host (small n only).  With colonies > 1 the calls below (and mmas_best_tour / mmas_best_length[_async]) report
+ * colony `colony` of mmas_select_colony (default 0; MMAS_EINVAL if out of range). */
+int mmas_select_colony(mmas_ctx *h, int32_t colony);
+int32_t mmas_colonies(const mmas_ctx *h);
+/* Device bytes of the pheromone state (trails, eta^beta, 1/choice_info, candidate and sparse
+ * tables) of every colony. */
+int64_t mmas_pheromone_bytes(const mmas_ctx *h);
 int32_t mmas_n(const mmas_ctx *h);
 int32_t mmas_iteration(const mmas_ctx *h);
 /* last iteration's routes of this shard: out has ants_local*n int32 */

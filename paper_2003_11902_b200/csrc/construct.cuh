@@ -56,6 +56,10 @@ struct RegTabuX {
         if (!kLazyW && lane == (int)(c >> 5)) w |= 1u << (c & 31);
         if (lane == (int)(c & 31)) wt |= 1u << (c >> 5);
     }
+    __device__ __forceinline__ void unmark(uint32_t c, int lane) {
+        if (!kLazyW && lane == (int)(c >> 5)) w &= ~(1u << (c & 31));
+        if (lane == (int)(c & 31)) wt &= ~(1u << (c >> 5));
+    }
     __device__ __forceinline__ void prepare(int lane) {
         if (kLazyW) w = warp_transpose32(wt, lane);
     }
@@ -82,6 +86,9 @@ struct SmemTabu {
     __device__ __forceinline__ uint32_t top_bit(uint32_t c) const { return t[c >> 5] << (~c & 31u); }
     __device__ __forceinline__ void mark(uint32_t c, int lane) {
         if (lane == 0) t[c >> 5] |= 1u << (c & 31);
+    }
+    __device__ __forceinline__ void unmark(uint32_t c, int lane) {
+        if (lane == 0) t[c >> 5] &= ~(1u << (c & 31));
     }
     __device__ __forceinline__ void prepare(int) {}
     __device__ __forceinline__ void sync() { __syncwarp(); }
@@ -283,6 +290,75 @@ __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, co
     }
 }
 
+// Fallback WRS over all unvisited cities (row a3, R9) with the memory-lean pheromone (R30):
+// row cur of inv_w is not stored.  A city off the row's sparse list has the background trail
+// b, so its 1 / choice_info is 1 / (b^alpha eta^beta) with eta^beta recomputed from the
+// coordinates (heur_edge: the exact value the dense heuristic matrix holds); the few sparse
+// trails carry their own.  The sparse cities are hidden from the background scan through the
+// tabu (marked, scanned, unmarked), then evaluated with their stored values; every city draws
+// the uniform of the dense scan (R13), so the argmax -- ties to the lowest id -- is the dense one.
+template <class Tabu>
+__device__ __forceinline__ uint32_t lean_fallback(const LeanArgs& Ln, const double2* __restrict__ xy, int cur,
+                                                  Tabu& tabu, int n, int alpha, uint32_t step,
+                                                  uint32_t ant, uint32_t iter, PhiloxKey key, int lane) {
+    const float b = __ldcg(Ln.bg + Ln.parity);   // the background trail after the last update
+    const uint16_t* ids = Ln.sp_id + (size_t)cur * Ln.cap;
+    const float* invs = Ln.sp_inv + (size_t)cur * Ln.cap;
+    // 1. hide the row's unvisited sparse cities (warp-collective marks, one city at a time);
+    //    bit r of `hid`: this lane's slot r * 32 + lane was hidden
+    uint32_t hid = 0;
+    tabu.prepare(lane);
+    for (int r = 0; r * 32 < Ln.cap; ++r) {
+        const uint32_t j = ids[r * 32 + lane];
+        const uint32_t jc = j < (uint32_t)n ? j : 0u;
+        const bool unvisited = !tabu.visited(jc);   // all lanes (the register tabu shuffles)
+        const bool hide = j < (uint32_t)n && unvisited;
+        if (hide) hid |= 1u << r;
+        for (unsigned m = __ballot_sync(kFull, hide); m; m &= m - 1u) {
+            const uint32_t jj = __shfl_sync(kFull, j, __ffs(m) - 1);
+            tabu.mark(jj, lane);
+        }
+        tabu.sync();
+    }
+    tabu.prepare(lane);
+    // 2. background scan: lane l takes the 4-city groups 128t + 4l (one Philox per group)
+    const double2 xc = __ldg(xy + cur);
+    const float ba = pow_alpha(b, alpha);
+    uint32_t bm = kNone, bc = kNone;
+    for (int base = 0; base < n; base += 128) {
+        const int c0 = base + 4 * lane;
+        const uint32_t nib = chunk_nibble(tabu, c0, n);
+        if (!__any_sync(kFull, nib != 0xFu)) continue;
+        const uint4 x = philox4x32_10(ctr_city((uint32_t)c0 >> 2, step, ant, iter), key);
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if ((nib >> q) & 1u) continue;
+            const float h = heur_edge(xc, __ldg(xy + c0 + q), Ln.beta);
+            const float iv = __fdiv_rn(1.0f, __fmul_rn(ba, h));   // = inv_weight(b, h, alpha)
+            const uint32_t mag = key_magnitude(__fmul_rn(det_log2(uniform_open(xs[q])), iv));
+            if (mag < bm) { bm = mag; bc = (uint32_t)(c0 + q); }   // ascending cities: ties keep the lower
+        }
+    }
+    // 3. unhide the hidden ones and evaluate them with their stored 1 / choice_info
+    for (int r = 0; r * 32 < Ln.cap; ++r) {
+        const uint32_t j = ids[r * 32 + lane];
+        const bool h = (hid >> r) & 1u;
+        if (h) {
+            const uint4 x = philox4x32_10(ctr_city(j >> 2, step, ant, iter), key);
+            const uint32_t w = (j & 3u) == 0 ? x.x : (j & 3u) == 1 ? x.y : (j & 3u) == 2 ? x.z : x.w;
+            const uint32_t mag = key_magnitude(__fmul_rn(det_log2(uniform_open(w)), invs[r * 32 + lane]));
+            if (mag < bm || (mag == bm && j < bc)) { bm = mag; bc = j; }
+        }
+        for (unsigned m = __ballot_sync(kFull, h); m; m &= m - 1u) {
+            const uint32_t jj = __shfl_sync(kFull, j, __ffs(m) - 1);
+            tabu.unmark(jj, lane);
+        }
+        tabu.sync();
+    }
+    return warp_select(bm, bc);
+}
+
 template <bool kArgmax, class Tabu>
 __device__ __noinline__ uint32_t fallback_select(const float* __restrict__ row, const Tabu tabu, int n,
                                                  uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
@@ -294,7 +370,7 @@ __device__ __noinline__ uint32_t fallback_select(const float* __restrict__ row, 
 
 // ---- per-ant epilogue: tour length (int64) + local iteration-best key (row a5) ----
 __device__ __forceinline__ unsigned long long finish_ant(const ConstructArgs& A, const uint16_t* route, int al,
-                                                         uint32_t ant, int lane) {
+                                                         uint32_t ant, int lane, long long* lengths = nullptr) {
     long long len = 0;
 #pragma unroll 4
     for (int k = lane; k < A.n; k += 32) {
@@ -304,7 +380,7 @@ __device__ __forceinline__ unsigned long long finish_ant(const ConstructArgs& A,
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(kFull, len, o);
-    if (lane == 0) A.lengths[al] = len;
+    if (lane == 0) (lengths ? lengths : A.lengths)[al] = len;
     return ((unsigned long long)len << 24) | ant;   // iteration-best key (R8)
 }
 
@@ -313,7 +389,7 @@ __device__ __forceinline__ unsigned long long finish_ant(const ConstructArgs& A,
 // of the split path -- this shard's best record (key, route) into slot `rank` of every
 // peer's buffer, a system-wide fence, the flags; then a bounded wait for every peer's flag
 // of this iteration and the selection over the gathered records (the local key reset).
-__device__ __forceinline__ void exchange_select_block(const ConstructArgs& A, int lane, int warp) {
+__device__ __forceinline__ bool exchange_select_block(const ConstructArgs& A, int lane, int warp) {
     const ExchangeArgs& X = A.X;
     __shared__ unsigned long long s_key;
     if (threadIdx.x == 0) s_key = A.m_local > 0 ? __ldcg(A.best_key) : ~0ull;   // an empty shard never wins
@@ -335,29 +411,40 @@ __device__ __forceinline__ void exchange_select_block(const ConstructArgs& A, in
         __threadfence_system();
         for (int p = 0; p < X.world; ++p) *(volatile uint32_t*)xflag(X.peers[p], X, (int)X.parity, X.rank) = X.seq;
     }
+    __shared__ unsigned s_lost;
     if (warp == 0) {
+        bool lost = false;
         if (lane < X.world) {
-            volatile uint32_t* f = xflag(A.xown, X, (int)X.parity, lane);
+            // the flags are written by other devices: acquire at system scope (pairs with the
+            // writer's __threadfence_system before its flag store)
+            const uint32_t* f = xflag(A.xown, X, (int)X.parity, lane);
             const long long t0 = clock64();
-            while (*f != X.seq) {
-                if (clock64() - t0 > (1ll << 34)) {
-                    atomicExch(A.xerr, 1u);
+            while (ld_acquire_sys(f) != X.seq) {
+                if (clock64() - t0 > X.spin_bound) {
+                    atomicOr(A.xerr, kErrPeerTimeout);
+                    lost = true;
                     break;
                 }
                 __nanosleep(200);
             }
         }
-        __syncwarp();
-        __threadfence();
-        SelectArgs S = A.sel;
-        S.records = A.xown + (size_t)X.parity * X.world * X.rec_bytes;
-        S.count = X.world;
-        select_best_warp(S, lane);
+        lost = __any_sync(kFull, lost) || ld_volatile_u32(A.xerr) != 0u;
+        __threadfence_system();
+        // a lost peer: no selection over stale records (and no update, see fused_update)
+        if (!lost) {
+            SelectArgs S = A.sel;
+            S.records = A.xown + (size_t)X.parity * X.world * X.rec_bytes;
+            S.count = X.world;
+            select_best_warp(S, lane);
+        }
         if (lane == 0) {
             *A.done = 0u;
             if (A.m_local > 0) *A.best_key = ~0ull;
+            s_lost = lost;
         }
     }
+    __syncthreads();
+    return s_lost != 0u;
 }
 
 // Block epilogue: the block's best key and fallback count reach global memory with
@@ -365,7 +452,7 @@ __device__ __forceinline__ void exchange_select_block(const ConstructArgs& A, in
 // up at the end of the launch).  world == 1: the last block to finish selects the
 // iteration best with one warp (row a5; all route writes are fenced first).
 __device__ __forceinline__ bool block_finish(const ConstructArgs& A, unsigned long long wbest, long long wfb,
-                                             int lane, int warp) {
+                                             int lane, int warp, bool* aborted = nullptr) {
     __shared__ unsigned long long s_best, s_fb;
     __shared__ unsigned s_last;
     if (threadIdx.x == 0) {
@@ -393,9 +480,11 @@ __device__ __forceinline__ bool block_finish(const ConstructArgs& A, unsigned lo
     }
     __syncthreads();
     const bool last = s_last != 0u;
+    if (aborted) *aborted = false;
     if (last && A.xchg) {
         // world > 1 inside the fused launch: the whole last block publishes, waits, selects
-        exchange_select_block(A, lane, warp);
+        const bool lost = exchange_select_block(A, lane, warp);
+        if (aborted) *aborted = lost;
     } else if (last) {
         select_best_block(A.sel);
         if (threadIdx.x == 0) *A.done = 0u;
@@ -446,6 +535,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
             : "r"(smem_u32(bar)), "r"(phase)
             : "memory");
     }
+}
+
+// L2 prefetch of a global range (cp.async.bulk.prefetch.L2; no completion to wait for)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// this block's 1/gridDim share of [base, base + bytes) (16-byte granules), 32 KB per request
+__device__ __forceinline__ void prefetch_l2_share(const void* base, unsigned long long bytes) {
+    const unsigned long long granules = bytes >> 4;
+    const unsigned long long per = (granules + gridDim.x - 1) / gridDim.x;
+    const unsigned long long g0 = per * blockIdx.x, g1 = min(granules, g0 + per);
+    for (unsigned long long g = g0; g < g1; g += 2048)
+        prefetch_l2_bulk(reinterpret_cast<const unsigned char*>(base) + (g << 4),
+                         (uint32_t)(min(g1 - g, 2048ull) << 4));
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -582,8 +685,8 @@ __device__ __forceinline__ void scan_unvisited_staged(const float* __restrict__ 
 // Removes the update launch and its ramp from the iteration.
 // Shared memory: [128 + 8w) mbarrier of warp w, [256 + 2w rowbytes) its tau / heur rows.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void fused_update(const UpdateArgs U, unsigned int* epoch, bool last_block, uint32_t epoch0,
-                                          int lane, int warp) {
+__device__ __noinline__ void fused_update(const UpdateArgs U, unsigned int* epoch, bool last_block, bool abort,
+                                          uint32_t epoch0, int lane, int warp) {
     const int wpb = (int)(blockDim.x >> 5);
     const int tw = (int)gridDim.x * wpb;
     const uint32_t rowbytes = (uint32_t)U.ld * 4u;
@@ -607,16 +710,37 @@ __device__ __noinline__ void fused_update(const UpdateArgs U, unsigned int* epoc
         fetch(i);
         if (lane < U.cl) cid = __ldg(U.cand_id + (size_t)i * U.cl + lane);
     }
-    // grid barrier (all blocks are resident: grid <= SMs, one block each)
+    // grid barrier (all blocks resident: grid <= SMs, one block each, checked at create).
+    // Bounded: a barrier that does not release within spin_bound cycles sets the error word
+    // and the block skips the update; the last block releases with the abort bit when its
+    // exchange lost a peer (the bit stays set in the epoch word: later launches skip too).
+    __shared__ unsigned s_abort;
     __syncthreads();   // the last block's selection warp is done
     if (threadIdx.x == 0) {
         if (last_block) {
             __threadfence();
-            atomicAdd(epoch, 1u);
+            atomicAdd(epoch, abort && !(epoch0 & kEpochAbort) ? kEpochAbort + 1u : 1u);
         }
-        while (ld_acquire_gpu(epoch) == epoch0) __nanosleep(32);
+        uint32_t v;
+        const long long t0 = clock64();
+        bool timeout = false;
+        while ((v = ld_acquire_gpu(epoch)) == epoch0) {
+            if (clock64() - t0 > U.spin_bound) {
+                atomicOr(U.err, kErrGridBarrier);
+                timeout = true;
+                break;
+            }
+            __nanosleep(32);
+        }
+        s_abort = timeout || (v & kEpochAbort) != 0u;
     }
     __syncthreads();
+    if (s_abort) {
+        // drain this warp's row prefetch before the shared memory goes away
+        if (i < U.n) mbar_wait(bar, 0);
+        if (blockIdx.x == 0 && threadIdx.x == 0) *U.iter_dev += 1u;
+        return;
+    }
     trace_mark(4);
     const float tmin = __ldcg(U.scal), tmax = __ldcg(U.scal + 1), delta = __ldcg(U.scal + 2);
     const int n4 = (U.n + 3) >> 2;
@@ -661,7 +785,14 @@ template <int kSlots, bool kSmemTable, bool kRegTabu, bool kFull32, bool kWide =
 // colony fills the SMs (C3's 3795 ants: 25 warps per SM); with kWide (few ant warps per SM,
 // C5) the register budget is left to the compiler
 __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmemTable || kWide) ? 1 : 4)
-    construct_cl_kernel(ConstructArgs A) {
+    construct_cl_kernel(const ConstructArgs A) {
+    // colony (grid.y, R29): its per-colony pointers as locals (a modified copy of the whole
+    // argument struct would live in registers through the step loop); the tail takes a copy
+    const int col = (int)blockIdx.y;
+    const float* __restrict__ c_inv_w = A.inv_w + col * A.cs.nn;
+    const float* __restrict__ c_cand_inv = A.cand_inv + col * A.cs.cand;
+    uint16_t* __restrict__ c_routes = A.routes + col * A.cs.routes;
+    const PhiloxKey c_key = col ? colony_key(A.key, (uint32_t)col) : A.key;
     pdl_wait();
     trace_mark(0);
     static_assert(!kFull32 || kSlots == 1, "kFull32: cl == 32, one slot per lane");
@@ -681,7 +812,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
             constexpr uint32_t kChunk = 32768;
             const uint32_t s_base = smem_u32(g_smem);
             for (uint32_t off = 0; off < A.table_bytes_inv; off += kChunk)
-                bulk_g2s(s_base + 128u + off, reinterpret_cast<const unsigned char*>(A.cand_inv) + off,
+                bulk_g2s(s_base + 128u + off, reinterpret_cast<const unsigned char*>(c_cand_inv) + off,
                          min(kChunk, A.table_bytes_inv - off), bar);
             for (uint32_t off = 0; off < A.table_bytes_id; off += kChunk)
                 bulk_g2s(s_base + 128u + A.table_bytes_inv + off,
@@ -689,19 +820,20 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
                          min(kChunk, A.table_bytes_id - off), bar);
         }
     }
+    if (threadIdx.x == 0 && A.l2_prefetch_bytes) prefetch_l2_share(c_inv_w, A.l2_prefetch_bytes);
     // 32-bit shared-window addresses of the two tables (plain LDS with a register address)
     uint32_t s_inv = smem_u32(g_smem) + 128u;
     uint32_t s_id = s_inv + A.table_bytes_inv;
     // opaque: keep the addresses in registers (otherwise ptxas re-derives the shared
     // window base with a long-latency S2UR SR_CgaCtaId inside every step)
     asm volatile("" : "+r"(s_inv), "+r"(s_id));
-    const RoundKeys rk(A.key);
+    const RoundKeys rk(c_key);
     const uint32_t id_lane = s_id + 2u * (uint32_t)lane;     // kFull32: slot = lane
     const uint32_t inv_lane = s_inv + 4u * (uint32_t)lane;
     uint32_t* tabu_base = reinterpret_cast<uint32_t*>(g_smem + tab_off) + warp * nwords;
-    const uint32_t iter = *A.iter_dev;
+    const uint32_t iter = A.iter_dev[col];
     // grid-barrier generation of the fused update: read before this block can arrive
-    const uint32_t epoch0 = (kSmemTable && A.fuse_update) ? ld_acquire_gpu(A.epoch) : 0u;
+    const uint32_t epoch0 = (kSmemTable && A.fuse_update) ? ld_acquire_gpu(A.epoch + 2 * col) : 0u;
     if (!kSmemTable && A.fb_row_off) {   // the fallback chunk pipelines (scan_unvisited_staged)
         if (threadIdx.x < 4 * kFbBufs) mbar_init(reinterpret_cast<uint64_t*>(g_smem) + threadIdx.x, 1);
         if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(g_smem + 96)[threadIdx.x] = 0u;
@@ -720,10 +852,10 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
         Tabu tabu;
         tabu.init(tabu_base, nwords, lane);
         // Alg. 1: start node u ~ U{0, n-1} (R13)
-        const uint32_t start = __umulhi(philox4x32_10(ctr_start(ant, iter), A.key).x, (uint32_t)n);
+        const uint32_t start = __umulhi(philox4x32_10(ctr_start(ant, iter), c_key).x, (uint32_t)n);
         tabu.mark(start, lane);
         tabu.sync();
-        uint16_t* route = A.routes + (size_t)al * A.ldr;
+        uint16_t* route = c_routes + (size_t)al * A.ldr;
         uint32_t stage = (lane == 0) ? start : 0u;
         uint32_t cur = start;
         long long fb = 0;
@@ -732,7 +864,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
         float L[kSlots][4];
 #pragma unroll
         for (int q = 0; q < kSlots; ++q) {
-            const uint4 x = philox4x32_10(ctr_slot((uint32_t)(lane + 32 * q), 0u, ant, iter), A.key);
+            const uint4 x = philox4x32_10(ctr_slot((uint32_t)(lane + 32 * q), 0u, ant, iter), c_key);
             L[q][0] = det_log2(uniform_open(x.x));
             L[q][1] = det_log2(uniform_open(x.y));
             L[q][2] = det_log2(uniform_open(x.z));
@@ -816,7 +948,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
                     iv = lds_f32(inv_lane + cur * 128u);
                 } else {
                     c = __ldg(A.cand_id + cur * 32u + lane);
-                    iv = __ldg(A.cand_inv + cur * 32u + lane);
+                    iv = __ldg(c_cand_inv + cur * 32u + lane);
                 }
                 hook_a();
                 const uint32_t t = tabu.top_bit(c);
@@ -839,7 +971,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
                         iv = lds_f32(s_inv + 4u * (uint32_t)idx);
                     } else {
                         c = __ldg(A.cand_id + idx);
-                        iv = __ldg(A.cand_inv + idx);
+                        iv = __ldg(c_cand_inv + idx);
                     }
                     const bool vis = tabu.visited(has ? c : cur);
                     const uint32_t mag = vis ? 0x80000000u : key_magnitude(__fmul_rn(Lv[q], iv));
@@ -874,7 +1006,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
         };
         // SPECULATIVE step (register tabu): commits its argmax unconditionally and reports
         // whether every candidate was visited (the caller then rolls the group back)
-        auto spec_step = [&](auto J, int s) -> bool {
+        auto spec_step = [&](auto J, int s, uint32_t& taken) -> bool {
             constexpr int j = decltype(J)::value;
             float Lv[kSlots];
 #pragma unroll
@@ -889,6 +1021,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
             // id < n even when best >= 2^31 (then it is undone by the caller)
             __builtin_assume(nxt < 65536u);
             commit(nxt, s);
+            taken = nxt;
             return best >= 0x80000000u;
         };
         // GENERIC step (runtime j): guards, and the R9 fallback (row a3) inlined ONCE
@@ -903,20 +1036,28 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
             uint32_t nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
             if (best >= 0x80000000u) {   // every candidate visited: R9 fallback
                 ++fb;
+                const long long t_fb = trace_clock();
                 tabu.prepare(lane);
-                const float* row = A.inv_w + (size_t)cur * A.ld;
+                const float* row = c_inv_w + (size_t)cur * A.ld;
                 uint32_t fm = kNone, fc = kNone;
+                if (A.lean.cand_tau) {
+                    // memory-lean pheromone (R30): no inv_w row; the scan recomputes it
+                    commit(lean_fallback(A.lean, A.xy, (int)cur, tabu, n, A.alpha, (uint32_t)s, ant, iter, c_key, lane),
+                           s);
+                    return;
+                }
                 if (A.fallback_argmax)
-                    scan_unvisited<true>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm, fc);
+                    scan_unvisited<true>(row, tabu, n, (uint32_t)s, ant, iter, c_key, lane, fm, fc);
                 else if (!kSmemTable && A.fb_row_off) {
-                    scan_unvisited_staged(row, tabu, n, A.ld, A.fb_row_off, (uint32_t)s, ant, iter, A.key, lane,
+                    scan_unvisited_staged(row, tabu, n, A.ld, A.fb_row_off, (uint32_t)s, ant, iter, c_key, lane,
                                           warp, fm, fc);
                 } else if (!kSmemTable && A.prune_fallback)
-                    scan_unvisited<false, false, !kSmemTable>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm,
+                    scan_unvisited<false, false, !kSmemTable>(row, tabu, n, (uint32_t)s, ant, iter, c_key, lane, fm,
                                                               fc);
                 else
-                    scan_unvisited<false>(row, tabu, n, (uint32_t)s, ant, iter, A.key, lane, fm, fc);
+                    scan_unvisited<false>(row, tabu, n, (uint32_t)s, ant, iter, c_key, lane, fm, fc);
                 nxt = warp_select(fm, fc);
+                trace_fallback(t_fb, lane);
             }
             commit(nxt, s);
         };
@@ -954,14 +1095,19 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
                     // SPECULATIVE group: the four steps run as one straight-line block (no
                     // branch between them, so the scheduler can overlap one step's random-key
                     // slices with the next step's chain); a step that needed the fallback is
-                    // detected once at the end and the whole group is rolled back (tabu word,
-                    // current city, route staging) and redone by the generic path
-                    const uint32_t w0 = tabu.w, wt0 = tabu.wt, cur0 = cur, stage0 = stage;
-                    bool hit = spec_step(I0{}, 4 * g + 0);
-                    hit |= spec_step(I1{}, 4 * g + 1);
-                    hit |= spec_step(I2{}, 4 * g + 2);
-                    hit |= spec_step(I3{}, 4 * g + 3);
-                    if (__builtin_expect(!hit, 1)) {
+                    // detected once at the end.  The group is then rolled back to the state
+                    // before its FIRST such step jf (tabu: the group's entry words with the steps
+                    // before jf re-marked; current city: step jf-1's choice) and the generic path
+                    // redoes steps jf..3.  (A hit step's choice is a visited city, so its mark
+                    // changed nothing; the route staging of steps >= jf is overwritten by the
+                    // redo before the next segment store.)
+                    const uint32_t w0 = tabu.w, wt0 = tabu.wt, cur0 = cur;
+                    uint32_t t0, t1, t2, t3;
+                    const bool h0 = spec_step(I0{}, 4 * g + 0, t0);
+                    const bool h1 = spec_step(I1{}, 4 * g + 1, t1);
+                    const bool h2 = spec_step(I2{}, 4 * g + 2, t2);
+                    const bool h3 = spec_step(I3{}, 4 * g + 3, t3);
+                    if (__builtin_expect(!(h0 | h1 | h2 | h3), 1)) {
                         rotate();
                         ++g;
                         continue;
@@ -969,7 +1115,22 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
                     tabu.w = w0;
                     tabu.wt = wt0;
                     cur = cur0;
-                    stage = stage0;
+                    if (!h0) {
+                        tabu.mark(t0, lane);
+                        cur = t0;
+                        j0 = 1;
+                        if (!h1) {
+                            tabu.mark(t1, lane);
+                            cur = t1;
+                            j0 = 2;
+                            if (!h2) {
+                                tabu.mark(t2, lane);
+                                cur = t2;
+                                j0 = 3;
+                            }
+                        }
+                    }
+                    (void)t3;
                     sliced_all = true;   // every slice of this group already ran
                 } else {
                     int jf = -1;
@@ -997,15 +1158,18 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
         }
         flush_route(route, n, lane, stage);
         __syncwarp();
-        if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane));
+        if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane, A.lengths + (long long)col * A.cs.ants));
         wfb += fb;
     }
     pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
     trace_mark(2);
-    const bool last = block_finish(A, wbest, wfb, lane, warp);
+    ConstructArgs At = A;
+    if (col) colony_offset(At, col);
+    bool aborted;
+    const bool last = block_finish(At, wbest, wfb, lane, warp, &aborted);
     trace_mark(3);
     if constexpr (kSmemTable) {
-        if (A.fuse_update) fused_update(A.upd, A.epoch, last, epoch0, lane, warp);
+        if (At.fuse_update) fused_update(At.upd, At.epoch, last, aborted, epoch0, lane, warp);
     }
     trace_mark(5);
 }
@@ -1015,7 +1179,12 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
 // every step scans all unvisited cities (Alg. 3 over the whole row).
 // ---------------------------------------------------------------------------
 template <bool kRegTabu>
-__global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
+__global__ void __launch_bounds__(128) construct_full_kernel(const ConstructArgs A) {
+    // colony (grid.y, R29): per-colony pointers as locals, a colony copy for the tail
+    const int col = (int)blockIdx.y;
+    const float* __restrict__ c_inv_w = A.inv_w + col * A.cs.nn;
+    uint16_t* __restrict__ c_routes = A.routes + col * A.cs.routes;
+    const PhiloxKey c_key = col ? colony_key(A.key, (uint32_t)col) : A.key;
     pdl_wait();
     using Tabu = typename std::conditional<kRegTabu, RegTabu, SmemTabu>::type;
     const int lane = threadIdx.x & 31;
@@ -1023,22 +1192,22 @@ __global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
     const int n = A.n;
     const int nwords = (((n + 31) >> 5) + 3) & ~3;
     uint32_t* tabu_base = reinterpret_cast<uint32_t*>(g_smem + 128) + warp * nwords;
-    const uint32_t iter = *A.iter_dev;
+    const uint32_t iter = A.iter_dev[col];
     unsigned long long wbest = ~0ull;
 
     for (int al = blockIdx.x * A.warps_per_block + warp; al < A.m_local; al += gridDim.x * A.warps_per_block) {
         const uint32_t ant = (uint32_t)(A.ant_lo + al);
         Tabu tabu;
         tabu.init(tabu_base, nwords, lane);
-        const uint32_t start = __umulhi(philox4x32_10(ctr_start(ant, iter), A.key).x, (uint32_t)n);
+        const uint32_t start = __umulhi(philox4x32_10(ctr_start(ant, iter), c_key).x, (uint32_t)n);
         tabu.mark(start, lane);
         tabu.sync();
-        uint16_t* route = A.routes + (size_t)al * A.ldr;
+        uint16_t* route = c_routes + (size_t)al * A.ldr;
         uint32_t stage = (lane == 0) ? start : 0u;
         uint32_t cur = start;
         for (int s = 1; s < n; ++s) {
             uint32_t bm = kNone, bc = kNone;
-            scan_unvisited<false, true>(A.inv_w + (size_t)cur * A.ld, tabu, n, (uint32_t)s, ant, iter, A.key, lane, bm,
+            scan_unvisited<false, true>(c_inv_w + (size_t)cur * A.ld, tabu, n, (uint32_t)s, ant, iter, c_key, lane, bm,
                                   bc);
             const uint32_t nxt = warp_select(bm, bc);
             tabu.mark(nxt, lane);
@@ -1048,10 +1217,12 @@ __global__ void __launch_bounds__(128) construct_full_kernel(ConstructArgs A) {
         }
         flush_route(route, n, lane, stage);
         __syncwarp();
-        if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane));
+        if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane, A.lengths + (long long)col * A.cs.ants));
     }
     pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
-    block_finish(A, wbest, 0, lane, warp);
+    ConstructArgs At = A;
+    if (col) colony_offset(At, col);
+    block_finish(At, wbest, 0, lane, warp);
 }
 
 
@@ -1157,29 +1328,34 @@ __device__ __forceinline__ void ct_mark(uint16_t* ent, int L, int n, uint32_t u)
     }
 }
 
-__global__ void __launch_bounds__(128) construct_ct_kernel(ConstructArgs A) {
+__global__ void __launch_bounds__(128) construct_ct_kernel(const ConstructArgs A) {
+    // colony (grid.y, R29): per-colony pointers as locals, a colony copy for the tail
+    const int col = (int)blockIdx.y;
+    const float* __restrict__ c_inv_w = A.inv_w + col * A.cs.nn;
+    uint16_t* __restrict__ c_routes = A.routes + col * A.cs.routes;
+    const PhiloxKey c_key = col ? colony_key(A.key, (uint32_t)col) : A.key;
     pdl_wait();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int n = A.n;
     const int ent_len = (n + 255) & ~255;                 // padded: a trip may read past L
     uint16_t* ent = reinterpret_cast<uint16_t*>(g_smem + 128) + (size_t)warp * ent_len;
-    const uint32_t iter = *A.iter_dev;
+    const uint32_t iter = A.iter_dev[col];
     unsigned long long wbest = ~0ull;
 
     for (int al = blockIdx.x * A.warps_per_block + warp; al < A.m_local; al += gridDim.x * A.warps_per_block) {
         const uint32_t ant = (uint32_t)(A.ant_lo + al);
         for (int i = lane; i < n; i += 32) ent[i] = (uint16_t)i;
         __syncwarp();
-        const uint32_t start = __umulhi(philox4x32_10(ctr_start(ant, iter), A.key).x, (uint32_t)n);
+        const uint32_t start = __umulhi(philox4x32_10(ctr_start(ant, iter), c_key).x, (uint32_t)n);
         if (lane == 0) ct_mark(ent, n, n, start);
         __syncwarp();
-        uint16_t* route = A.routes + (size_t)al * A.ldr;
+        uint16_t* route = c_routes + (size_t)al * A.ldr;
         uint32_t stage = (lane == 0) ? start : 0u;
         uint32_t cur = start;
         for (int s = 1; s < n; ++s) {
             const int L = n - s;
-            const float* row = A.inv_w + (size_t)cur * A.ld;
+            const float* row = c_inv_w + (size_t)cur * A.ld;
             uint32_t bm = kNone, bc = kNone;
             // the next trip's list entries and inv_w gathers are loaded one trip ahead
             // (two register sets, loop unrolled by two so no copies are needed)
@@ -1189,10 +1365,10 @@ __global__ void __launch_bounds__(128) construct_ct_kernel(ConstructArgs A) {
             ct_load_trip(ent, row, 0, lane, L, eA, ivA);
             for (int base = 0; base < L; base += 512) {
                 if (base + 256 < L) ct_load_trip(ent, row, base + 256, lane, L, eB, ivB);
-                ct_trip(eA, ivA, base, lane, L, (uint32_t)s, ant, iter, A.key, bm, bc, thr);
+                ct_trip(eA, ivA, base, lane, L, (uint32_t)s, ant, iter, c_key, bm, bc, thr);
                 if (base + 256 >= L) break;
                 if (base + 512 < L) ct_load_trip(ent, row, base + 512, lane, L, eA, ivA);
-                ct_trip(eB, ivB, base + 256, lane, L, (uint32_t)s, ant, iter, A.key, bm, bc, thr);
+                ct_trip(eB, ivB, base + 256, lane, L, (uint32_t)s, ant, iter, c_key, bm, bc, thr);
             }
             const uint32_t nxt = warp_select(bm, bc);
             if (lane == 0) ct_mark(ent, L, n, nxt);
@@ -1202,10 +1378,12 @@ __global__ void __launch_bounds__(128) construct_ct_kernel(ConstructArgs A) {
         }
         flush_route(route, n, lane, stage);
         __syncwarp();
-        if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane));
+        if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane, A.lengths + (long long)col * A.cs.ants));
     }
     pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
-    block_finish(A, wbest, 0, lane, warp);
+    ConstructArgs At = A;
+    if (col) colony_offset(At, col);
+    block_finish(At, wbest, 0, lane, warp);
 }
 
 }  // namespace mmas

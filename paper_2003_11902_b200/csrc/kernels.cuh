@@ -30,6 +30,24 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
+// Device error word of a context (mmas_status): a device-side wait that gave up sets a bit
+// and the iteration's selection + update are skipped from then on (the replicas stay at the
+// last completed iteration instead of silently diverging).
+constexpr uint32_t kErrPeerTimeout = 1u;   // a peer's exchange flag did not arrive (row a7)
+constexpr uint32_t kErrGridBarrier = 2u;   // the fused launch's grid barrier did not release
+// Default bound of every device-side spin: ~2^34 cycles (~9 s at 1.9 GHz); MMAS_SPIN_BOUND
+// (cycles, read at create) overrides it -- the failure-path tests use a short one
+constexpr long long kSpinBound = 1ll << 34;
+// Epoch word of the fused launch's grid barrier: bit 31 marks an aborted iteration (sticky)
+constexpr uint32_t kEpochAbort = 0x80000000u;
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) { return *(const volatile uint32_t*)p; }
+
 // Phase timestamps of construct_cl_kernel (tools/trace_phases.py; only with -DMMAS_TRACE):
 // per block [entry, table staged, warp 0's ants done, block_finish done (the last block:
 // + selection), barrier released, end], %globaltimer ns, thread 0.  No code otherwise.
@@ -42,8 +60,19 @@ __device__ __forceinline__ void trace_mark(int k) {
         g_trace[blockIdx.x * 8 + k] = t;
     }
 }
+// fallback scans: [0] cycles summed over every fallback (lane 0's clock), [1] their count
+__device__ unsigned long long g_fbcyc[2];
+__device__ __forceinline__ long long trace_clock() { return clock64(); }
+__device__ __forceinline__ void trace_fallback(long long t0, int lane) {
+    if (lane == 0) {
+        atomicAdd(&g_fbcyc[0], (unsigned long long)(clock64() - t0));
+        atomicAdd(&g_fbcyc[1], 1ull);
+    }
+}
 #else
 __device__ __forceinline__ void trace_mark(int) {}
+__device__ __forceinline__ long long trace_clock() { return 0; }
+__device__ __forceinline__ void trace_fallback(long long, int) {}
 #endif
 
 // TSPLIB EUC_2D (R12): (int)(sqrt(dx*dx + dy*dy) + 0.5) in double.
@@ -68,6 +97,15 @@ __device__ __forceinline__ float inv_weight(float tau, float heur, int alpha) {
     return __fdiv_rn(1.0f, __fmul_rn(pow_alpha(tau, alpha), heur));
 }
 
+// eta^beta of edge (p, q) (R11, R12, R18 integer beta): (float)(1.0 / max(d,1)^beta) in double
+__device__ __forceinline__ float heur_edge(double2 p, double2 q, int beta) {
+    const int32_t d = euc2d(p, q);
+    const double D = (double)(d > 1 ? d : 1);
+    double Db = 1.0;
+    for (int k = 0; k < beta; ++k) Db = __dmul_rn(Db, D);
+    return __double2float_rn(__ddiv_rn(1.0, Db));
+}
+
 // Keys are strictly negative (log2 u < 0, inv_w > 0), so "largest key" is
 // "smallest magnitude": the magnitude bits order like unsigned integers.
 // kNone marks "no candidate" (R15: initial key -inf).
@@ -79,6 +117,27 @@ __device__ __forceinline__ uint32_t warp_select(uint32_t mag, uint32_t city) {
     const uint32_t best = __reduce_min_sync(kFull, mag);
     if (best == kNone) return kNone;
     return __reduce_min_sync(kFull, mag == best ? city : kNone);
+}
+
+// ---------------------------------------------------------------------------
+// Concurrent independent colonies (the paper's repeated runs, P:1143-1145,
+// and its colony-size study, Sec. 5.4).  A context may hold k colonies: colony c
+// is an independent MMAS run with Philox key seed + c (R29), its own trails,
+// inv_w, candidate 1/w table, routes, best-so-far and limits; the heuristic matrix, candidate
+// ids and coordinates are shared.  Every kernel runs all colonies in one launch with
+// blockIdx.y = colony and shifts its per-colony pointers by these strides at entry.
+// ---------------------------------------------------------------------------
+struct ColonyStride {
+    long long nn;      // floats between two colonies' tau (and inv_w) matrices: n * ld
+    long long cand;    // floats between two colonies' cand_inv tables
+    long long routes;  // u16 between two colonies' route blocks (also 2-opt pos / queue): m_local * ldr
+    int ants;          // lengths per colony: m_local
+    int vec;           // u16 between two colonies' n-vectors (ib / gb route, succ, pred): ldr
+    int inq;           // u32 words of 2-opt queued bits per colony
+};
+__device__ __forceinline__ PhiloxKey colony_key(PhiloxKey k, uint32_t c) {
+    const unsigned long long s = ((unsigned long long)k.k1 << 32 | k.k0) + c;   // R29: seed + c
+    return PhiloxKey{(uint32_t)s, (uint32_t)(s >> 32)};
 }
 
 // ---------------------------------------------------------------------------
@@ -104,7 +163,22 @@ struct SelectArgs {
     float* scal;         // [tau_min, tau_max, delta]
     uint16_t* succ;
     uint16_t* pred;
+    const uint32_t* err;  // split path: skip the selection once the context's error word is set
+    ColonyStride cs;      // select_best_kernel: grid.y = colonies
 };
+__device__ __forceinline__ void colony_offset(SelectArgs& S, int c) {
+    const ColonyStride& cs = S.cs;
+    S.local_key += c;
+    S.routes += c * cs.routes;
+    S.ib_route += (long long)c * cs.vec;
+    S.gb_route += (long long)c * cs.vec;
+    S.gb_len += c;
+    S.ib_len += c;
+    S.ib_ant += c;
+    S.scal += 4 * c;
+    S.succ += (long long)c * cs.vec;
+    S.pred += (long long)c * cs.vec;
+}
 
 __device__ __noinline__ void select_best_warp(const SelectArgs S, int lane) {
     const int n = S.n;
@@ -233,6 +307,8 @@ __device__ __noinline__ void select_best_block(const SelectArgs S) {
 
 __global__ void select_best_kernel(SelectArgs S) {
     pdl_wait();
+    if (S.err && ld_volatile_u32(S.err)) return;   // a lost peer: no selection (mmas_status)
+    if (blockIdx.y) colony_offset(S, (int)blockIdx.y);
     if (threadIdx.x < 32) select_best_warp(S, threadIdx.x);
 }
 
@@ -241,6 +317,7 @@ struct ExchangeArgs {
     unsigned char* const* peers;   // device array: every rank's exchange buffer (peer-mapped)
     int world, rank, rec_bytes;
     uint32_t parity, seq;
+    long long spin_bound;          // cycles before a wait for a peer's flag gives up (kSpinBound)
 };
 
 __device__ __forceinline__ unsigned char* xrecord(unsigned char* buf, const ExchangeArgs& X, int p, int r) {
@@ -249,6 +326,31 @@ __device__ __forceinline__ unsigned char* xrecord(unsigned char* buf, const Exch
 __device__ __forceinline__ uint32_t* xflag(unsigned char* buf, const ExchangeArgs& X, int p, int r) {
     return reinterpret_cast<uint32_t*>(buf + (size_t)2 * X.world * X.rec_bytes) + p * X.world + r;
 }
+
+// ---------------------------------------------------------------------------
+// Memory-lean pheromone (the O(n^2) pheromone memory is the limit the paper
+// names).  EXACT, not an approximation (R30): every trail
+// that was never deposited on undergoes the same fp32 operations, so it equals one scalar, the
+// background b (b_0 = tau_max; b <- min(max(rho b, tau_min), tau_max) each iteration); and a
+// deposited trail equals b again at most L + 1 iterations after its last deposit
+// (L = ceil(ln F / ln rho), F = tau_min / tau_max).  So a row keeps its cl candidate trails
+// densely and at most 2 (L + 1) other trails (each iteration deposits on <= 2 edges of a row)
+// in a small sparse list; every other trail is b, its choice_info recomputed from the
+// coordinates (eta^beta by heur_edge).  Memory O(n (cl + cap)) instead of 3 n^2 floats.
+// ---------------------------------------------------------------------------
+constexpr uint16_t kLeanEmpty = 0xFFFFu;
+constexpr uint32_t kErrLeanFull = 4u;    // a sparse row overflowed (the bound makes this impossible)
+struct LeanArgs {
+    float* cand_tau;         // n x cl_ld: trails of the candidate edges
+    const float* cand_heur;  // n x cl_ld: eta^beta of the candidate edges
+    uint16_t* sp_id;         // n x cap: off-candidate trails different from b (kLeanEmpty = free)
+    float* sp_tau;           // n x cap
+    float* sp_inv;           // n x cap: 1 / choice_info of those trails
+    float* bg;               // [2]: background trail before (bg[p]) / after (bg[p ^ 1]) this update
+    int cap;                 // slots per row (multiple of 32)
+    int parity;              // p = iteration & 1
+    int beta;
+};
 
 // pheromone update arguments (row a6; pheromone_update_kernel below)
 struct UpdateArgs {
@@ -265,7 +367,23 @@ struct UpdateArgs {
     int cl;
     int smem_row;      // 1: the new inv_w row is staged in smem for the cand gather (ld floats fit)
     uint32_t* iter_dev;
+    uint32_t* err;     // context error word: set -> the update is skipped (kernel) / set on a
+                       // grid-barrier timeout (fused)
+    long long spin_bound;  // cycles before the fused launch's grid barrier gives up (kSpinBound)
+    ColonyStride cs;       // pheromone_update_kernel: grid.y = colonies
+    LeanArgs lean;         // lean_update_kernel (cand_tau != null)
+    const double2* xy;     // coordinates (lean: eta^beta of the sparse trails)
 };
+__device__ __forceinline__ void colony_offset(UpdateArgs& U, int c) {
+    const ColonyStride& cs = U.cs;
+    U.tau += c * cs.nn;
+    U.inv_w += c * cs.nn;
+    U.scal += 4 * c;
+    U.succ += (long long)c * cs.vec;
+    U.pred += (long long)c * cs.vec;
+    U.cand_inv += c * cs.cand;
+    U.iter_dev += c;
+}
 
 // Row a6 on one float4 of row i (columns c0 .. c0+3): evaporation, deposit along the
 // succ/pred edges of T_dep, clamp (R1, R4-R6), then 1/choice_info (R19).  Shared by the
@@ -302,6 +420,9 @@ struct ConstructArgs {
     uint32_t fb_row_off;         // L2-table kernel: shared-memory offset of the fallback row buffer (0 = none)
     int warps_per_block;
     uint32_t table_bytes_inv, table_bytes_id;  // smem-table variant: padded table sizes
+    // > 0: every block asks L2 for its share of the inv_w matrix (n x ld f32, this many bytes)
+    // at launch start, so the fallback rows (row a3) are L2 hits, not HBM round trips
+    unsigned long long l2_prefetch_bytes;
     uint16_t* __restrict__ routes;          // m_local x ldr
     long long* __restrict__ lengths;        // m_local
     unsigned long long* __restrict__ best_key;       // local min (len << 24 | ant)
@@ -326,7 +447,26 @@ struct ConstructArgs {
     ExchangeArgs X;
     unsigned char* xown;   // this rank's exchange buffer
     uint32_t* xerr;        // set when a peer's flag does not arrive (bounded wait)
+    ColonyStride cs;       // colonies (grid.y): per-colony pointer strides
+    LeanArgs lean;         // memory-lean pheromone (R30; lean.cand_tau != null): the fallback scans
+                           // recompute inv_w rows from the coordinates and the background trail
 };
+// The arguments of colony c (blockIdx.y) -- every per-colony pointer shifted (R29 key)
+__device__ __forceinline__ void colony_offset(ConstructArgs& A, int c) {
+    const ColonyStride& cs = A.cs;
+    A.inv_w += c * cs.nn;
+    A.tau += c * cs.nn;
+    A.cand_inv += c * cs.cand;
+    A.iter_dev += c;
+    A.key = colony_key(A.key, (uint32_t)c);
+    A.routes += c * cs.routes;
+    A.lengths += (long long)c * cs.ants;
+    A.best_key += c;
+    A.done += 2 * c;
+    A.epoch += 2 * c;
+    colony_offset(A.sel, c);
+    colony_offset(A.upd, c);
+}
 
 }  // namespace mmas
 
@@ -394,18 +534,20 @@ __global__ void wait_peers_kernel(unsigned char* own, ExchangeArgs X, uint32_t* 
     pdl_wait();
     const int r = threadIdx.x;
     if (r < X.world) {
-        volatile uint32_t* f = xflag(own, X, (int)X.parity, r);
+        // the flag is written by another device: acquire at system scope (pairs with the
+        // writer's __threadfence_system before its flag store)
+        const uint32_t* f = xflag(own, X, (int)X.parity, r);
         const long long t0 = clock64();
-        while (*f != X.seq) {
-            if (clock64() - t0 > (1ll << 34)) {
-                atomicExch(err, 1u);
+        while (ld_acquire_sys(f) != X.seq) {
+            if (clock64() - t0 > X.spin_bound) {
+                atomicOr(err, kErrPeerTimeout);
                 break;
             }
             __nanosleep(200);
         }
     }
     __syncwarp();
-    __threadfence();
+    __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -419,6 +561,7 @@ __global__ void wait_peers_kernel(unsigned char* own, ExchangeArgs X, uint32_t* 
 
 __global__ void __launch_bounds__(256) pheromone_update_kernel(UpdateArgs U) {
     extern __shared__ __align__(16) float s_row[];   // new inv_w row (cl > 0: for the gather)
+    if (blockIdx.y) colony_offset(U, (int)blockIdx.y);
     const int n4 = (U.n + 3) >> 2;
     // Prologue before the dependency wait: tau, heur and the candidate ids are not written
     // by the construction / 2-opt / selection kernels this one depends on (tau's last writer
@@ -439,6 +582,10 @@ __global__ void __launch_bounds__(256) pheromone_update_kernel(UpdateArgs U) {
         if (U.cl > 0 && (int)threadIdx.x < U.cl) cid = U.cand_id[(size_t)blockIdx.x * U.cl + threadIdx.x];
     }
     pdl_wait();
+    if (U.err && ld_volatile_u32(U.err)) {   // a lost peer: the replica keeps its trails (mmas_status)
+        if (blockIdx.x == 0 && threadIdx.x == 0) *U.iter_dev += 1u;
+        return;
+    }
     const float tmin = U.scal[0], tmax = U.scal[1], delta = U.scal[2];
     bool first = true;
     for (int i = blockIdx.x; i < U.n; i += gridDim.x) {
@@ -489,19 +636,118 @@ __global__ void __launch_bounds__(256) pheromone_update_kernel(UpdateArgs U) {
 // ---------------------------------------------------------------------------
 // eta^beta for integer beta (R11, R18): (float)(1 / D^beta), D = max(d, 1).
 // Pad columns (n <= c < ld) get 1.0 so every float4 of a row is finite.
+// Row a6 in the lean representation (R30): one warp per row i -- the candidate trails, the
+// sparse trails (dropped when equal to the new background), then the deposits on edges
+// (i, succ i), (i, pred i) that are in neither (inserted at the value the dense update gives
+// a trail that was at the background).  Same fp32 operations as update_quad, element by element.
+__device__ __forceinline__ float evap_deposit_clamp(float tau, bool dep, float rho_f, float tmin, float tmax,
+                                                    float delta) {
+    float t = fmaxf(__fmul_rn(rho_f, tau), tmin);
+    if (dep) t = __fadd_rn(t, delta);
+    return fminf(t, tmax);
+}
+__global__ void __launch_bounds__(256) lean_update_kernel(UpdateArgs U) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int i = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+    const LeanArgs& Ln = U.lean;
+    if (U.err && ld_volatile_u32(U.err)) {   // a lost peer: keep the trails (mmas_status)
+        if (blockIdx.x == 0 && threadIdx.x == 0) *U.iter_dev += 1u;
+        return;
+    }
+    const float tmin = U.scal[0], tmax = U.scal[1], delta = U.scal[2];
+    const float b0 = Ln.bg[Ln.parity];
+    const float b1 = evap_deposit_clamp(b0, false, U.rho_f, tmin, tmax, delta);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Ln.bg[Ln.parity ^ 1] = b1;
+        *U.iter_dev += 1u;
+    }
+    if (i >= U.n) return;
+    const int si = U.succ[i], pi = U.pred[i];
+    bool has_s = false, has_p = false;
+    // candidate trails (dense)
+    for (int k = lane; k < U.cl; k += 32) {
+        const size_t e = (size_t)i * U.cl + k;
+        const int c = U.cand_id[e];
+        const float t = evap_deposit_clamp(Ln.cand_tau[e], c == si || c == pi, U.rho_f, tmin, tmax, delta);
+        Ln.cand_tau[e] = t;
+        U.cand_inv[e] = inv_weight(t, Ln.cand_heur[e], U.alpha);
+        has_s |= c == si;
+        has_p |= c == pi;
+    }
+    // sparse trails: update, drop the ones equal to the background
+    const double2 xi = U.xy[i];
+    uint32_t free_mask_lo = 0;   // free slots among the lane's first 32 (bit = slot / 32)
+    for (int k = lane; k < Ln.cap; k += 32) {
+        const size_t e = (size_t)i * Ln.cap + k;
+        const int j = Ln.sp_id[e];
+        if (j == kLeanEmpty) {
+            free_mask_lo |= 1u << (k >> 5);
+            continue;
+        }
+        const bool dep = j == si || j == pi;
+        has_s |= j == si;
+        has_p |= j == pi;
+        const float t = evap_deposit_clamp(Ln.sp_tau[e], dep, U.rho_f, tmin, tmax, delta);
+        if (t == b1) {
+            Ln.sp_id[e] = kLeanEmpty;
+            free_mask_lo |= 1u << (k >> 5);
+        } else {
+            Ln.sp_tau[e] = t;
+            Ln.sp_inv[e] = inv_weight(t, heur_edge(xi, U.xy[j], Ln.beta), U.alpha);
+        }
+    }
+    has_s = __any_sync(kFull, has_s);
+    has_p = __any_sync(kFull, has_p);
+    // deposits on trails that were at the background: insert where the result differs from it
+    const float tdep = evap_deposit_clamp(b0, true, U.rho_f, tmin, tmax, delta);
+    int want[2] = {has_s || si == i ? -1 : si, has_p || pi == i || pi == si ? -1 : pi};
+    for (int w = 0; w < 2; ++w) {
+        if (want[w] < 0 || tdep == b1) continue;
+        // the lowest free slot: (lane, round) with round-major order
+        int slot = -1;
+        for (int r = 0; r * 32 < Ln.cap && slot < 0; ++r) {
+            const unsigned m = __ballot_sync(kFull, (free_mask_lo >> r) & 1u);
+            if (m) slot = r * 32 + __ffs(m) - 1;
+        }
+        if (slot < 0) {
+            if (lane == 0) atomicOr(U.err, kErrLeanFull);
+            break;
+        }
+        if (lane == (slot & 31)) {
+            free_mask_lo &= ~(1u << (slot >> 5));
+            const size_t e = (size_t)i * Ln.cap + slot;
+            Ln.sp_id[e] = (uint16_t)want[w];
+            Ln.sp_tau[e] = tdep;
+            Ln.sp_inv[e] = inv_weight(tdep, heur_edge(xi, U.xy[want[w]], Ln.beta), U.alpha);
+        }
+        __syncwarp();
+    }
+}
+
+// Lean setup: the candidate edges' eta^beta, trails tau_max and 1 / choice_info; every
+// sparse slot free; background tau_max
+__global__ void lean_init_kernel(const double2* __restrict__ xy, int n, int cl, const uint16_t* cand_id, int beta,
+                                 int alpha, const float* scal, LeanArgs Ln, float* cand_inv) {
+    const float tmax = scal[1];
+    const size_t total = (size_t)n * cl;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e / cl);
+        const float h = heur_edge(xy[i], xy[cand_id[e]], beta);
+        const_cast<float*>(Ln.cand_heur)[e] = h;
+        Ln.cand_tau[e] = tmax;
+        cand_inv[e] = inv_weight(tmax, h, alpha);
+    }
+    const size_t sp = (size_t)n * Ln.cap;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < sp; e += (size_t)gridDim.x * blockDim.x)
+        Ln.sp_id[e] = kLeanEmpty;
+    if (blockIdx.x == 0 && threadIdx.x == 0) Ln.bg[0] = Ln.bg[1] = tmax;
+}
+
 __global__ void heur_kernel(const double2* __restrict__ xy, int n, int ld, int beta, float* heur) {
     const int i = blockIdx.y;
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ld; c += gridDim.x * blockDim.x) {
-        float h = 1.0f;
-        if (c < n) {
-            const int32_t d = euc2d(xy[i], xy[c]);
-            const double D = (double)(d > 1 ? d : 1);
-            double Db = 1.0;
-            for (int k = 0; k < beta; ++k) Db = __dmul_rn(Db, D);
-            h = __double2float_rn(__ddiv_rn(1.0, Db));
-        }
-        heur[(size_t)i * ld + c] = h;
-    }
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ld; c += gridDim.x * blockDim.x)
+        heur[(size_t)i * ld + c] = c < n ? heur_edge(xy[i], xy[c], beta) : 1.0f;
 }
 
 // Nearest-neighbour tour from city 0 (R3; the initial trail limits, Alg. 1):

@@ -126,6 +126,17 @@ struct mmas_ctx {
     uint32_t fb_row_off = 0;                // L2-table kernel: fallback row buffer in smem
     uint32_t tb_inv = 0, tb_id = 0;
 
+    // memory-lean pheromone (R30): no n x n matrices; candidate trails + sparse rows
+    bool lean = false;
+    int lean_cap = 0, lean_L = 0;
+    float *cand_tau = nullptr, *cand_heur = nullptr, *sp_tau = nullptr, *sp_inv = nullptr, *bg = nullptr;
+    uint16_t* sp_id = nullptr;
+
+    // concurrent independent colonies (R29): K per-colony copies of the mutable state
+    int colonies = 1;
+    int view = 0;                           // colony the introspection calls report
+    ColonyStride cs{};
+
     // host mirrors
     int32_t iteration = 0;
     int64_t launches = 0;
@@ -145,7 +156,8 @@ struct mmas_ctx {
     unsigned char* xbuf = nullptr;            // own buffer: [2][world] records + [2][world] flags
     unsigned char** xpeers_dev = nullptr;     // device array of every rank's (peer-mapped) buffer
     std::vector<void*> xopened;               // IPC mappings to close
-    uint32_t* xerr = nullptr;                 // set by wait_peers_kernel on timeout
+    uint32_t* xerr = nullptr;                 // device error word (kErr*): a device-side wait gave up
+    long long spin_bound = kSpinBound;        // device-side waits give up after this many cycles
     bool xattached = false;
 
     // profiling
@@ -223,10 +235,27 @@ SelectArgs select_args(mmas_ctx* h, const unsigned char* records, int count) {
     S.scal = h->scal;
     S.succ = h->succ;
     S.pred = h->pred;
+    S.err = h->xerr;
+    S.cs = h->cs;
     return S;
 }
 
 UpdateArgs update_args(mmas_ctx* h);
+
+LeanArgs lean_args(mmas_ctx* h) {
+    LeanArgs L{};
+    if (!h->lean) return L;
+    L.cand_tau = h->cand_tau;
+    L.cand_heur = h->cand_heur;
+    L.sp_id = h->sp_id;
+    L.sp_tau = h->sp_tau;
+    L.sp_inv = h->sp_inv;
+    L.bg = h->bg;
+    L.cap = h->lean_cap;
+    L.parity = h->iteration & 1;
+    L.beta = (int)h->cfg.beta;
+    return L;
+}
 
 ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = false) {
     ConstructArgs A{};
@@ -249,8 +278,17 @@ ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = f
     A.fallback_argmax = h->cfg.fallback == MMAS_FALLBACK_ARGMAX;
     // pruned fallback scans where 16+ ant warps per SM hide their reduction latency (C3:
     // 5.78 -> 5.34 ms); the branch-free scan at fewer (C5: 29.4 vs 33.0 ms pruned)
-    A.prune_fallback = h->m_local >= 16 * h->num_sms;
+    A.prune_fallback = (long long)h->m_local * h->colonies >= 16ll * h->num_sms;
     A.fb_row_off = h->fb_row_off;
+    // candidate-list colonies whose inv_w matrix takes at most half the L2: its fallback rows
+    // are prefetched into L2 at launch start (4 MB at pr1002: < 1 us of HBM time); MMAS_L2_PF=0
+    // turns it off (A/B)
+    {
+        static const char* pf = std::getenv("MMAS_L2_PF");
+        const unsigned long long bytes = (unsigned long long)h->n * h->ld * sizeof(float);
+        A.l2_prefetch_bytes = (h->cl > 0 && !h->rwm && !h->lean && 2 * bytes * h->colonies <= (unsigned long long)h->l2_bytes &&
+                               !(pf && pf[0] == '0')) ? bytes : 0ull;
+    }
     A.warps_per_block = h->cons_warps;
     A.table_bytes_inv = h->tb_inv;
     A.table_bytes_id = h->tb_id;
@@ -264,6 +302,8 @@ ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = f
     A.epoch = h->done + 1;
     A.upd = update_args(h);
     A.xchg = 0;
+    A.cs = h->cs;
+    A.lean = lean_args(h);
     return A;
 }
 
@@ -304,8 +344,8 @@ void set_smem_attr(int optin) {
 
 template <int S, bool T, bool R, bool F, bool W = false>
 void launch_cl_f(mmas_ctx* h, const ConstructArgs& A) {
-    launch_pdl(construct_cl_kernel<S, T, R, F, W>, dim3(h->cons_grid), dim3(h->cons_warps * 32), h->cons_smem,
-               h->stream, A);
+    launch_pdl(construct_cl_kernel<S, T, R, F, W>, dim3(h->cons_grid, h->colonies), dim3(h->cons_warps * 32),
+               h->cons_smem, h->stream, A);
 }
 
 // cl <= 32 (tables padded to 32 slots): one slot per lane; more than 8 ant warps per block
@@ -320,7 +360,7 @@ void launch_cl(mmas_ctx* h, const ConstructArgs& A) {
             }
         } else {
             // L2 table, fewer than 16 ant warps per SM: the uncapped-register instantiation
-            if (h->m_local < 16 * h->num_sms) {
+            if ((long long)h->m_local * h->colonies < 16ll * h->num_sms) {
                 launch_cl_f<1, T, R, true, true>(h, A);
                 return;
             }
@@ -359,15 +399,15 @@ int launch_two_opt(mmas_ctx* h, bool fuse_select);
 // full-row construction (cl == 0): compact-tabu list or bitmask scan; or the roulette wheel
 void launch_full(mmas_ctx* h, const ConstructArgs& A) {
     if (h->rwm && h->compact_tabu)
-        construct_rwm_kernel<true><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+        construct_rwm_kernel<true><<<dim3(h->cons_grid, h->colonies), h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
     else if (h->rwm)
-        construct_rwm_kernel<false><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+        construct_rwm_kernel<false><<<dim3(h->cons_grid, h->colonies), h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
     else if (h->compact_tabu)
-        construct_ct_kernel<<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+        construct_ct_kernel<<<dim3(h->cons_grid, h->colonies), h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
     else if (h->reg_tabu)
-        construct_full_kernel<true><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+        construct_full_kernel<true><<<dim3(h->cons_grid, h->colonies), h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
     else
-        construct_full_kernel<false><<<h->cons_grid, h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
+        construct_full_kernel<false><<<dim3(h->cons_grid, h->colonies), h->cons_warps * 32, h->cons_smem, h->stream>>>(A);
 }
 
 // Construction (rows a1-a4) -- and, with local search on, the 2-opt pass (row a8) that
@@ -413,7 +453,7 @@ int launch_construct(mmas_ctx* h, bool fuse_select, const ExchangeArgs* xfused =
 
 int launch_select(mmas_ctx* h, const unsigned char* records, int count) {
     PhaseScope ps(h, 1);
-    select_best_kernel<<<1, 32, 0, h->stream>>>(select_args(h, records, count));
+    select_best_kernel<<<dim3(1, h->colonies), 32, 0, h->stream>>>(select_args(h, records, count));
     h->launches++;
     CU(cudaGetLastError());
     return MMAS_OK;
@@ -443,18 +483,18 @@ int launch_two_opt(mmas_ctx* h, bool fuse_select) {
         // one block of kLsWarps warps per ant (speculative parallel FIFO, two_opt_coop_kernel)
         T.warps_per_block = kLsWarps;
         if (h->ls_int_xy)
-            launch_pdl(two_opt_coop_kernel<true>, dim3(std::max(1, h->m_local)), dim3(kLsWarps * 32), per_ant,
+            launch_pdl(two_opt_coop_kernel<true>, dim3(std::max(1, h->m_local), h->colonies), dim3(kLsWarps * 32), per_ant,
                        h->stream, T, construct_args(h, fuse_select));
         else
-            launch_pdl(two_opt_coop_kernel<false>, dim3(std::max(1, h->m_local)), dim3(kLsWarps * 32), per_ant,
+            launch_pdl(two_opt_coop_kernel<false>, dim3(std::max(1, h->m_local), h->colonies), dim3(kLsWarps * 32), per_ant,
                        h->stream, T, construct_args(h, fuse_select));
     } else {
         T.warps_per_block = 4;
         const int grid = std::max(1, (h->m_local + 3) / 4);
         if (h->ls_int_xy)
-            launch_pdl(two_opt_kernel<true>, dim3(grid), dim3(128), 0, h->stream, T, construct_args(h, fuse_select));
+            launch_pdl(two_opt_kernel<true>, dim3(grid, h->colonies), dim3(128), 0, h->stream, T, construct_args(h, fuse_select));
         else
-            launch_pdl(two_opt_kernel<false>, dim3(grid), dim3(128), 0, h->stream, T, construct_args(h, fuse_select));
+            launch_pdl(two_opt_kernel<false>, dim3(grid, h->colonies), dim3(128), 0, h->stream, T, construct_args(h, fuse_select));
     }
     h->launches++;
     CU(cudaGetLastError());
@@ -477,6 +517,11 @@ UpdateArgs update_args(mmas_ctx* h) {
     U.cand_inv = h->cand_inv;
     U.cl = h->cl_ld;
     U.iter_dev = h->iter_dev;
+    U.err = h->xerr;
+    U.spin_bound = h->spin_bound;
+    U.cs = h->cs;
+    U.lean = lean_args(h);
+    U.xy = h->xy;
     U.smem_row = h->cl > 0 && sizeof(float) * (size_t)h->ld <= (size_t)h->smem_optin - 1024;
     return U;
 }
@@ -485,8 +530,14 @@ int launch_update(mmas_ctx* h) {
     PhaseScope ps(h, 2);
     UpdateArgs U = update_args(h);
     const int threads = 256;
+    if (h->lean) {   // one warp per row over the lean representation (R30)
+        launch_pdl(lean_update_kernel, dim3((h->n + 7) / 8), dim3(threads), 0, h->stream, U);
+        h->launches++;
+        CU(cudaGetLastError());
+        return MMAS_OK;
+    }
     const size_t smem = U.smem_row ? sizeof(float) * (size_t)h->ld : 0;
-    launch_pdl(pheromone_update_kernel, dim3(h->n), dim3(threads), smem, h->stream, U);
+    launch_pdl(pheromone_update_kernel, dim3(h->n, h->colonies), dim3(threads), smem, h->stream, U);
     h->launches++;
     CU(cudaGetLastError());
     return MMAS_OK;
@@ -499,7 +550,8 @@ void free_ctx(mmas_ctx* h) {
     void* ptrs[] = {h->xy, h->heur, h->tau, h->inv_w, h->cand_inv, h->cand_id, h->routes, h->lengths,
                     h->best_key, h->fallback_count, h->ib_route, h->gb_route, h->succ, h->pred, h->gb_len,
                     h->ib_len, h->ib_ant, h->scal, h->iter_dev, h->local_record, h->done,
-                    h->ls_nn, h->ls_nnd, h->ls_xys, h->ls_nnp, h->ls_pos, h->ls_queue, h->ls_inq, h->ls_moves};
+                    h->ls_nn, h->ls_nnd, h->ls_xys, h->ls_nnp, h->ls_pos, h->ls_queue, h->ls_inq, h->ls_moves,
+                    h->cand_tau, h->cand_heur, h->sp_id, h->sp_tau, h->sp_inv, h->bg};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : h->xopened) cudaIpcCloseMemHandle(p);
@@ -516,6 +568,27 @@ int dalloc(T** p, size_t count) {
     cudaError_t e = cudaMalloc((void**)p, sizeof(T) * std::max<size_t>(count, 1));
     if (e != cudaSuccess) return fail(MMAS_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
     return MMAS_OK;
+}
+
+// The one-launch iteration's grid barrier needs every block of the grid resident at once:
+// blocks per SM that fit (registers, shared memory, threads of this instantiation) x SMs >= grid
+bool grid_co_resident(mmas_ctx* h) {
+    int per_sm = 0;
+    cudaError_t e;
+    const int threads = h->cons_warps * 32;
+    if (h->reg_tabu)
+        e = h->cons_warps > 8
+                ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, construct_cl_kernel<1, true, true, true, true>, threads, h->cons_smem)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, construct_cl_kernel<1, true, true, true>, threads, h->cons_smem);
+    else
+        e = h->cons_warps > 8
+                ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, construct_cl_kernel<1, true, false, true, true>, threads, h->cons_smem)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, construct_cl_kernel<1, true, false, true>, threads, h->cons_smem);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return (long long)per_sm * h->num_sms >= (long long)h->cons_grid * h->colonies;
 }
 
 int setup(mmas_ctx* h) {
@@ -544,35 +617,53 @@ int setup(mmas_ctx* h) {
     h->key.k0 = (uint32_t)c.seed;
     h->key.k1 = (uint32_t)(c.seed >> 32);
     h->rec_bytes = round_up(8 + 2 * n, 16);
+    h->colonies = std::max(1, c.colonies);
+    if (const char* sb = std::getenv("MMAS_SPIN_BOUND")) h->spin_bound = std::max(1ll << 10, std::atoll(sb));
 
     const size_t nn = (size_t)n * h->ld;
+    // per-colony strides (R29; kernels shift by blockIdx.y * stride)
+    const size_t K = (size_t)h->colonies;
+    const size_t ma = (size_t)std::max(h->m_local, 1);
+    h->cs.nn = (long long)nn;
+    h->cs.cand = (long long)n * h->cl_ld + 64;
+    h->cs.routes = (long long)ma * h->ldr;
+    h->cs.ants = (int)ma;
+    h->cs.vec = h->ldr;
+    h->cs.inq = 0;
     int st;
-    if ((st = dalloc(&h->xy, n)) || (st = dalloc(&h->heur, nn)) || (st = dalloc(&h->tau, nn)) ||
-        (st = dalloc(&h->inv_w, nn)) || (st = dalloc(&h->cand_inv, (size_t)n * h->cl_ld + 64)) ||
+    h->lean = c.pheromone == MMAS_PHEROMONE_LEAN;
+    const size_t nn_alloc = h->lean ? 0 : nn;   // lean (R30): no n x n matrices at all
+    if ((st = dalloc(&h->xy, n)) || (st = dalloc(&h->heur, nn_alloc)) || (st = dalloc(&h->tau, nn_alloc * K)) ||
+        (st = dalloc(&h->inv_w, nn_alloc * K)) || (st = dalloc(&h->cand_inv, (size_t)h->cs.cand * K)) ||
         (st = dalloc(&h->cand_id, (size_t)n * h->cl_ld + 64)) ||
-        (st = dalloc(&h->routes, (size_t)std::max(h->m_local, 1) * h->ldr)) ||
-        (st = dalloc(&h->lengths, (size_t)std::max(h->m_local, 1))) || (st = dalloc(&h->best_key, 1)) ||
-        (st = dalloc(&h->fallback_count, 1)) || (st = dalloc(&h->ib_route, n)) || (st = dalloc(&h->gb_route, (size_t)h->ldr)) ||
-        (st = dalloc(&h->succ, n)) || (st = dalloc(&h->pred, n)) || (st = dalloc(&h->gb_len, 1)) ||
-        (st = dalloc(&h->ib_len, 1)) || (st = dalloc(&h->ib_ant, 1)) || (st = dalloc(&h->scal, 4)) ||
-        (st = dalloc(&h->iter_dev, 1)) || (st = dalloc(&h->local_record, (size_t)h->rec_bytes)) ||
-        (st = dalloc(&h->done, 2)))
+        (st = dalloc(&h->routes, ma * h->ldr * K)) ||
+        (st = dalloc(&h->lengths, ma * K)) || (st = dalloc(&h->best_key, K)) ||
+        (st = dalloc(&h->fallback_count, 1)) || (st = dalloc(&h->ib_route, (size_t)h->ldr * K)) ||
+        (st = dalloc(&h->gb_route, (size_t)h->ldr * K)) ||
+        (st = dalloc(&h->succ, (size_t)h->ldr * K)) || (st = dalloc(&h->pred, (size_t)h->ldr * K)) ||
+        (st = dalloc(&h->gb_len, K)) || (st = dalloc(&h->ib_len, K)) || (st = dalloc(&h->ib_ant, K)) ||
+        (st = dalloc(&h->scal, 4 * K)) || (st = dalloc(&h->iter_dev, K)) ||
+        (st = dalloc(&h->local_record, (size_t)h->rec_bytes)) || (st = dalloc(&h->done, 2 * K)) ||
+        (st = dalloc(&h->xerr, 1)))
         return st;
 
     CU(cudaMemcpyAsync(h->xy, c.coords, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, h->stream));
-    CU(cudaMemsetAsync(h->routes, 0, sizeof(uint16_t) * (size_t)std::max(h->m_local, 1) * h->ldr, h->stream));
-    CU(cudaMemsetAsync(h->lengths, 0, sizeof(long long) * (size_t)std::max(h->m_local, 1), h->stream));
-    CU(cudaMemsetAsync(h->best_key, 0xFF, sizeof(unsigned long long), h->stream));
+    CU(cudaMemsetAsync(h->routes, 0, sizeof(uint16_t) * ma * h->ldr * K, h->stream));
+    CU(cudaMemsetAsync(h->lengths, 0, sizeof(long long) * ma * K, h->stream));
+    CU(cudaMemsetAsync(h->best_key, 0xFF, sizeof(unsigned long long) * K, h->stream));
     CU(cudaMemsetAsync(h->fallback_count, 0, sizeof(unsigned long long), h->stream));
-    CU(cudaMemsetAsync(h->gb_len, 0xFF, sizeof(long long), h->stream));   // -1: empty
-    CU(cudaMemsetAsync(h->ib_len, 0xFF, sizeof(long long), h->stream));
-    CU(cudaMemsetAsync(h->iter_dev, 0, sizeof(uint32_t), h->stream));
-    CU(cudaMemsetAsync(h->done, 0, 2 * sizeof(unsigned int), h->stream));
-    CU(cudaMemsetAsync(h->succ, 0, sizeof(uint16_t) * n, h->stream));
-    CU(cudaMemsetAsync(h->pred, 0, sizeof(uint16_t) * n, h->stream));
+    CU(cudaMemsetAsync(h->gb_len, 0xFF, sizeof(long long) * K, h->stream));   // -1: empty
+    CU(cudaMemsetAsync(h->ib_len, 0xFF, sizeof(long long) * K, h->stream));
+    CU(cudaMemsetAsync(h->iter_dev, 0, sizeof(uint32_t) * K, h->stream));
+    CU(cudaMemsetAsync(h->done, 0, 2 * sizeof(unsigned int) * K, h->stream));
+    CU(cudaMemsetAsync(h->xerr, 0, sizeof(uint32_t), h->stream));
+    CU(cudaMemsetAsync(h->succ, 0, sizeof(uint16_t) * h->ldr * K, h->stream));
+    CU(cudaMemsetAsync(h->pred, 0, sizeof(uint16_t) * h->ldr * K, h->stream));
 
     // eta^beta (R11, R18)
-    if (is_int_in(c.beta, 0, 8)) {
+    if (h->lean) {
+        // (lean: computed per edge where needed, heur_edge)
+    } else if (is_int_in(c.beta, 0, 8)) {
         dim3 g((h->ld + 255) / 256, n);
         heur_kernel<<<g, 256, 0, h->stream>>>(h->xy, n, h->ld, (int)c.beta, h->heur);
         h->launches++;
@@ -610,7 +701,6 @@ int setup(mmas_ctx* h) {
         h->ls_nwords = (n + 31) / 32;
         std::vector<uint16_t> nnl;
         candidate_lists(c.coords, n, h->ls_k, nnl);
-        const size_t ma = (size_t)std::max(h->m_local, 1);
         // neighbour distances (exact R12 values; the 2-opt evaluation reads d(a, c) from here)
         std::vector<int32_t> nnd(nnl.size());
         for (int i = 0; i < n; ++i)
@@ -626,9 +716,10 @@ int setup(mmas_ctx* h) {
             else
                 xys[(size_t)i] = make_short2((short)x, (short)y);
         }
+        h->cs.inq = (int)(ma * h->ls_nwords);
         if ((st = dalloc(&h->ls_nn, nnl.size())) || (st = dalloc(&h->ls_nnd, nnd.size())) ||
-            (st = dalloc(&h->ls_pos, ma * h->ldr)) ||
-            (st = dalloc(&h->ls_queue, ma * h->ldr)) || (st = dalloc(&h->ls_inq, ma * h->ls_nwords)) ||
+            (st = dalloc(&h->ls_pos, ma * h->ldr * K)) ||
+            (st = dalloc(&h->ls_queue, ma * h->ldr * K)) || (st = dalloc(&h->ls_inq, ma * h->ls_nwords * K)) ||
             (st = dalloc(&h->ls_moves, 1)))
             return st;
         if (h->ls_int_xy) {
@@ -662,21 +753,40 @@ int setup(mmas_ctx* h) {
     }
     const double pn = std::pow(c.p_best, 1.0 / (double)n);
     h->factor = (1.0 - pn) / (((double)n / 2.0 - 1.0) * pn);
-    float lim[4] = {0, 0, 0, 0};
+    std::vector<float> lim(4 * K, 0.0f);
     host_limits(c.rho, h->nn_len, h->factor, &lim[0], &lim[1]);
-    CU(cudaMemcpyAsync(h->scal, lim, sizeof(lim), cudaMemcpyHostToDevice, h->stream));
-    {
+    for (size_t k = 1; k < K; ++k) std::copy(lim.begin(), lim.begin() + 4, lim.begin() + 4 * k);   // same NN tour
+    CU(cudaMemcpyAsync(h->scal, lim.data(), sizeof(float) * lim.size(), cudaMemcpyHostToDevice, h->stream));
+    if (h->lean) {
+        // R30: L = iterations after which a trail without deposits equals tau_min (ratio F =
+        // tau_min / tau_max), with margin for the fp32 rounding; <= 2 (L + 1) sparse trails per row
+        const double F = std::min(1.0, (double)lim[0] / (double)lim[1]);
+        const double rf = (double)(float)c.rho * (1.0 + 1e-6);
+        h->lean_L = F >= 1.0 ? 1 : (int)std::ceil(std::log(F * (1.0 - 1e-5)) / std::log(rf)) + 2;
+        h->lean_cap = round_up(2 * (h->lean_L + 1), 32);
+        const size_t ncl = (size_t)n * h->cl_ld + 64, nsp = (size_t)n * h->lean_cap;
+        if ((st = dalloc(&h->cand_tau, ncl)) || (st = dalloc(&h->cand_heur, ncl)) || (st = dalloc(&h->sp_id, nsp)) ||
+            (st = dalloc(&h->sp_tau, nsp)) || (st = dalloc(&h->sp_inv, nsp)) || (st = dalloc(&h->bg, 2)))
+            return st;
+        lean_init_kernel<<<std::max(1, std::min(4096, (int)((nsp + 255) / 256))), 256, 0, h->stream>>>(
+            h->xy, n, h->cl_ld, h->cand_id, (int)c.beta, h->alpha, h->scal, lean_args(h), h->cand_inv);
+        h->launches++;
+        CU(cudaGetLastError());
+    }
+    for (size_t k = 0; k < K && !h->lean; ++k) {
         dim3 g((h->ld + 255) / 256, n);
-        init_trails_kernel<<<g, 256, 0, h->stream>>>(h->tau, h->inv_w, h->heur, n, h->ld, h->alpha, h->scal);
+        init_trails_kernel<<<g, 256, 0, h->stream>>>(h->tau + k * nn, h->inv_w + k * nn, h->heur, n, h->ld, h->alpha,
+                                                     h->scal);
         h->launches++;
         CU(cudaGetLastError());
+        if (h->cl > 0) {
+            gather_cand_kernel<<<std::max(1, std::min(4096, (n * h->cl_ld + 255) / 256)), 256, 0, h->stream>>>(
+                h->inv_w + k * nn, n, h->ld, h->cand_id, h->cand_inv + k * h->cs.cand, h->cl_ld);
+            h->launches++;
+            CU(cudaGetLastError());
+        }
     }
-    if (h->cl > 0) {
-        gather_cand_kernel<<<std::max(1, std::min(4096, (n * h->cl_ld + 255) / 256)), 256, 0, h->stream>>>(
-            h->inv_w, n, h->ld, h->cand_id, h->cand_inv, h->cl_ld);
-        h->launches++;
-        CU(cudaGetLastError());
-    }
+    CU(cudaStreamSynchronize(h->stream));   // lim goes out of scope
 
     // ---- construction launch plan ----
     // dynamic shared memory a construction kernel may take: the opt-in limit minus its
@@ -703,21 +813,23 @@ int setup(mmas_ctx* h) {
         const size_t per_warp = tabu_bytes;   // per ant warp: its tabu (shared-memory variant)
         // one block per SM holding the whole table; as many ant warps as needed
         const int wmax = h->slots == 1 ? 16 : 8;   // construct_cl_kernel's launch bounds
-        int w = std::max(1, std::min(wmax, (h->m_local + h->num_sms - 1) / std::max(h->num_sms, 1)));
+        // the SMs are shared out between the colonies (one persistent block per SM each)
+        const int sms = std::max(1, h->num_sms / h->colonies);
+        int w = std::max(1, std::min(wmax, (h->m_local + sms - 1) / sms));
         size_t need = 128 + (size_t)h->tb_inv + h->tb_id + 16 + (size_t)w * per_warp;
         h->smem_table = need <= cons_dyn_max;
         if (h->smem_table) {
             // persistent: at most one block per SM, each loads the table once and loops over
             // its ants (large colonies do not re-stage the table per wave)
             h->cons_warps = w;
-            h->cons_grid = std::max(1, std::min(h->num_sms, (h->m_local + w - 1) / w));
+            h->cons_grid = std::max(1, std::min(sms, (h->m_local + w - 1) / w));
             h->cons_smem = need;
             // fused update (construct.cuh fused_update): one iteration = one launch.  Needs the
             // whole grid resident (grid <= SMs, one block each), one candidate slot per lane,
             // no exchange or local search between construction and update, and room for each
             // warp's tau + heur rows in the block's shared memory
             const size_t fused_need = 256 + (size_t)w * 2 * 4 * h->ld;
-            const bool fusable = !c.local_search && h->slots == 1 && !c.separate_update &&
+            const bool fusable = !c.local_search && h->slots == 1 && !c.separate_update && !h->lean &&
                                  std::max(need, fused_need) <= cons_dyn_max;
             h->fuse_update = fusable && c.world == 1;
             h->fuse_peers = fusable && c.world > 1 && h->m_local > 0;
@@ -778,6 +890,8 @@ int setup(mmas_ctx* h) {
     }
     allow_max_smem(pheromone_update_kernel, h->smem_optin);
     CU(cudaGetLastError());
+    // the one-launch iteration only where its whole grid fits on the device at once
+    if ((h->fuse_update || h->fuse_peers) && !grid_co_resident(h)) h->fuse_update = h->fuse_peers = false;
     CU(cudaStreamSynchronize(h->stream));
     return MMAS_OK;
 }
@@ -807,6 +921,17 @@ int validate(const mmas_config* c) {
     if (c->selection == MMAS_SELECT_RWM && c->fallback == MMAS_FALLBACK_ARGMAX)
         return fail(MMAS_EINVAL, "selection = MMAS_SELECT_RWM uses the roulette wheel as its fallback (R28)");
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(MMAS_EINVAL, "need 0 <= rank < world");
+    if (c->colonies < 0 || c->colonies > 65535) return fail(MMAS_EINVAL, "colonies must satisfy 0 <= k <= 65535 (0 = 1)");
+    if (c->pheromone != MMAS_PHEROMONE_DENSE && c->pheromone != MMAS_PHEROMONE_LEAN)
+        return fail(MMAS_EINVAL, "pheromone must be MMAS_PHEROMONE_*");
+    if (c->pheromone == MMAS_PHEROMONE_LEAN &&
+        (c->cand_len < 1 || !is_int_in(c->beta, 0, 8) || c->selection != MMAS_SELECT_WRS ||
+         c->fallback != MMAS_FALLBACK_WRS || c->colonies > 1))
+        return fail(MMAS_EINVAL, "pheromone = MMAS_PHEROMONE_LEAN needs cand_len >= 1, integer beta in [0, 8], WRS "
+                                 "selection and fallback, one colony (R30)");
+    if (c->colonies > 1 && c->world != 1)
+        return fail(MMAS_EINVAL, "concurrent colonies (colonies > 1) need world == 1 (shard independent colonies "
+                                 "over ranks instead: each rank its own context)");
     double lo_x = INFINITY, hi_x = -INFINITY, lo_y = INFINITY, hi_y = -INFINITY;
     for (int i = 0; i < c->n; ++i) {
         const double x = c->coords[2 * i], y = c->coords[2 * i + 1];
@@ -885,9 +1010,15 @@ mmas_ctx* mmas_create(const double* coords, int32_t n, double alpha, double beta
 
 int64_t mmas_record_bytes(const mmas_ctx* h) { return h ? h->rec_bytes : fail(MMAS_EINVAL, "context is NULL"); }
 
+static int single_colony(mmas_ctx* h) {
+    return h->colonies == 1 ? MMAS_OK
+                            : fail(MMAS_ESTATE, "the split / exchange calls serve sharded single colonies (colonies == 1)");
+}
+
 int mmas_construct(mmas_ctx* h, void* record_dev) {
     int st = check(h);
     if (st) return st;
+    if ((st = single_colony(h))) return st;
     if (!record_dev) return fail(MMAS_EINVAL, "record_dev is NULL");
     CU(cudaSetDevice(h->device));
     if ((st = launch_construct(h, false))) return st;
@@ -916,8 +1047,6 @@ static int ensure_xbuf(mmas_ctx* h) {
     const size_t bytes = (size_t)mmas_exchange_bytes(h);
     CU(cudaMalloc(reinterpret_cast<void**>(&h->xbuf), bytes));   // cudaMalloc: IPC-exportable
     CU(cudaMemset(h->xbuf, 0, bytes));
-    CU(cudaMalloc(reinterpret_cast<void**>(&h->xerr), sizeof(uint32_t)));
-    CU(cudaMemset(h->xerr, 0, sizeof(uint32_t)));
     CU(cudaMalloc(reinterpret_cast<void**>(&h->xpeers_dev), sizeof(unsigned char*) * h->cfg.world));
     return MMAS_OK;
 }
@@ -951,6 +1080,20 @@ int mmas_exchange_attach(mmas_ctx* h, void* const* peer_buffers) {
     for (int p = 0; p < h->cfg.world; ++p) {
         v[p] = p == h->cfg.rank ? h->xbuf : static_cast<unsigned char*>(peer_buffers[p]);
         if (!v[p]) return fail(MMAS_EINVAL, "peer buffer is NULL");
+        // a buffer on another device: the exchange kernels store into it and poll its flags
+        // over NVLink, which needs peer access from this context's device
+        cudaPointerAttributes pa{};
+        CU(cudaPointerGetAttributes(&pa, v[p]));
+        if (pa.type == cudaMemoryTypeDevice && pa.device != h->device) {
+            int can = 0;
+            CU(cudaDeviceCanAccessPeer(&can, h->device, pa.device));
+            if (!can)
+                return fail(MMAS_ECUDA, "device " + std::to_string(h->device) + " cannot access the exchange buffer "
+                                        "on device " + std::to_string(pa.device) + " (no peer access)");
+            const cudaError_t e = cudaDeviceEnablePeerAccess(pa.device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else if (e != cudaSuccess) return fail(MMAS_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+        }
     }
     CU(cudaMemcpy(h->xpeers_dev, v.data(), sizeof(unsigned char*) * v.size(), cudaMemcpyHostToDevice));
     h->xattached = true;
@@ -981,6 +1124,7 @@ static ExchangeArgs exchange_args(mmas_ctx* h) {
     X.rec_bytes = h->rec_bytes;
     X.parity = (uint32_t)h->iteration & 1u;
     X.seq = (uint32_t)h->iteration + 1u;
+    X.spin_bound = h->spin_bound;
     return X;
 }
 
@@ -1037,20 +1181,28 @@ int mmas_iterate_exchange(mmas_ctx* h, int32_t iters) {
     return MMAS_OK;
 }
 
-int mmas_exchange_status(mmas_ctx* h) {
+int mmas_device_status(mmas_ctx* h) {
     int st = check(h);
     if (st) return st;
-    if (!h->xerr) return MMAS_OK;
     CU(cudaSetDevice(h->device));
     uint32_t e = 0;
     CU(cudaMemcpyAsync(&e, h->xerr, sizeof(e), cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
-    return e ? fail(MMAS_ENCCL, "peer exchange timed out waiting for a rank's record") : MMAS_OK;
+    if (e & kErrPeerTimeout)
+        return fail(MMAS_ETIMEDOUT, "peer exchange timed out waiting for a rank's record; the selection and "
+                                    "update have been skipped since (the trails are those of the last complete iteration)");
+    if (e & kErrGridBarrier)
+        return fail(MMAS_ETIMEDOUT, "the fused launch's grid barrier timed out (a block was not resident); the "
+                                    "update has been skipped since");
+    return MMAS_OK;
 }
+
+int mmas_exchange_status(mmas_ctx* h) { return mmas_device_status(h); }
 
 int mmas_update(mmas_ctx* h, const void* records_dev, int32_t count) {
     int st = check(h);
     if (st) return st;
+    if ((st = single_colony(h))) return st;
     if (!records_dev || count < 1) return fail(MMAS_EINVAL, "need records_dev != NULL and count >= 1");
     CU(cudaSetDevice(h->device));
     if ((st = launch_select(h, (const unsigned char*)records_dev, count))) return st;
@@ -1083,8 +1235,9 @@ int64_t mmas_best_tour(mmas_ctx* h, int32_t* tour_out) {
     CU(cudaSetDevice(h->device));
     long long len = -1;
     std::vector<uint16_t> r((size_t)h->n);
-    CU(cudaMemcpyAsync(&len, h->gb_len, sizeof(len), cudaMemcpyDeviceToHost, h->stream));
-    CU(cudaMemcpyAsync(r.data(), h->gb_route, sizeof(uint16_t) * h->n, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(&len, h->gb_len + h->view, sizeof(len), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(r.data(), h->gb_route + (size_t)h->view * h->cs.vec, sizeof(uint16_t) * h->n,
+                       cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     if (len < 0) return fail(MMAS_ESTATE, "no global best yet (run at least one iteration)");
     for (int i = 0; i < h->n; ++i) tour_out[i] = r[i];
@@ -1096,7 +1249,7 @@ int64_t mmas_best_length(mmas_ctx* h) {
     if (st) return st;
     CU(cudaSetDevice(h->device));
     long long len = -1;
-    CU(cudaMemcpyAsync(&len, h->gb_len, sizeof(len), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(&len, h->gb_len + h->view, sizeof(len), cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     if (len < 0) return fail(MMAS_ESTATE, "no global best yet (run at least one iteration)");
     return len;
@@ -1107,13 +1260,23 @@ int mmas_best_length_async(mmas_ctx* h, int64_t* host_dst) {
     if (st) return st;
     if (!host_dst) return fail(MMAS_EINVAL, "host_dst is NULL");
     CU(cudaSetDevice(h->device));
-    CU(cudaMemcpyAsync(host_dst, h->gb_len, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(host_dst, h->gb_len + h->view, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
     return MMAS_OK;
 }
 
 void mmas_destroy(mmas_ctx* h) { free_ctx(h); }
 
 int32_t mmas_n(const mmas_ctx* h) { return h ? h->n : 0; }
+
+int mmas_select_colony(mmas_ctx* h, int32_t colony) {
+    int st = check(h);
+    if (st) return st;
+    if (colony < 0 || colony >= h->colonies) return fail(MMAS_EINVAL, "colony out of range");
+    h->view = colony;
+    return MMAS_OK;
+}
+
+int32_t mmas_colonies(const mmas_ctx* h) { return h ? h->colonies : 0; }
 int32_t mmas_iteration(const mmas_ctx* h) { return h ? h->iteration : 0; }
 
 int mmas_get_tours(mmas_ctx* h, int32_t* out, int32_t* first_ant, int32_t* count) {
@@ -1124,7 +1287,8 @@ int mmas_get_tours(mmas_ctx* h, int32_t* out, int32_t* first_ant, int32_t* count
     if (!out) return MMAS_OK;
     CU(cudaSetDevice(h->device));
     std::vector<uint16_t> r((size_t)std::max(h->m_local, 1) * h->ldr);
-    CU(cudaMemcpyAsync(r.data(), h->routes, sizeof(uint16_t) * r.size(), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(r.data(), h->routes + (size_t)h->view * h->cs.routes, sizeof(uint16_t) * r.size(),
+                       cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     for (int a = 0; a < h->m_local; ++a)
         for (int k = 0; k < h->n; ++k) out[(size_t)a * h->n + k] = r[(size_t)a * h->ldr + k];
@@ -1136,7 +1300,8 @@ int mmas_get_lengths(mmas_ctx* h, int64_t* out) {
     if (st) return st;
     if (!out) return fail(MMAS_EINVAL, "out is NULL");
     CU(cudaSetDevice(h->device));
-    CU(cudaMemcpyAsync(out, h->lengths, sizeof(int64_t) * h->m_local, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(out, h->lengths + (size_t)h->view * h->cs.ants, sizeof(int64_t) * h->m_local,
+                       cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     return MMAS_OK;
 }
@@ -1152,9 +1317,75 @@ static int get_matrix(mmas_ctx* h, const float* src, float* out) {
     return MMAS_OK;
 }
 
-int mmas_get_pheromone(mmas_ctx* h, float* out) { return get_matrix(h, h ? h->tau : nullptr, out); }
-int mmas_get_inv_w(mmas_ctx* h, float* out) { return get_matrix(h, h ? h->inv_w : nullptr, out); }
-int mmas_get_heuristic(mmas_ctx* h, float* out) { return get_matrix(h, h ? h->heur : nullptr, out); }
+// Lean mode (R30): the dense n x n view of tau (which = 0), inv_w (1) or eta^beta (2), expanded
+// on the host from the background trail, the candidate trails and the sparse rows; eta^beta
+// and the background's 1 / choice_info with the device's arithmetic (R12, R18, R19)
+static int lean_expand(mmas_ctx* h, int which, float* out) {
+    int st = check(h);
+    if (st) return st;
+    if (!out) return fail(MMAS_EINVAL, "out is NULL");
+    CU(cudaSetDevice(h->device));
+    const int n = h->n, cl = h->cl_ld, cap = h->lean_cap;
+    std::vector<double> xy(2 * (size_t)n);
+    std::vector<uint16_t> cid((size_t)n * cl), sid((size_t)n * cap);
+    std::vector<float> cv((size_t)n * cl), sv((size_t)n * cap);
+    float bg = 0.f;
+    const float* cand_src = which == 0 ? h->cand_tau : which == 1 ? h->cand_inv : h->cand_heur;
+    const float* sp_src = which == 0 ? h->sp_tau : h->sp_inv;
+    CU(cudaMemcpyAsync(xy.data(), h->xy, sizeof(double) * xy.size(), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(cid.data(), h->cand_id, sizeof(uint16_t) * cid.size(), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(cv.data(), cand_src, sizeof(float) * cv.size(), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(sid.data(), h->sp_id, sizeof(uint16_t) * sid.size(), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(sv.data(), sp_src, sizeof(float) * sv.size(), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(&bg, h->bg + (h->iteration & 1), sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    const int beta = (int)h->cfg.beta;
+    float ba = 1.0f;   // pow_alpha(bg): repeated fp32 multiplication (R17)
+    if (h->alpha >= 1) {
+        ba = bg;
+        for (int k = 1; k < h->alpha; ++k) ba = ba * bg;
+    }
+    for (int i = 0; i < n; ++i) {
+        float* row = out + (size_t)i * n;
+        for (int j = 0; j < n; ++j) {
+            if (which == 0) {
+                row[j] = bg;
+                continue;
+            }
+            const int32_t d = host_dist(xy.data(), i, j);
+            double Db = 1.0;
+            for (int k = 0; k < beta; ++k) Db = Db * (double)(d > 1 ? d : 1);
+            const float heur = (float)(1.0 / Db);
+            row[j] = which == 2 ? heur : 1.0f / (ba * heur);
+        }
+        for (int k = 0; k < cl; ++k) row[cid[(size_t)i * cl + k]] = cv[(size_t)i * cl + k];
+        if (which != 2)
+            for (int k = 0; k < cap; ++k)
+                if (sid[(size_t)i * cap + k] != kLeanEmpty) row[sid[(size_t)i * cap + k]] = sv[(size_t)i * cap + k];
+    }
+    return MMAS_OK;
+}
+
+int mmas_get_pheromone(mmas_ctx* h, float* out) {
+    if (h && h->lean) return lean_expand(h, 0, out);
+    return get_matrix(h, h ? h->tau + (size_t)h->view * h->cs.nn : nullptr, out);
+}
+int mmas_get_inv_w(mmas_ctx* h, float* out) {
+    if (h && h->lean) return lean_expand(h, 1, out);
+    return get_matrix(h, h ? h->inv_w + (size_t)h->view * h->cs.nn : nullptr, out);
+}
+int mmas_get_heuristic(mmas_ctx* h, float* out) {
+    if (h && h->lean) return lean_expand(h, 2, out);
+    return get_matrix(h, h ? h->heur : nullptr, out);
+}
+
+int64_t mmas_pheromone_bytes(const mmas_ctx* h) {
+    if (!h) return MMAS_EINVAL;
+    const int64_t ncl = (int64_t)h->n * h->cl_ld;
+    if (h->lean)   // candidate trails + eta^beta + 1/w, sparse id + trail + 1/w
+        return ncl * 12 + (int64_t)h->n * h->lean_cap * 10;
+    return (int64_t)3 * h->n * h->ld * 4 * h->colonies + ncl * 4 * h->colonies;   // tau, inv_w, heur + cand_inv
+}
 
 int mmas_get_candidates(mmas_ctx* h, int32_t* out) {
     int st = check(h);
@@ -1175,7 +1406,7 @@ int mmas_get_limits(mmas_ctx* h, float* tau_min, float* tau_max) {
     if (st) return st;
     CU(cudaSetDevice(h->device));
     float s[4];
-    CU(cudaMemcpyAsync(s, h->scal, sizeof(s), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(s, h->scal + 4 * h->view, sizeof(s), cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     if (tau_min) *tau_min = s[0];
     if (tau_max) *tau_max = s[1];
@@ -1192,7 +1423,7 @@ int mmas_get_stats(mmas_ctx* h, mmas_stats* out) {
     CU(cudaStreamSynchronize(h->stream));
     out->iterations = h->iteration;
     out->fallback_steps = (int64_t)fb;
-    out->ant_steps = (int64_t)h->iteration * h->m_local * (h->n - 1);
+    out->ant_steps = (int64_t)h->iteration * h->m_local * (h->n - 1) * h->colonies;
     out->ants_local = h->m_local;
     out->first_ant = h->ant_lo;
     out->local_search_moves = 0;
@@ -1285,6 +1516,19 @@ int mmas_sync(mmas_ctx* h) {
 
 // Debug: copy the construct_cl_kernel phase timestamps (a -DMMAS_TRACE build; see
 // tools/trace_phases.py).  Not part of the documented ABI; MMAS_ESTATE otherwise.
+// Debug: fallback-scan cycles (sum, count) since load (a -DMMAS_TRACE build), and reset.
+extern "C" int mmas_debug_fb_cycles(unsigned long long* out) {
+#ifdef MMAS_TRACE
+    if (cudaMemcpyFromSymbol(out, mmas::g_fbcyc, 2 * sizeof(unsigned long long)) != cudaSuccess) return MMAS_ECUDA;
+    const unsigned long long z[2] = {0ull, 0ull};
+    if (cudaMemcpyToSymbol(mmas::g_fbcyc, z, sizeof(z)) != cudaSuccess) return MMAS_ECUDA;
+    return MMAS_OK;
+#else
+    (void)out;
+    return MMAS_ESTATE;
+#endif
+}
+
 extern "C" int mmas_debug_trace(unsigned long long* out, int count) {
 #ifdef MMAS_TRACE
     if (!out || count < 0 || count > 1024 * 8) return MMAS_EINVAL;

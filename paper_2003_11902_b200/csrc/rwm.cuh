@@ -54,6 +54,7 @@ __device__ __forceinline__ int rwm_select(WF&& wf, int len, float u, int lane) {
 // R27) in shared memory.  One uniform per step: counter (0x20000000, s, a, it), word 0.
 template <bool kCT>
 __global__ void __launch_bounds__(128) construct_rwm_kernel(ConstructArgs A) {
+    if (blockIdx.y) colony_offset(A, (int)blockIdx.y);
     pdl_wait();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;

@@ -27,6 +27,13 @@ struct TwoOptArgs {
     uint32_t* inq;                     // m_local x nwords scratch ("don't-look bit" clear <=> queued)
     unsigned long long* moves;         // total applied moves (stats)
 };
+__device__ __forceinline__ void colony_offset(TwoOptArgs& T, ConstructArgs& A, int c) {
+    T.routes += c * A.cs.routes;
+    T.pos += c * A.cs.routes;
+    T.queue += c * A.cs.routes;
+    T.inq += (long long)c * A.cs.inq;
+    colony_offset(A, c);
+}
 
 // ---- coordinates and EUC_2D distances of the local search --------------------------
 // kIntXY: every coordinate is an integer with |x|, |y| <= 16383 (checked at setup), so
@@ -237,6 +244,7 @@ namespace mmas {
 // output replaces the ant's tour).
 template <bool kInt>
 __global__ void __launch_bounds__(128) two_opt_kernel(TwoOptArgs T, ConstructArgs A) {
+    if (blockIdx.y) colony_offset(T, A, (int)blockIdx.y);
     pdl_wait();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -338,6 +346,7 @@ __device__ __forceinline__ MoveEval eval_node(const TwoOptArgs& T, const uint16_
 
 template <bool kInt>
 __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs T, ConstructArgs A) {
+    if (blockIdx.y) colony_offset(T, A, (int)blockIdx.y);
     pdl_wait();
     extern __shared__ __align__(16) uint16_t ls_smem[];
     __shared__ uint4 s_eval[kLsWarps];

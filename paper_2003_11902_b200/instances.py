@@ -104,6 +104,7 @@ class Workload:
     mmas_seed: int = 42
     tabu: int = 0         # full-row tabu: 0 = bitmask (BT), 1 = compact (CT, R27)
     selection: int = 0    # node selection: 0 = WRS (Alg. 3), 1 = parallel roulette wheel (R28)
+    colonies: int = 1     # concurrent independent colonies, colony c seeded mmas_seed + c (R29)
 
     def coords(self) -> np.ndarray:
         return make_coords(self.shape, self.n, self.seed)
@@ -139,4 +140,8 @@ CONFIGS = {
     "C4RWMCT": Workload("pr2392-shaped, roulette wheel, compact tabu", 2392, 2392, 0, 100, 0.5, 0, "pr2392", 2392,
                         tabu=1, selection=1),
     "C5": Workload("d18512-shaped", 18512, 800, 32, 20, 0.7, 1, "d18512", 18512),
+    # 8 concurrent independent pr1002-shaped colonies (the paper's repeated-run
+    # protocol P:1143-1145) in one context, every launch running all eight
+    "C2x8": Workload("pr1002-shaped, 8 concurrent colonies", 1002, 1002, 32, 1000, 0.5, 0, "pr1002", 1002,
+                     colonies=8),
 }

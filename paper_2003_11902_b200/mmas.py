@@ -16,11 +16,12 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # tools/trace_phases.py makes); the CUDA path is the only path either way
 LIB_PATH = os.environ.get("MMAS_LIB") or os.path.join(_HERE, "libmmas.so")
 
-MMAS_OK, MMAS_EINVAL, MMAS_ENOMEM, MMAS_ECUDA, MMAS_ENCCL, MMAS_ESTATE = 0, -1, -2, -3, -4, -5
+MMAS_OK, MMAS_EINVAL, MMAS_ENOMEM, MMAS_ECUDA, MMAS_ENCCL, MMAS_ESTATE, MMAS_ETIMEDOUT = 0, -1, -2, -3, -4, -5, -6
 DEPOSIT_ITERATION_BEST, DEPOSIT_GLOBAL_BEST = 0, 1
 FALLBACK_WRS, FALLBACK_ARGMAX = 0, 1
 TABU_BITMASK, TABU_COMPACT = 0, 1
 SELECT_WRS, SELECT_RWM = 0, 1
+PHEROMONE_DENSE, PHEROMONE_LEAN = 0, 1
 
 # every symbol include/mmas.h declares (checked by tests/test_capi.py)
 EXPORTED = (
@@ -29,8 +30,8 @@ EXPORTED = (
     "mmas_best_length_async", "mmas_destroy",
     "mmas_exchange_bytes", "mmas_exchange_buffer", "mmas_exchange_ipc_handle", "mmas_exchange_open_ipc",
     "mmas_exchange_attach", "mmas_construct_publish", "mmas_update_exchange", "mmas_iterate_exchange",
-    "mmas_exchange_status",
-    "mmas_n", "mmas_iteration", "mmas_get_tours", "mmas_get_lengths", "mmas_get_pheromone",
+    "mmas_exchange_status", "mmas_device_status",
+    "mmas_select_colony", "mmas_colonies", "mmas_pheromone_bytes", "mmas_n", "mmas_iteration", "mmas_get_tours", "mmas_get_lengths", "mmas_get_pheromone",
     "mmas_get_inv_w", "mmas_get_heuristic", "mmas_get_candidates", "mmas_get_limits",
     "mmas_get_stats", "mmas_profile", "mmas_get_phase_times", "mmas_kernel_launches",
     "mmas_stream", "mmas_sync", "mmas_debug_philox", "mmas_debug_log2",
@@ -52,6 +53,7 @@ class Config(ctypes.Structure):
         ("local_search", ctypes.c_int32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
         ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("use_caller_stream", ctypes.c_int32),
         ("tabu", ctypes.c_int32), ("selection", ctypes.c_int32), ("separate_update", ctypes.c_int32),
+        ("colonies", ctypes.c_int32), ("pheromone", ctypes.c_int32),
     ]
 
 
@@ -99,6 +101,14 @@ def lib():
     L.mmas_exchange_attach.argtypes = [V, ctypes.POINTER(ctypes.c_void_p)]
     for name in ("mmas_construct_publish", "mmas_update_exchange", "mmas_exchange_status"):
         getattr(L, name).argtypes = [V]
+    # symbols newer than round 1: an older in-tree build (A/B runs) may lack them;
+    # tests/test_capi.py fails loudly on a library that does not export every one
+    for name, args, res in (("mmas_device_status", [V], None), ("mmas_select_colony", [V, ctypes.c_int32], None),
+                            ("mmas_colonies", [V], None), ("mmas_pheromone_bytes", [V], ctypes.c_int64)):
+        if hasattr(L, name):
+            getattr(L, name).argtypes = args
+            if res is not None:
+                getattr(L, name).restype = res
     L.mmas_iterate_exchange.argtypes = [V, ctypes.c_int32]
     L.mmas_best_tour.argtypes = [V, P(ctypes.c_int32)]
     L.mmas_best_tour.restype = ctypes.c_int64
@@ -145,7 +155,7 @@ class Colony:
     def __init__(self, coords, n_ants, cand_len, alpha=1.0, beta=2.0, rho=0.5, seed=42, p_best=0.01,
                  deposit_global=False, fallback_argmax=False, local_search=False, device=-1, stream=None,
                  rank=0, world=1, tabu=TABU_BITMASK, selection=SELECT_WRS,
-                 separate_update=False):
+                 separate_update=False, colonies=1, pheromone=PHEROMONE_DENSE):
         L = lib()
         c = np.ascontiguousarray(coords, dtype=np.float64).reshape(-1, 2)
         self.n = c.shape[0]
@@ -172,6 +182,8 @@ class Colony:
         cfg.tabu = int(tabu)
         cfg.selection = int(selection)
         cfg.separate_update = int(bool(separate_update))
+        cfg.colonies = int(colonies)
+        cfg.pheromone = int(pheromone)
         h = ctypes.c_void_p()
         _err(L.mmas_create_ex(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h
@@ -238,6 +250,10 @@ class Colony:
     def exchange_status(self):
         _err(lib().mmas_exchange_status(self._h))
 
+    def status(self):
+        """Raises MMASError (MMAS_ETIMEDOUT) if a bounded device-side wait gave up."""
+        _err(lib().mmas_device_status(self._h))
+
     def update(self, records_dev_ptr: int, count: int):
         _err(lib().mmas_update(self._h, ctypes.c_void_p(records_dev_ptr), int(count)))
 
@@ -262,6 +278,18 @@ class Colony:
         _err(lib().mmas_best_length_async(self._h, ctypes.c_void_p(host_ptr)))
 
     # -- introspection --
+    @property
+    def colonies(self):
+        return int(lib().mmas_colonies(self._h))
+
+    @property
+    def pheromone_bytes(self):
+        return int(lib().mmas_pheromone_bytes(self._h))
+
+    def select_colony(self, colony: int):
+        """Introspection and best_tour/best_length report colony `colony` from now on."""
+        _err(lib().mmas_select_colony(self._h, int(colony)))
+
     @property
     def iteration(self):
         return int(lib().mmas_iteration(self._h))

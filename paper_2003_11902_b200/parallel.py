@@ -74,8 +74,12 @@ class PeerShardedColony:
         self.colony.exchange_open_ipc(handles)
         dist.barrier(group=group)
 
-    def iterate(self, iters: int = 1):
+    def iterate(self, iters: int = 1, check: bool = True):
+        """`iters` iterations; with check (default) synchronises once at the end and raises if
+        a peer's record did not arrive (the device-side wait is bounded, mmas_status)."""
         self.colony.iterate_exchange(iters)
+        if check:
+            self.colony.status()
 
     def best_tour(self):
         return self.colony.best_tour()

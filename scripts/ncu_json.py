@@ -16,9 +16,12 @@ WANT = {"dram__bytes_read.sum": "dram_bytes_read", "dram__bytes_write.sum": "dra
         "smsp__inst_executed.sum": "inst_executed", "gpu__time_duration.sum": "duration", "sm__inst_executed.sum": "sm_inst_executed",
         "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
         "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
-        "lts__t_bytes.sum": "l2_bytes"}
+        "lts__t_bytes.sum": "l2_bytes", "lts__t_sectors_op_read.sum": "l2_sectors_read",
+        "lts__t_sectors_op_write.sum": "l2_sectors_write", "lts__t_sectors_op_atom.sum": "l2_sectors_atom",
+        "lts__t_sectors_op_red.sum": "l2_sectors_red", "sm__cycles_elapsed.avg": "sm_cycles"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "inst": 1, "ns": 1e-3, "us": 1, "usecond": 1,
-         "ms": 1e3, "msecond": 1e3, "%": 1, "": 1}
+         "ms": 1e3, "msecond": 1e3, "%": 1, "": 1, "sector": 1, "Ksector": 1e3, "Msector": 1e6, "cycle": 1,
+         "Kcycle": 1e3, "Mcycle": 1e6}
 
 
 def main():
@@ -51,7 +54,8 @@ def main():
                     e["duration_us"] = val * SCALE.get(units[i], 1)
                 else:
                     e[key] = val * SCALE.get(units[i], 1)
-        for k in ("dram_bytes_read", "dram_bytes_write", "inst_executed", "l2_bytes"):
+        for k in ("dram_bytes_read", "dram_bytes_write", "inst_executed", "l2_bytes", "l2_sectors_read",
+                  "l2_sectors_write", "l2_sectors_atom", "l2_sectors_red"):
             if k in e:
                 e[k] = int(round(e[k]))
         d.setdefault(cfg, {})[kern] = e

@@ -24,6 +24,13 @@ print("kernel:", v[h.index("Kernel Name")] if "Kernel Name" in h else "?")
 for name in want:
     if name in h:
         print(f"  {name:60s} {v[h.index(name)]} {raw[1][h.index(name)]}")
+# every L2 / DRAM byte and sector counter of the capture (the memory-side roofline evidence)
+for name, val, unit in zip(h, v, raw[1]):
+    if name in want:
+        continue
+    if (name.startswith("lts__t_sectors") or name.startswith("lts__t_bytes") or name.startswith("dram__bytes")
+            or name.startswith("lts__throughput") or name.startswith("l1tex__t_bytes")) and not name.endswith("_lookup_hit"):
+        print(f"  {name:60s} {val} {unit}")
 stalls = []
 for name, val in zip(h, v):
     if name.startswith("smsp__pcsamp_warps_issue_stalled_") and not name.endswith("not_issued"):
