@@ -182,6 +182,7 @@ def workload_config(w, args, world):
                         + (f" per colony x {w.colonies} colonies" if w.colonies > 1 else "")
                         + f", cl={w.cand_len}, rho={w.rho}, alpha=1, beta=2",
             "n": w.n, "n_ants": w.n_ants, "global_ants": m_total, "cand_len": w.cand_len, "colonies": w.colonies,
+            "pheromone": "lean (R30)" if w.pheromone else "dense n x n",
             "scaling": args.scaling, "tabu": "compact" if w.tabu else "bitmask",
             "selection": "roulette wheel" if w.selection else "WRS",
             "local_search": "2-opt" if w.local_search else "none",
@@ -276,7 +277,8 @@ def run_ours(args):
     col = mmas.Colony(coords, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
                       separate_update=args.separate_update,
                       local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection,
-                      stream=stream, rank=rank, world=world, colonies=w.colonies)
+                      stream=stream, rank=rank, world=world, colonies=w.colonies,
+                      pheromone=w.pheromone)
     rb = col.record_bytes
     local = torch.zeros(rb, dtype=torch.uint8, device="cuda")
     gathered = torch.zeros(world * rb, dtype=torch.uint8, device="cuda")
@@ -362,7 +364,9 @@ def run_ours(args):
     # world == 1 with the table in shared memory: the update (row a6) runs inside the same
     # launch (construct.cuh fused_update), so that launch also moves the update's 16 n^2 B
     fused = bool(col.stats()["update_fused"]) and (world == 1 or exchange == "p2p")
-    upd_bytes = 16 * w.n * w.n * K
+    # dense: read tau + heur, write tau + inv_w (16 n^2 B); lean (R30): every stored trail read
+    # and written once with its 1 / choice_info (2 x the pheromone state)
+    upd_bytes = 2 * col.pheromone_bytes if w.pheromone else 16 * w.n * w.n * K
     if fused:
         bytes_per_launch += upd_bytes
     hbm_peak, peak_src = measured_peaks()
@@ -456,7 +460,8 @@ def run_ours(args):
         c = mmas.Colony(pinned, m_total, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=dev,
                         separate_update=args.separate_update,
                         local_search=bool(w.local_search), tabu=w.tabu, selection=w.selection,
-                        stream=stream, rank=rank, world=world, colonies=w.colonies)
+                        stream=stream, rank=rank, world=world, colonies=w.colonies,
+                      pheromone=w.pheromone)
         if exchange == "p2p":
             wire_p2p(c)
         return c
@@ -524,6 +529,7 @@ def run_ours(args):
                                      "collective": f"{backend} all-gather of the records",
                                      "none": "none (one GPU)"}[exchange],
                         "timed_iterations": [args.warmup, args.warmup + args.steps - 1],
+                        "pheromone_bytes": col.pheromone_bytes,
                         "iteration_launches": "one (construction + selection + update fused)" if fused else
                                               "construction (+ selection) then update",
                         "paper_context": PAPER_CONTEXT.get(args.config, "") + " (other hardware, context only)"},

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <utility>
 #include <cmath>
 #include <cstdio>
@@ -591,7 +592,23 @@ bool grid_co_resident(mmas_ctx* h) {
     return (long long)per_sm * h->num_sms >= (long long)h->cons_grid * h->colonies;
 }
 
+// MMAS_CREATE_PROFILE=1: host wall time of each setup phase on stderr (the e2e number's
+// create share, bench.py)
+struct SetupClock {
+    bool on = std::getenv("MMAS_CREATE_PROFILE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), t = t0;
+    void mark(const char* what, cudaStream_t st) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "mmas_create %-28s %8.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 int setup(mmas_ctx* h) {
+    SetupClock clk;
     const mmas_config& c = h->cfg;
     const int n = c.n;
     if (c.device >= 0) CU(cudaSetDevice(c.device));
@@ -647,6 +664,7 @@ int setup(mmas_ctx* h) {
         (st = dalloc(&h->xerr, 1)))
         return st;
 
+    clk.mark("device / stream / allocations", h->stream);
     CU(cudaMemcpyAsync(h->xy, c.coords, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, h->stream));
     CU(cudaMemsetAsync(h->routes, 0, sizeof(uint16_t) * ma * h->ldr * K, h->stream));
     CU(cudaMemsetAsync(h->lengths, 0, sizeof(long long) * ma * K, h->stream));
@@ -679,6 +697,7 @@ int setup(mmas_ctx* h) {
         CU(cudaStreamSynchronize(h->stream));
     }
 
+    clk.mark("memsets + eta^beta", h->stream);
     // candidate lists (host, parallel over rows)
     if (h->cl > 0) {
         std::vector<uint16_t> cand;
@@ -737,6 +756,7 @@ int setup(mmas_ctx* h) {
         CU(cudaStreamSynchronize(h->stream));
     }
 
+    clk.mark("candidate + 2-opt lists", h->stream);
     // initial limits from the NN tour (Alg. 1); F from libm pow (R2)
     {
         // NN tour on the device (one block; the host loop was O(n^2) on one core)
@@ -788,6 +808,7 @@ int setup(mmas_ctx* h) {
     }
     CU(cudaStreamSynchronize(h->stream));   // lim goes out of scope
 
+    clk.mark("NN tour + trails", h->stream);
     // ---- construction launch plan ----
     // dynamic shared memory a construction kernel may take: the opt-in limit minus its
     // static shared memory (block_finish's slots; 128 B, reserve 1 KB)
@@ -890,8 +911,10 @@ int setup(mmas_ctx* h) {
     }
     allow_max_smem(pheromone_update_kernel, h->smem_optin);
     CU(cudaGetLastError());
+    clk.mark("launch plan + attributes", h->stream);
     // the one-launch iteration only where its whole grid fits on the device at once
     if ((h->fuse_update || h->fuse_peers) && !grid_co_resident(h)) h->fuse_update = h->fuse_peers = false;
+    clk.mark("co-residency check", h->stream);
     CU(cudaStreamSynchronize(h->stream));
     return MMAS_OK;
 }

@@ -105,6 +105,7 @@ class Workload:
     tabu: int = 0         # full-row tabu: 0 = bitmask (BT), 1 = compact (CT, R27)
     selection: int = 0    # node selection: 0 = WRS (Alg. 3), 1 = parallel roulette wheel (R28)
     colonies: int = 1     # concurrent independent colonies, colony c seeded mmas_seed + c (R29)
+    pheromone: int = 0    # 0 = dense n x n matrices, 1 = memory-lean (R30, same results)
 
     def coords(self) -> np.ndarray:
         return make_coords(self.shape, self.n, self.seed)
@@ -142,6 +143,11 @@ CONFIGS = {
     "C5": Workload("d18512-shaped", 18512, 800, 32, 20, 0.7, 1, "d18512", 18512),
     # 8 concurrent independent pr1002-shaped colonies (the paper's repeated-run
     # protocol P:1143-1145) in one context, every launch running all eight
+    # the memory-lean pheromone (R30) on the d18512 workload (~20 MB of pheromone
+    # state instead of 3 x 1.37 GB) and on the largest u16 instance (n = 65535)
+    "C5L": Workload("d18512-shaped, lean pheromone", 18512, 800, 32, 20, 0.7, 1, "d18512", 18512, pheromone=1),
+    "C65KL": Workload("65535-city uniform, lean pheromone", 65535, 800, 32, 10, 0.7, 0, "uniform", 65535,
+                      pheromone=1),
     "C2x8": Workload("pr1002-shaped, 8 concurrent colonies", 1002, 1002, 32, 1000, 0.5, 0, "pr1002", 1002,
                      colonies=8),
 }
