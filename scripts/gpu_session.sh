@@ -23,13 +23,17 @@ if has smoke; then
   tail -2 $OUT/smoke.log
 fi
 if has bench; then
-  timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
-  head -c 600 $OUT/bench.json; echo
+  # the driver's command (iterations 5-24) and the default (steady state, 1000 steps)
+  timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench_driver.json 2> $OUT/bench_driver.err; echo "bench rc=$?" >> $OUT/bench_driver.err
+  head -c 400 $OUT/bench_driver.json; echo
+  MMAS_CREATE_PROFILE=1 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
+  head -c 400 $OUT/bench.json; echo
 fi
-for cfg in C1 C3 C4 C4CT C5 C2RWM C4RWM C4RWMCT; do
+for cfg in C1 C3 C4 C4CT C5 C5L C65KL C2x8 C2RWM C4RWM C4RWMCT; do
   if has bench$cfg; then
-    steps=50; [[ $cfg == C4* ]] && steps=20; [ $cfg == C5 ] && steps=6; [ $cfg == C2RWM ] && steps=200
-    timeout 1200 python bench.py --config $cfg --steps $steps --warmup 3 --no-cpu-baseline > $OUT/bench_$cfg.json 2> $OUT/bench_$cfg.err
+    steps=50; [[ $cfg == C4* ]] && steps=20; [[ $cfg == C5* ]] && steps=6; [ $cfg == C65KL ] && steps=3
+    [ $cfg == C2RWM ] && steps=200; [ $cfg == C2x8 ] && steps=20
+    timeout 1200 python bench.py --config $cfg --steps $steps --warmup 5 --no-cpu-baseline > $OUT/bench_$cfg.json 2> $OUT/bench_$cfg.err
     head -c 300 $OUT/bench_$cfg.json; echo
   fi
 done
@@ -46,12 +50,18 @@ digest() {  # digest CONFIG KERNEL REPORT_BASENAME
     [ "${KEEP_REPS:-0}" == 1 ] || rm -f $OUT/$3.ncu-rep
   fi
 }
+L2M="lts__t_bytes.sum,lts__t_sectors_op_read.sum,lts__t_sectors_op_write.sum,lts__t_sectors_op_atom.sum,lts__t_sectors_op_red.sum"
 if has ncu; then
+  # the driver's bench command (iterations 5-24 timed)
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
-     python bench.py --steps 30 --warmup 3 --no-cpu-baseline > $OUT/ncu_launches_bench.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:construct -s 400 -c 1 -o $OUT/prof_construct_C2 \
-     python bench.py --steps 420 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_construct.log 2>&1
-  digest C2 construct_cl_kernel prof_construct_C2
+     python bench.py --steps 20 --warmup 5 --no-cpu-baseline > $OUT/ncu_launches_bench.log 2>&1
+  # construction in the driver's window (iteration 10) and at steady state (iteration 400)
+  timeout 900 ncu --set full --metrics $L2M --clock-control none --import-source on -k regex:construct -s 10 -c 1 \
+     -o $OUT/prof_construct_C2_it10 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > $OUT/ncu_full_construct10.log 2>&1
+  digest C2@10 construct_cl_kernel prof_construct_C2_it10
+  timeout 900 ncu --set full --metrics $L2M --clock-control none --import-source on -k regex:construct -s 400 -c 1 \
+     -o $OUT/prof_construct_C2_it400 python bench.py --steps 420 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_construct.log 2>&1
+  digest C2@400 construct_cl_kernel prof_construct_C2_it400
   # C2 fuses the update into the construction launch; the stand-alone update kernel is
   # captured from the A/B path (--separate-update)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:pheromone_update -s 400 -c 1 -o $OUT/prof_update_C2 \
@@ -59,13 +69,13 @@ if has ncu; then
   digest C2 pheromone_update_kernel prof_update_C2
   ls -la $OUT
 fi
-for cfg in C1 C3 C4 C4CT C2RWM C4RWM C4RWMCT C5; do
+for cfg in C1 C3 C4 C4CT C2RWM C4RWM C4RWMCT C5 C5L C2x8; do
   if has ncu$cfg; then
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:construct -s 5 -c 1 -o $OUT/prof_construct_$cfg \
+    timeout 900 ncu --set full --metrics $L2M --clock-control none --import-source on -k regex:construct -s 5 -c 1 -o $OUT/prof_construct_$cfg \
        python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_construct_$cfg.log 2>&1
     kern=construct_cl_kernel
     case $cfg in C4) kern=construct_full_kernel;; C4CT) kern=construct_ct_kernel;; *RWM*) kern=construct_rwm_kernel;; esac
-    digest $cfg $kern prof_construct_$cfg
+    digest $cfg@5 $kern prof_construct_$cfg
   fi
 done
 if has ncuC5; then
