@@ -297,9 +297,11 @@ __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, co
 // trails carry their own.  The sparse cities are hidden from the background scan through the
 // tabu (marked, scanned, unmarked), then evaluated with their stored values; every city draws
 // the uniform of the dense scan (R13), so the argmax -- ties to the lowest id -- is the dense one.
+// (out of line and by value -- it leaves the tabu as it found it -- so the rarely taken lean
+// path adds no registers to the construction's step loop)
 template <class Tabu>
-__device__ __forceinline__ uint32_t lean_fallback(const LeanArgs& Ln, const double2* __restrict__ xy, int cur,
-                                                  Tabu& tabu, int n, int alpha, uint32_t step,
+__device__ __noinline__ uint32_t lean_fallback(const LeanArgs Ln, const double2* __restrict__ xy, int cur,
+                                               Tabu tabu, int n, int alpha, uint32_t step,
                                                   uint32_t ant, uint32_t iter, PhiloxKey key, int lane) {
     const float b = __ldcg(Ln.bg + Ln.parity);   // the background trail after the last update
     const uint16_t* ids = Ln.sp_id + (size_t)cur * Ln.cap;
@@ -321,24 +323,45 @@ __device__ __forceinline__ uint32_t lean_fallback(const LeanArgs& Ln, const doub
         tabu.sync();
     }
     tabu.prepare(lane);
-    // 2. background scan: lane l takes the 4-city groups 128t + 4l (one Philox per group)
+    // 2. background scan: lane l takes the 4-city groups 128t + 4l (one Philox per group),
+    //    two groups per trip (independent chains); with integral coordinates the group's four
+    //    coordinates are one 16-byte load and 1 / choice_info comes from the table by distance
     const double2 xc = __ldg(xy + cur);
+    const short2 xcs = Ln.xys ? __ldg(Ln.xys + cur) : make_short2(0, 0);
     const float ba = pow_alpha(b, alpha);
     uint32_t bm = kNone, bc = kNone;
-    for (int base = 0; base < n; base += 128) {
-        const int c0 = base + 4 * lane;
-        const uint32_t nib = chunk_nibble(tabu, c0, n);
-        if (!__any_sync(kFull, nib != 0xFu)) continue;
+    auto group = [&](int c0, uint32_t nib) {
+        if (nib == 0xFu) return;
         const uint4 x = philox4x32_10(ctr_city((uint32_t)c0 >> 2, step, ant, iter), key);
         const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+        float iv[4];
+        if (Ln.xys) {
+            const int4 pk = __ldg(reinterpret_cast<const int4*>(Ln.xys + c0));   // 4 short2 (c0 % 4 == 0)
+            const int pv[4] = {pk.x, pk.y, pk.z, pk.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const short2 pq = make_short2((short)(pv[q] & 0xFFFF), (short)(pv[q] >> 16));
+                iv[q] = ((nib >> q) & 1u) ? 0.f : __ldg(Ln.inv_tab + euc2d_int(xcs, pq));
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                iv[q] = ((nib >> q) & 1u) ? 0.f
+                                          : __fdiv_rn(1.0f, __fmul_rn(ba, heur_edge(xc, __ldg(xy + c0 + q), Ln.beta)));
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if ((nib >> q) & 1u) continue;
-            const float h = heur_edge(xc, __ldg(xy + c0 + q), Ln.beta);
-            const float iv = __fdiv_rn(1.0f, __fmul_rn(ba, h));   // = inv_weight(b, h, alpha)
-            const uint32_t mag = key_magnitude(__fmul_rn(det_log2(uniform_open(xs[q])), iv));
+            const uint32_t mag = key_magnitude(__fmul_rn(det_log2(uniform_open(xs[q])), iv[q]));
             if (mag < bm) { bm = mag; bc = (uint32_t)(c0 + q); }   // ascending cities: ties keep the lower
         }
+    };
+    for (int base = 0; base < n; base += 256) {
+        const int ca = base + 4 * lane, cb = ca + 128;
+        const uint32_t na = chunk_nibble(tabu, ca, n), nb = chunk_nibble(tabu, cb, n);
+        if (!__any_sync(kFull, (na & nb) != 0xFu)) continue;
+        group(ca, na);
+        group(cb, nb);
     }
     // 3. unhide the hidden ones and evaluate them with their stored 1 / choice_info
     for (int r = 0; r * 32 < Ln.cap; ++r) {
@@ -1371,6 +1394,7 @@ __global__ void __launch_bounds__(128) construct_ct_kernel(const ConstructArgs A
                 ct_trip(eB, ivB, base + 256, lane, L, (uint32_t)s, ant, iter, c_key, bm, bc, thr);
             }
             const uint32_t nxt = warp_select(bm, bc);
+            __syncwarp();   // every lane's reads of this step's list before lane 0 rewrites it
             if (lane == 0) ct_mark(ent, L, n, nxt);
             stage_route(route, s, nxt, lane, stage);
             __syncwarp();

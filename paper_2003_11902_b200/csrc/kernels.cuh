@@ -83,6 +83,28 @@ __device__ __forceinline__ int32_t euc2d(double2 p, double2 q) {
     return (int32_t)__dadd_rn(r, 0.5);
 }
 
+// Integer EUC_2D (the local search and the lean pheromone's fallback scans):
+// kIntXY: every coordinate is an integer with |x|, |y| <= 16383 (checked at setup), so
+// S = dx^2 + dy^2 < 2^31 is exact in 32 bits and nint(sqrt(S)) -- the R12 distance, which
+// the double formula computes exactly for such S (sqrt(S) is never within 2^-30 of a
+// half-integer) -- comes from an approximate sqrt rounded to the nearest integer k0
+// (|error| << 1/2 except next to a half-integer) and one integer correction:
+// (2k-1)^2 <= 4S < (2k+1)^2  <=>  k^2 - k < S <= k^2 + k   (4S is even, (2k+-1)^2 odd).
+// No fp64 (DSQRT is a ~20-instruction subroutine with a long DFMA chain).  Pinned against
+// the double formula in tests/test_capi.py (exhaustive S <= 2^22, random S < 2^31, and the
+// near-half-integer cases k^2 + k, k^2 + k + 1).
+__device__ __forceinline__ int32_t euc2d_int(short2 p, short2 q) {
+    const int dx = (int)p.x - (int)q.x, dy = (int)p.y - (int)q.y;
+    const uint32_t S = (uint32_t)(dx * dx) + (uint32_t)(dy * dy);
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(__uint2float_rn(S)));
+    uint32_t k = (uint32_t)__float2int_rn(r);
+    const uint32_t kk = k * k;
+    if (kk + k < S) ++k;
+    else if (k > 0u && kk - k >= S) --k;
+    return (int32_t)k;
+}
+
 // tau^alpha for integer alpha (R17) by repeated fp32 multiplication.
 __device__ __forceinline__ float pow_alpha(float t, int alpha) {
     if (alpha == 1) return t;
@@ -350,6 +372,13 @@ struct LeanArgs {
     int cap;                 // slots per row (multiple of 32)
     int parity;              // p = iteration & 1
     int beta;
+    // integral coordinates with |x|, |y| <= 16383 (else null): the fallback scans take the
+    // distance in 32-bit integer arithmetic (euc2d_int, exactly R12) and the background's
+    // 1 / choice_info from a table by distance, rewritten by every update for the new b
+    const short2* xys;
+    const float* heur_tab;   // [dtab]: eta^beta of distance d (R11, R18), setup
+    float* inv_tab;          // [dtab]: 1 / (b^alpha eta^beta(d)) for the current background b
+    int dtab;
 };
 
 // pheromone update arguments (row a6; pheromone_update_kernel below)
@@ -662,6 +691,9 @@ __global__ void __launch_bounds__(256) lean_update_kernel(UpdateArgs U) {
         Ln.bg[Ln.parity ^ 1] = b1;
         *U.iter_dev += 1u;
     }
+    if (Ln.inv_tab)   // the next construction's background 1 / choice_info by distance
+        for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < Ln.dtab; d += gridDim.x * blockDim.x)
+            Ln.inv_tab[d] = inv_weight(b1, Ln.heur_tab[d], U.alpha);
     if (i >= U.n) return;
     const int si = U.succ[i], pi = U.pred[i];
     bool has_s = false, has_p = false;
@@ -741,6 +773,15 @@ __global__ void lean_init_kernel(const double2* __restrict__ xy, int n, int cl, 
     const size_t sp = (size_t)n * Ln.cap;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < sp; e += (size_t)gridDim.x * blockDim.x)
         Ln.sp_id[e] = kLeanEmpty;
+    if (Ln.inv_tab)
+        for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < Ln.dtab; d += gridDim.x * blockDim.x) {
+            const double D = (double)(d > 1 ? d : 1);   // heur_edge's arithmetic for distance d
+            double Db = 1.0;
+            for (int k = 0; k < beta; ++k) Db = __dmul_rn(Db, D);
+            const float h = __double2float_rn(__ddiv_rn(1.0, Db));
+            const_cast<float*>(Ln.heur_tab)[d] = h;
+            Ln.inv_tab[d] = inv_weight(tmax, h, alpha);
+        }
     if (blockIdx.x == 0 && threadIdx.x == 0) Ln.bg[0] = Ln.bg[1] = tmax;
 }
 
@@ -754,14 +795,19 @@ __global__ void heur_kernel(const double2* __restrict__ xy, int n, int ld, int b
 // one 1024-thread block; per step every thread takes the closest unvisited city among
 // j = tid, tid + 1024, ... as a (d, j) key, the block reduces the key to its minimum (ties
 // -> lowest id) and thread 0 moves there.  Visited bits in shared memory (n <= 65535).
-constexpr int kNnThreads = 1024;
-__global__ void __launch_bounds__(kNnThreads) nn_tour_kernel(const double2* __restrict__ xy, int n,
+constexpr int kNnThreads = 1024;   // upper bound; launched with nn_threads(n)
+// Nearest-neighbour tour from city 0, ties -> lowest id (R3; Alg. 1): one block,
+// each step a block-wide argmin of (d, id) over the unvisited cities by two 32-bit warp
+// reductions (redux.sync) per level.  Setup only, but inside bench.py's end-to-end timing.
+__host__ __device__ constexpr int nn_threads(int n) { return n <= 2048 ? 256 : n <= 8192 ? 512 : 1024; }
+__global__ void __launch_bounds__(kNnThreads) nn_tour_kernel(const double2* __restrict__ xy,
+                                                             const short2* __restrict__ xys, int n,
                                                              long long* len_out) {
     __shared__ uint32_t vis[2048];
-    __shared__ unsigned long long s_key[kNnThreads / 32];
+    __shared__ uint32_t s_d[kNnThreads / 32], s_j[kNnThreads / 32];
     __shared__ int s_cur;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int w = tid; w < 2048; w += kNnThreads) vis[w] = 0u;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    for (int w = tid; w < 2048; w += blockDim.x) vis[w] = 0u;
     if (tid == 0) {
         vis[0] = 1u;
         s_cur = 0;
@@ -771,31 +817,32 @@ __global__ void __launch_bounds__(kNnThreads) nn_tour_kernel(const double2* __re
     for (int s = 1; s < n; ++s) {
         const int cur = s_cur;
         const double2 pc = xy[cur];
-        unsigned long long best = ~0ull;
-        for (int j = tid; j < n; j += kNnThreads) {
+        const short2 pcs = xys ? xys[cur] : make_short2(0, 0);
+        uint32_t bd = kNone, bj = kNone;
+        for (int j = tid; j < n; j += blockDim.x) {   // ascending j: ties keep the lower id
             if ((vis[j >> 5] >> (j & 31)) & 1u) continue;
-            const unsigned long long k = ((unsigned long long)(uint32_t)euc2d(pc, xy[j]) << 32) | (uint32_t)j;
-            best = k < best ? k : best;
+            // integral coordinates: the exact 32-bit path (euc2d_int == R12), else fp64
+            const uint32_t d = (uint32_t)(xys ? euc2d_int(pcs, xys[j]) : euc2d(pc, xy[j]));
+            if (d < bd) {
+                bd = d;
+                bj = (uint32_t)j;
+            }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long v = __shfl_xor_sync(kFull, best, o);
-            best = v < best ? v : best;
+        uint32_t wd = __reduce_min_sync(kFull, bd);
+        uint32_t wj = __reduce_min_sync(kFull, bd == wd ? bj : kNone);
+        if (lane == 0) {
+            s_d[warp] = wd;
+            s_j[warp] = wj;
         }
-        if (lane == 0) s_key[warp] = best;
         __syncthreads();
         if (warp == 0) {
-            unsigned long long b = s_key[lane];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long v = __shfl_xor_sync(kFull, b, o);
-                b = v < b ? v : b;
-            }
+            const uint32_t d = lane < nw ? s_d[lane] : kNone, jj = lane < nw ? s_j[lane] : kNone;
+            wd = __reduce_min_sync(kFull, d);
+            wj = __reduce_min_sync(kFull, d == wd ? jj : kNone);
             if (lane == 0) {
-                const int nxt = (int)(b & 0xFFFFFFFFu);
-                len += (long long)(b >> 32);
-                vis[nxt >> 5] |= 1u << (nxt & 31);
-                s_cur = nxt;
+                len += (long long)wd;
+                vis[wj >> 5] |= 1u << (wj & 31);
+                s_cur = (int)wj;
             }
         }
         __syncthreads();

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -94,6 +95,7 @@ struct mmas_ctx {
     int64_t nn_len = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    bool pooled = false;                    // device buffers from the per-device pool (dalloc)
     PhiloxKey key{};
     int rec_bytes = 0;
 
@@ -132,6 +134,9 @@ struct mmas_ctx {
     int lean_cap = 0, lean_L = 0;
     float *cand_tau = nullptr, *cand_heur = nullptr, *sp_tau = nullptr, *sp_inv = nullptr, *bg = nullptr;
     uint16_t* sp_id = nullptr;
+    short2* lean_xys = nullptr;              // integral coordinates (else null)
+    float *heur_tab = nullptr, *inv_tab = nullptr;
+    int dtab = 0;
 
     // concurrent independent colonies (R29): K per-colony copies of the mutable state
     int colonies = 1;
@@ -255,6 +260,10 @@ LeanArgs lean_args(mmas_ctx* h) {
     L.cap = h->lean_cap;
     L.parity = h->iteration & 1;
     L.beta = (int)h->cfg.beta;
+    L.xys = h->lean_xys;
+    L.heur_tab = h->heur_tab;
+    L.inv_tab = h->inv_tab;
+    L.dtab = h->dtab;
     return L;
 }
 
@@ -345,8 +354,8 @@ void set_smem_attr(int optin) {
 
 template <int S, bool T, bool R, bool F, bool W = false>
 void launch_cl_f(mmas_ctx* h, const ConstructArgs& A) {
-    launch_pdl(construct_cl_kernel<S, T, R, F, W>, dim3(h->cons_grid, h->colonies), dim3(h->cons_warps * 32),
-               h->cons_smem, h->stream, A);
+    launch_pdl(construct_cl_kernel<S, T, R, F, W>, dim3(h->cons_grid, h->colonies),
+               dim3(h->cons_warps * 32), h->cons_smem, h->stream, A);
 }
 
 // cl <= 32 (tables padded to 32 slots): one slot per lane; more than 8 ant warps per block
@@ -550,24 +559,61 @@ void free_ctx(mmas_ctx* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     void* ptrs[] = {h->xy, h->heur, h->tau, h->inv_w, h->cand_inv, h->cand_id, h->routes, h->lengths,
                     h->best_key, h->fallback_count, h->ib_route, h->gb_route, h->succ, h->pred, h->gb_len,
-                    h->ib_len, h->ib_ant, h->scal, h->iter_dev, h->local_record, h->done,
+                    h->ib_len, h->ib_ant, h->scal, h->iter_dev, h->local_record, h->done, h->xerr,
                     h->ls_nn, h->ls_nnd, h->ls_xys, h->ls_nnp, h->ls_pos, h->ls_queue, h->ls_inq, h->ls_moves,
-                    h->cand_tau, h->cand_heur, h->sp_id, h->sp_tau, h->sp_inv, h->bg};
+                    h->cand_tau, h->cand_heur, h->sp_id, h->sp_tau, h->sp_inv, h->bg,
+                    h->lean_xys, h->heur_tab, h->inv_tab};
+    // (pool allocations go back to the pool in stream order; the stream is drained below)
     for (void* p : ptrs)
-        if (p) cudaFree(p);
+        if (p) {
+            if (h->pooled && h->stream) cudaFreeAsync(p, h->stream);
+            else cudaFree(p);
+        }
+    if (h->stream) cudaStreamSynchronize(h->stream);
     for (void* p : h->xopened) cudaIpcCloseMemHandle(p);
     if (h->xbuf) cudaFree(h->xbuf);
     if (h->xpeers_dev) cudaFree(h->xpeers_dev);
-    if (h->xerr) cudaFree(h->xerr);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }
 
+// Context buffers come from one stream-ordered memory pool per device that keeps what is
+// freed (release threshold: unlimited), so creating a colony after another was destroyed maps
+// no new memory (mmas_create is inside bench.py's end-to-end timing); MMAS_NO_POOL=1 uses
+// plain cudaMalloc.  The peer-exchange buffer stays a cudaMalloc allocation (IPC-exportable).
+thread_local cudaStream_t g_alloc_stream = nullptr;   // set by setup() while it allocates
+thread_local cudaMemPool_t g_alloc_pool = nullptr;
+
+cudaMemPool_t device_pool(int device) {
+    static std::mutex mu;
+    static std::vector<cudaMemPool_t> pools;
+    if (std::getenv("MMAS_NO_POOL")) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)pools.size() <= device) pools.resize(device + 1, nullptr);
+    if (!pools[device]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaMemPool_t pool;
+        if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        pools[device] = pool;
+    }
+    return pools[device];
+}
+
 template <class T>
 int dalloc(T** p, size_t count) {
-    cudaError_t e = cudaMalloc((void**)p, sizeof(T) * std::max<size_t>(count, 1));
-    if (e != cudaSuccess) return fail(MMAS_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    const size_t bytes = sizeof(T) * std::max<size_t>(count, 1);
+    cudaError_t e = g_alloc_pool ? cudaMallocFromPoolAsync((void**)p, bytes, g_alloc_pool, g_alloc_stream)
+                                 : cudaMalloc((void**)p, bytes);
+    if (e != cudaSuccess) return fail(MMAS_ENOMEM, std::string("device allocation: ") + cudaGetErrorString(e));
     return MMAS_OK;
 }
 
@@ -635,6 +681,18 @@ int setup(mmas_ctx* h) {
     h->key.k1 = (uint32_t)(c.seed >> 32);
     h->rec_bytes = round_up(8 + 2 * n, 16);
     h->colonies = std::max(1, c.colonies);
+    // allocate the context's buffers from the device pool, in this stream's order
+    struct PoolScope {
+        PoolScope(mmas_ctx* h) {
+            g_alloc_pool = device_pool(h->device);
+            g_alloc_stream = h->stream;
+            h->pooled = g_alloc_pool != nullptr;
+        }
+        ~PoolScope() {
+            g_alloc_pool = nullptr;
+            g_alloc_stream = nullptr;
+        }
+    } pool_scope(h);
     if (const char* sb = std::getenv("MMAS_SPIN_BOUND")) h->spin_bound = std::max(1ll << 10, std::atoll(sb));
 
     const size_t nn = (size_t)n * h->ld;
@@ -762,7 +820,26 @@ int setup(mmas_ctx* h) {
         // NN tour on the device (one block; the host loop was O(n^2) on one core)
         long long* d_len = nullptr;
         CU(cudaMallocAsync(reinterpret_cast<void**>(&d_len), sizeof(long long), h->stream));
-        nn_tour_kernel<<<1, kNnThreads, 0, h->stream>>>(h->xy, n, d_len);
+        // integral coordinates within +-16383: the NN tour's distances in 32-bit arithmetic
+        short2* d_xys = nullptr;
+        {
+            bool integral = true;
+            std::vector<short2> xs((size_t)n);
+            for (int i = 0; i < n && integral; ++i) {
+                const double x = c.coords[2 * i], y = c.coords[2 * i + 1];
+                if (x != std::floor(x) || y != std::floor(y) || std::fabs(x) > 16383.0 || std::fabs(y) > 16383.0)
+                    integral = false;
+                else
+                    xs[(size_t)i] = make_short2((short)x, (short)y);
+            }
+            if (integral) {
+                CU(cudaMallocAsync(reinterpret_cast<void**>(&d_xys), sizeof(short2) * n, h->stream));
+                CU(cudaMemcpyAsync(d_xys, xs.data(), sizeof(short2) * n, cudaMemcpyHostToDevice, h->stream));
+                CU(cudaStreamSynchronize(h->stream));
+            }
+        }
+        nn_tour_kernel<<<1, nn_threads(n), 0, h->stream>>>(h->xy, d_xys, n, d_len);
+        if (d_xys) CU(cudaFreeAsync(d_xys, h->stream));
         h->launches++;
         CU(cudaGetLastError());
         long long len = 0;
@@ -788,6 +865,27 @@ int setup(mmas_ctx* h) {
         if ((st = dalloc(&h->cand_tau, ncl)) || (st = dalloc(&h->cand_heur, ncl)) || (st = dalloc(&h->sp_id, nsp)) ||
             (st = dalloc(&h->sp_tau, nsp)) || (st = dalloc(&h->sp_inv, nsp)) || (st = dalloc(&h->bg, 2)))
             return st;
+        // integral coordinates within +-16383: 32-bit distances and tables by distance (R30)
+        bool integral = true;
+        double lo_x = INFINITY, hi_x = -INFINITY, lo_y = INFINITY, hi_y = -INFINITY;
+        std::vector<short2> xs((size_t)n);
+        for (int i = 0; i < n && integral; ++i) {
+            const double x = c.coords[2 * i], y = c.coords[2 * i + 1];
+            if (x != std::floor(x) || y != std::floor(y) || std::fabs(x) > 16383.0 || std::fabs(y) > 16383.0)
+                integral = false;
+            else
+                xs[(size_t)i] = make_short2((short)x, (short)y);
+            lo_x = std::min(lo_x, x); hi_x = std::max(hi_x, x);
+            lo_y = std::min(lo_y, y); hi_y = std::max(hi_y, y);
+        }
+        if (integral && !std::getenv("MMAS_LEAN_NO_TABLE")) {
+            h->dtab = (int)std::ceil(std::sqrt((hi_x - lo_x) * (hi_x - lo_x) + (hi_y - lo_y) * (hi_y - lo_y))) + 2;
+            if ((st = dalloc(&h->lean_xys, (size_t)n + 4)) || (st = dalloc(&h->heur_tab, (size_t)h->dtab)) ||
+                (st = dalloc(&h->inv_tab, (size_t)h->dtab)))
+                return st;
+            CU(cudaMemcpyAsync(h->lean_xys, xs.data(), sizeof(short2) * n, cudaMemcpyHostToDevice, h->stream));
+            CU(cudaStreamSynchronize(h->stream));   // xs goes out of scope
+        }
         lean_init_kernel<<<std::max(1, std::min(4096, (int)((nsp + 255) / 256))), 256, 0, h->stream>>>(
             h->xy, n, h->cl_ld, h->cand_id, (int)c.beta, h->alpha, h->scal, lean_args(h), h->cand_inv);
         h->launches++;
@@ -908,6 +1006,13 @@ int setup(mmas_ctx* h) {
                              h->ls_coop_smem_max);
         cudaFuncSetAttribute(two_opt_coop_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              h->ls_coop_smem_max);
+        // experiment (MMAS_LS_CARVEOUT = percent of the unified L1/shared memory given to shared
+        // memory): fewer resident 2-opt blocks per SM, but an L1 large enough for the coordinates
+        if (const char* co = std::getenv("MMAS_LS_CARVEOUT")) {
+            const int pct = std::atoi(co);
+            cudaFuncSetAttribute(two_opt_coop_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            cudaFuncSetAttribute(two_opt_coop_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+        }
     }
     allow_max_smem(pheromone_update_kernel, h->smem_optin);
     CU(cudaGetLastError());
@@ -1405,8 +1510,8 @@ int mmas_get_heuristic(mmas_ctx* h, float* out) {
 int64_t mmas_pheromone_bytes(const mmas_ctx* h) {
     if (!h) return MMAS_EINVAL;
     const int64_t ncl = (int64_t)h->n * h->cl_ld;
-    if (h->lean)   // candidate trails + eta^beta + 1/w, sparse id + trail + 1/w
-        return ncl * 12 + (int64_t)h->n * h->lean_cap * 10;
+    if (h->lean)   // candidate trails + eta^beta + 1/w, sparse id + trail + 1/w, tables by distance
+        return ncl * 12 + (int64_t)h->n * h->lean_cap * 10 + (int64_t)h->dtab * 8;
     return (int64_t)3 * h->n * h->ld * 4 * h->colonies + ncl * 4 * h->colonies;   // tau, inv_w, heur + cand_inv
 }
 

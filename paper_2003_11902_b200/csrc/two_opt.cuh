@@ -35,28 +35,7 @@ __device__ __forceinline__ void colony_offset(TwoOptArgs& T, ConstructArgs& A, i
     colony_offset(A, c);
 }
 
-// ---- coordinates and EUC_2D distances of the local search --------------------------
-// kIntXY: every coordinate is an integer with |x|, |y| <= 16383 (checked at setup), so
-// S = dx^2 + dy^2 < 2^31 is exact in 32 bits and nint(sqrt(S)) -- the R12 distance, which
-// the double formula computes exactly for such S (sqrt(S) is never within 2^-30 of a
-// half-integer) -- comes from an approximate sqrt rounded to the nearest integer k0
-// (|error| << 1/2 except next to a half-integer) and one integer correction:
-// (2k-1)^2 <= 4S < (2k+1)^2  <=>  k^2 - k < S <= k^2 + k   (4S is even, (2k+-1)^2 odd).
-// No fp64 (DSQRT is a ~20-instruction subroutine with a long DFMA chain).  Pinned against
-// the double formula in tests/test_capi.py (exhaustive S <= 2^22, random S < 2^31, and the
-// near-half-integer cases k^2 + k, k^2 + k + 1).
-__device__ __forceinline__ int32_t euc2d_int(short2 p, short2 q) {
-    const int dx = (int)p.x - (int)q.x, dy = (int)p.y - (int)q.y;
-    const uint32_t S = (uint32_t)(dx * dx) + (uint32_t)(dy * dy);
-    float r;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(__uint2float_rn(S)));
-    uint32_t k = (uint32_t)__float2int_rn(r);
-    const uint32_t kk = k * k;
-    if (kk + k < S) ++k;
-    else if (k > 0u && kk - k >= S) --k;
-    return (int32_t)k;
-}
-
+// ---- coordinates and EUC_2D distances of the local search (euc2d_int: kernels.cuh) ----
 template <bool kInt>
 struct Pts;
 template <>

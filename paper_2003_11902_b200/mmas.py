@@ -284,7 +284,10 @@ class Colony:
 
     @property
     def pheromone_bytes(self):
-        return int(lib().mmas_pheromone_bytes(self._h))
+        L = lib()
+        if not hasattr(L, "mmas_pheromone_bytes"):   # an older in-tree build (A/B runs)
+            return None
+        return int(L.mmas_pheromone_bytes(self._h))
 
     def select_colony(self, colony: int):
         """Introspection and best_tour/best_length report colony `colony` from now on."""
