@@ -60,8 +60,10 @@ __device__ __forceinline__ void trace_mark(int k) {
         g_trace[blockIdx.x * 8 + k] = t;
     }
 }
-// fallback scans: [0] cycles summed over every fallback (lane 0's clock), [1] their count
-__device__ unsigned long long g_fbcyc[2];
+// fallback scans: [0] cycles summed over every fallback (lane 0's clock), [1] their count;
+// cooperative 2-opt: [2] rounds, [3] evaluations retired, [4] evaluations discarded behind a winner,
+// [5..14] applied reversals by length (log2 buckets: < 2, < 4, ... , >= 512), [15] total length
+__device__ unsigned long long g_fbcyc[16];
 __device__ __forceinline__ long long trace_clock() { return clock64(); }
 __device__ __forceinline__ void trace_fallback(long long t0, int lane) {
     if (lane == 0) {
@@ -69,7 +71,19 @@ __device__ __forceinline__ void trace_fallback(long long t0, int lane) {
         atomicAdd(&g_fbcyc[1], 1ull);
     }
 }
+__device__ __forceinline__ void trace_ls_len(int len) {
+    const int b = min(9, max(0, 31 - __clz(max(len, 1)) ));
+    atomicAdd(&g_fbcyc[5 + b], 1ull);
+    atomicAdd(&g_fbcyc[15], (unsigned long long)len);
+}
+__device__ __forceinline__ void trace_ls_round(int retired, int discarded) {
+    atomicAdd(&g_fbcyc[2], 1ull);
+    atomicAdd(&g_fbcyc[3], (unsigned long long)retired);
+    atomicAdd(&g_fbcyc[4], (unsigned long long)discarded);
+}
 #else
+__device__ __forceinline__ void trace_ls_len(int) {}
+__device__ __forceinline__ void trace_ls_round(int, int) {}
 __device__ __forceinline__ void trace_mark(int) {}
 __device__ __forceinline__ long long trace_clock() { return 0; }
 __device__ __forceinline__ void trace_fallback(long long, int) {}

@@ -1647,8 +1647,8 @@ int mmas_sync(mmas_ctx* h) {
 // Debug: fallback-scan cycles (sum, count) since load (a -DMMAS_TRACE build), and reset.
 extern "C" int mmas_debug_fb_cycles(unsigned long long* out) {
 #ifdef MMAS_TRACE
-    if (cudaMemcpyFromSymbol(out, mmas::g_fbcyc, 2 * sizeof(unsigned long long)) != cudaSuccess) return MMAS_ECUDA;
-    const unsigned long long z[2] = {0ull, 0ull};
+    if (cudaMemcpyFromSymbol(out, mmas::g_fbcyc, 16 * sizeof(unsigned long long)) != cudaSuccess) return MMAS_ECUDA;
+    const unsigned long long z[16] = {};
     if (cudaMemcpyToSymbol(mmas::g_fbcyc, z, sizeof(z)) != cudaSuccess) return MMAS_ECUDA;
     return MMAS_OK;
 #else

@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
                 int nhead = head + retired;
                 if (nhead >= n) nhead -= n;
                 int ncount = count - retired;
+                if (tid == 0) trace_ls_round(retired, avail - retired);
                 if (win >= 0) {
                     const uint4 pe = s_eval[win];
                     const int mb = (int)(pe.y & 0xFFFFu), mc = (int)(pe.y >> 16), md = (int)pe.z;
@@ -403,6 +404,7 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
                         j = nj;
                         len = n - len;
                     }
+                    if (tid == 0) trace_ls_len(len);
                     for (int k = tid; k < len / 2; k += blockDim.x) {
                         int p = i + k;
                         if (p >= n) p -= n;

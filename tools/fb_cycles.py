@@ -28,7 +28,7 @@ def child(cfg, first, count):
     col = mmas.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=0)
     L = mmas.lib()
     L.mmas_debug_fb_cycles.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
-    buf = (ctypes.c_ulonglong * 2)()
+    buf = (ctypes.c_ulonglong * 16)()
     if first:
         col.iterate(first)
     col.sync()
