@@ -266,6 +266,19 @@ int64_t mmas_kernel_launches(const mmas_ctx *h);
 int mmas_debug_philox(const uint32_t *ctr_key, int64_t count, uint32_t *out_words, float *out_log2);
 int mmas_debug_log2(const float *u, int64_t count, float *out);
 
+/* ---- checkpoint / resume (synchronous; caller-owned host buffer) ----
+ * The random numbers are counter-based (keyed by seed, iteration, ant, step, city; R13), so a
+ * colony's future is a function of its device state and iteration counter alone:
+ * mmas_save_state writes them (a header identifying the instance and parameters, then the
+ * trails, 1/choice_info, candidate table, limits, best tours, iteration counters, last
+ * routes) into host_buf; mmas_load_state restores them into a context created with the same
+ * coordinates and configuration (MMAS_EINVAL if the header does not match), after which
+ * iterating continues exactly as the saved colony would have (tested in
+ * tests/test_checkpoint_gpu.py).  mmas_state_bytes gives the buffer size. */
+int64_t mmas_state_bytes(mmas_ctx *h);
+int mmas_save_state(mmas_ctx *h, void *host_buf, int64_t bytes);
+int mmas_load_state(mmas_ctx *h, const void *host_buf, int64_t bytes);
+
 /* Device pointer of the stream the context runs on (cudaStream_t). */
 void *mmas_stream(const mmas_ctx *h);
 /* Synchronises the context's stream. */

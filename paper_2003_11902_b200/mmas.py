@@ -31,7 +31,8 @@ EXPORTED = (
     "mmas_exchange_bytes", "mmas_exchange_buffer", "mmas_exchange_ipc_handle", "mmas_exchange_open_ipc",
     "mmas_exchange_attach", "mmas_construct_publish", "mmas_update_exchange", "mmas_iterate_exchange",
     "mmas_exchange_status", "mmas_device_status",
-    "mmas_select_colony", "mmas_colonies", "mmas_pheromone_bytes", "mmas_n", "mmas_iteration", "mmas_get_tours", "mmas_get_lengths", "mmas_get_pheromone",
+    "mmas_select_colony", "mmas_colonies", "mmas_pheromone_bytes", "mmas_state_bytes", "mmas_save_state",
+    "mmas_load_state", "mmas_n", "mmas_iteration", "mmas_get_tours", "mmas_get_lengths", "mmas_get_pheromone",
     "mmas_get_inv_w", "mmas_get_heuristic", "mmas_get_candidates", "mmas_get_limits",
     "mmas_get_stats", "mmas_profile", "mmas_get_phase_times", "mmas_kernel_launches",
     "mmas_stream", "mmas_sync", "mmas_debug_philox", "mmas_debug_log2",
@@ -104,7 +105,10 @@ def lib():
     # symbols newer than round 1: an older in-tree build (A/B runs) may lack them;
     # tests/test_capi.py fails loudly on a library that does not export every one
     for name, args, res in (("mmas_device_status", [V], None), ("mmas_select_colony", [V, ctypes.c_int32], None),
-                            ("mmas_colonies", [V], None), ("mmas_pheromone_bytes", [V], ctypes.c_int64)):
+                            ("mmas_colonies", [V], None), ("mmas_pheromone_bytes", [V], ctypes.c_int64),
+                            ("mmas_state_bytes", [V], ctypes.c_int64),
+                            ("mmas_save_state", [V, ctypes.c_void_p, ctypes.c_int64], None),
+                            ("mmas_load_state", [V, ctypes.c_void_p, ctypes.c_int64], None)):
         if hasattr(L, name):
             getattr(L, name).argtypes = args
             if res is not None:
@@ -288,6 +292,19 @@ class Colony:
         if not hasattr(L, "mmas_pheromone_bytes"):   # an older in-tree build (A/B runs)
             return None
         return int(L.mmas_pheromone_bytes(self._h))
+
+    def save_state(self) -> bytes:
+        """Checkpoint: the colony's whole state (include/mmas.h mmas_save_state)."""
+        L = lib()
+        nb = int(_err(L.mmas_state_bytes(self._h)))
+        buf = ctypes.create_string_buffer(nb)
+        _err(L.mmas_save_state(self._h, buf, nb))
+        return buf.raw
+
+    def load_state(self, state: bytes):
+        """Resume from save_state() of a context with the same coordinates and configuration."""
+        buf = ctypes.create_string_buffer(bytes(state), len(state))
+        _err(lib().mmas_load_state(self._h, buf, len(state)))
 
     def select_colony(self, colony: int):
         """Introspection and best_tour/best_length report colony `colony` from now on."""
