@@ -241,7 +241,7 @@ __device__ __forceinline__ uint32_t chunk_nibble(const Tabu& tabu, int c0, int n
 // branch (a threshold lagged by a trip, or warp-uniform skipping, measured slower: the
 // other warps hide the reduction).  At a few warps per SM with rows loaded from global the
 // branch-free scan is faster (C5 streams its rows through shared memory instead).
-template <bool kArgmax, bool kPrefetch = false, bool kPruneFb = false, class Tabu>
+template <bool kArgmax, bool kPrefetch = false, bool kPruneFb = false, bool kPfPrune = true, class Tabu>
 __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, const Tabu& tabu, int n,
                                                uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
                                                int lane, uint32_t& best_mag, uint32_t& best_c) {
@@ -267,9 +267,10 @@ __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, co
             if (base + 256 < n) load_trip(base + 256, na2, nb2, iva2, ivb2);
             if (__any_sync(kFull, (na & nb) != 0xFu)) {
                 const int ca = base + 4 * lane;
-                scan_chunk<kArgmax, kPrefetch>(iva, ca, na, step, ant, iter, key, best_mag, best_c, thr);
-                scan_chunk<kArgmax, kPrefetch>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c, thr);
-                if (!kArgmax) thr = warp_threshold(best_mag);
+                scan_chunk<kArgmax, kPrefetch && kPfPrune>(iva, ca, na, step, ant, iter, key, best_mag, best_c, thr);
+                scan_chunk<kArgmax, kPrefetch && kPfPrune>(ivb, ca + 128, nb, step, ant, iter, key, best_mag, best_c,
+                                                           thr);
+                if (!kArgmax && kPfPrune) thr = warp_threshold(best_mag);
             }
             na = na2;
             nb = nb2;
@@ -1077,6 +1078,11 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
                 } else if (!kSmemTable && A.prune_fallback)
                     scan_unvisited<false, false, !kSmemTable>(row, tabu, n, (uint32_t)s, ant, iter, c_key, lane, fm,
                                                               fc);
+                else if (kSmemTable)
+                    // the next trip's visited bits and inv_w float4s requested one trip ahead,
+                    // keys branch-free (A/B on C2's driver window: 0.2250 -> 0.2201 ms; with the
+                    // exact pruning of the full-row scans: 0.2327)
+                    scan_unvisited<false, true, false, false>(row, tabu, n, (uint32_t)s, ant, iter, c_key, lane, fm, fc);
                 else
                     scan_unvisited<false>(row, tabu, n, (uint32_t)s, ant, iter, c_key, lane, fm, fc);
                 nxt = warp_select(fm, fc);

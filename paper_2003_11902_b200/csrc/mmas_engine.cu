@@ -1640,6 +1640,137 @@ int mmas_sync(mmas_ctx* h) {
     return MMAS_OK;
 }
 
+// ---- checkpoint / resume ---------------------------------------------------------------
+// The colony's whole mutable state is device memory plus the host iteration counter (the
+// random numbers are counter-based, R13, so they carry no state): trails and 1/choice_info
+// (dense or lean), the candidate 1/w table, limits, global / iteration best, the device
+// iteration counters, the last iteration's routes and lengths, the fallback counter.
+namespace {
+struct StateHeader {
+    uint32_t magic, version;
+    int32_t n, cl_ld, m, m_local, ant_lo, colonies, lean, lean_cap, dtab, iteration;
+    uint64_t seed;
+    double alpha, beta, rho, p_best;
+    int32_t deposit, fallback, local_search, tabu, selection, world, rank, pad_;
+    int64_t payload;
+};
+constexpr uint32_t kStateMagic = 0x53414D4Du;   // "MMAS"
+
+std::vector<std::pair<void*, size_t>> state_segments(mmas_ctx* h) {
+    const size_t K = (size_t)h->colonies, ma = (size_t)std::max(h->m_local, 1);
+    const size_t nn = (size_t)h->n * h->ld;
+    std::vector<std::pair<void*, size_t>> v;
+    auto add = [&](void* p, size_t bytes) {
+        if (p && bytes) v.emplace_back(p, bytes);
+    };
+    if (!h->lean) {
+        add(h->tau, nn * K * 4);
+        add(h->inv_w, nn * K * 4);
+    } else {
+        const size_t ncl = (size_t)h->n * h->cl_ld + 64, nsp = (size_t)h->n * h->lean_cap;
+        add(h->cand_tau, ncl * 4);
+        add(h->sp_id, nsp * 2);
+        add(h->sp_tau, nsp * 4);
+        add(h->sp_inv, nsp * 4);
+        add(h->bg, 2 * 4);
+        add(h->inv_tab, (size_t)h->dtab * 4);
+    }
+    if (h->cl > 0) add(h->cand_inv, (size_t)h->cs.cand * K * 4);
+    add(h->scal, 4 * K * 4);
+    add(h->gb_route, (size_t)h->ldr * K * 2);
+    add(h->ib_route, (size_t)h->ldr * K * 2);
+    add(h->gb_len, K * 8);
+    add(h->ib_len, K * 8);
+    add(h->ib_ant, K * 4);
+    add(h->iter_dev, K * 4);
+    add(h->routes, ma * h->ldr * K * 2);
+    add(h->lengths, ma * K * 8);
+    add(h->fallback_count, 8);
+    if (h->ls_moves) add(h->ls_moves, 8);
+    return v;
+}
+
+StateHeader state_header(const mmas_ctx* h, int64_t payload) {
+    StateHeader H{};
+    H.magic = kStateMagic;
+    H.version = 1;
+    H.n = h->n;
+    H.cl_ld = h->cl_ld;
+    H.m = h->m;
+    H.m_local = h->m_local;
+    H.ant_lo = h->ant_lo;
+    H.colonies = h->colonies;
+    H.lean = h->lean ? 1 : 0;
+    H.lean_cap = h->lean_cap;
+    H.dtab = h->dtab;
+    H.iteration = h->iteration;
+    H.seed = h->cfg.seed;
+    H.alpha = h->cfg.alpha;
+    H.beta = h->cfg.beta;
+    H.rho = h->cfg.rho;
+    H.p_best = h->cfg.p_best;
+    H.deposit = h->cfg.deposit;
+    H.fallback = h->cfg.fallback;
+    H.local_search = h->cfg.local_search;
+    H.tabu = h->cfg.tabu;
+    H.selection = h->cfg.selection;
+    H.world = h->cfg.world;
+    H.rank = h->cfg.rank;
+    H.payload = payload;
+    return H;
+}
+}  // namespace
+
+int64_t mmas_state_bytes(mmas_ctx* h) {
+    int st = check(h);
+    if (st) return st;
+    int64_t total = sizeof(StateHeader);
+    for (auto& sgm : state_segments(h)) total += (int64_t)sgm.second;
+    return total;
+}
+
+int mmas_save_state(mmas_ctx* h, void* host_buf, int64_t bytes) {
+    int st = check(h);
+    if (st) return st;
+    const int64_t need = mmas_state_bytes(h);
+    if (!host_buf || bytes < need) return fail(MMAS_EINVAL, "host_buf is NULL or smaller than mmas_state_bytes");
+    CU(cudaSetDevice(h->device));
+    unsigned char* out = static_cast<unsigned char*>(host_buf);
+    const StateHeader H = state_header(h, need - (int64_t)sizeof(StateHeader));
+    std::memcpy(out, &H, sizeof(H));
+    size_t off = sizeof(H);
+    for (auto& sgm : state_segments(h)) {
+        CU(cudaMemcpyAsync(out + off, sgm.first, sgm.second, cudaMemcpyDeviceToHost, h->stream));
+        off += sgm.second;
+    }
+    CU(cudaStreamSynchronize(h->stream));
+    return MMAS_OK;
+}
+
+int mmas_load_state(mmas_ctx* h, const void* host_buf, int64_t bytes) {
+    int st = check(h);
+    if (st) return st;
+    const int64_t need = mmas_state_bytes(h);
+    if (!host_buf || bytes < need) return fail(MMAS_EINVAL, "host_buf is NULL or smaller than mmas_state_bytes");
+    const unsigned char* in = static_cast<const unsigned char*>(host_buf);
+    StateHeader H;
+    std::memcpy(&H, in, sizeof(H));
+    StateHeader mine = state_header(h, need - (int64_t)sizeof(StateHeader));
+    mine.iteration = H.iteration;   // the one field the checkpoint sets
+    if (H.magic != kStateMagic || H.version != 1 || std::memcmp(&H, &mine, sizeof(H)) != 0)
+        return fail(MMAS_EINVAL, "checkpoint does not match this context (instance size, colony, parameters or rank)");
+    CU(cudaSetDevice(h->device));
+    CU(cudaStreamSynchronize(h->stream));
+    size_t off = sizeof(H);
+    for (auto& sgm : state_segments(h)) {
+        CU(cudaMemcpyAsync(sgm.first, in + off, sgm.second, cudaMemcpyHostToDevice, h->stream));
+        off += sgm.second;
+    }
+    CU(cudaStreamSynchronize(h->stream));
+    h->iteration = H.iteration;
+    return MMAS_OK;
+}
+
 }  // extern "C"
 
 // Debug: copy the construct_cl_kernel phase timestamps (a -DMMAS_TRACE build; see
