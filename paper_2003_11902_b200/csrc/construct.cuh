@@ -615,10 +615,10 @@ template <class Tabu>
 __device__ __forceinline__ void scan_unvisited_staged(const float* __restrict__ row, const Tabu& tabu, int n, int ld,
                                                       uint32_t fb_off, uint32_t step, uint32_t ant, uint32_t iter,
                                                       PhiloxKey key, int lane, int warp, uint32_t& best_mag,
-                                                      uint32_t& best_c) {
+                                                      uint32_t& best_c, int part = 0, int nparts = 1) {
     const int nchunks = (n + kFbChunk - 1) / kFbChunk;   // <= 32 (n < 65536)
     uint32_t need = 0;
-    for (int c = 0; c < nchunks; ++c) {
+    for (int c = part; c < nchunks; c += nparts) {   // (cooperative scans: this warp's chunks)
         bool full = true;
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -797,6 +797,28 @@ __device__ __noinline__ void fused_update(const UpdateArgs U, unsigned int* epoc
 
 
 // ---------------------------------------------------------------------------
+// Paired fallback scans (C5: the L2-table kernel at a few ant warps per SM, rows streamed
+// from HBM through shared memory).  A fallback there is ~70 chunk trips on the ant's serial
+// chain while the SM idles (~25 % issue active); so the block's warps pair up: the even warp
+// of a pair builds an ant, the odd one only helps with its fallbacks.  The ant warp posts
+// (current city, step, ant), both meet at the pair's named barrier, each scans every other
+// 2048-city chunk with its own buffers, the helper posts its (key, city) minimum, both meet
+// again, and the ant warp takes the minimum of the two -- the same argmax, ties to the lowest
+// city (each warp's cities ascend; the pairwise minimum is lexicographic).
+// ---------------------------------------------------------------------------
+struct CoopSlot {
+    uint32_t cur, step, ant, done;
+    uint32_t mag, city;   // the helper's partial result
+};
+__device__ __forceinline__ void pair_barrier(int pair) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "r"(64) : "memory");
+}
+__device__ __forceinline__ void warp_best(uint32_t mag, uint32_t city, uint32_t& bmag, uint32_t& bcity) {
+    bmag = __reduce_min_sync(kFull, mag);
+    bcity = __reduce_min_sync(kFull, mag == bmag ? city : kNone);
+}
+
+// ---------------------------------------------------------------------------
 // Candidate-list construction (rows a1, a2, a3, a5-local).
 // kSlots = ceil(cl/32) candidate slots per lane; kSmemTable: the n x cl
 // (1/w, id) table is staged once per block into shared memory by TMA bulk
@@ -808,7 +830,7 @@ template <int kSlots, bool kSmemTable, bool kRegTabu, bool kFull32, bool kWide =
 // L2-table variants run 4-warp blocks and need 4 blocks per SM (128 registers) when the
 // colony fills the SMs (C3's 3795 ants: 25 warps per SM); with kWide (few ant warps per SM,
 // C5) the register budget is left to the compiler
-__global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmemTable || kWide) ? 1 : 4)
+__global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemTable ? 1 : (kWide ? 3 : 4))
     construct_cl_kernel(const ConstructArgs A) {
     // colony (grid.y, R29): its per-colony pointers as locals (a modified copy of the whole
     // argument struct would live in registers through the step loop); the tail takes a copy
@@ -867,11 +889,19 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
         __syncthreads();   // the barrier is initialised before anyone waits on it
         mbar_wait(bar, 0);
     }
+    // paired fallback scans (C5; see CoopSlot): even warp = ant, odd warp = its helper
+    constexpr bool kCoop = !kSmemTable && kWide && !kRegTabu;
+    __shared__ CoopSlot s_coop[kCoop ? 8 : 1];
+    const bool coop = kCoop && A.coop_fb && A.fb_row_off;
+    const bool helper = coop && (warp & 1);
+    const int pair = warp >> 1;
+    const int ant_slot = coop ? pair : warp, ants_per_block = coop ? (A.warps_per_block >> 1) : A.warps_per_block;
     trace_mark(1);
     unsigned long long wbest = ~0ull;
     long long wfb = 0;
 
-    for (int al = blockIdx.x * A.warps_per_block + warp; al < A.m_local; al += gridDim.x * A.warps_per_block) {
+    for (int al = blockIdx.x * ants_per_block + ant_slot; !helper && al < A.m_local;
+         al += gridDim.x * ants_per_block) {
         const uint32_t ant = (uint32_t)(A.ant_lo + al);
         Tabu tabu;
         tabu.init(tabu_base, nwords, lane);
@@ -1072,7 +1102,24 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
                 }
                 if (A.fallback_argmax)
                     scan_unvisited<true>(row, tabu, n, (uint32_t)s, ant, iter, c_key, lane, fm, fc);
-                else if (!kSmemTable && A.fb_row_off) {
+                else if (kCoop && coop) {
+                    if (lane == 0) {
+                        s_coop[pair].cur = cur;
+                        s_coop[pair].step = (uint32_t)s;
+                        s_coop[pair].ant = ant;
+                        s_coop[pair].done = 0u;
+                    }
+                    pair_barrier(pair);   // request posted: the helper scans the odd chunks
+                    scan_unvisited_staged(row, tabu, n, A.ld, A.fb_row_off, (uint32_t)s, ant, iter, c_key, lane,
+                                          warp, fm, fc, 0, 2);
+                    uint32_t m0, c0;
+                    warp_best(fm, fc, m0, c0);
+                    pair_barrier(pair);   // the helper's partial result is posted
+                    const uint32_t m1 = s_coop[pair].mag, c1 = s_coop[pair].city;
+                    const bool take = m1 < m0 || (m1 == m0 && c1 < c0);
+                    fm = take ? m1 : m0;
+                    fc = take ? c1 : c0;
+                } else if (!kSmemTable && A.fb_row_off) {
                     scan_unvisited_staged(row, tabu, n, A.ld, A.fb_row_off, (uint32_t)s, ant, iter, c_key, lane,
                                           warp, fm, fc);
                 } else if (!kSmemTable && A.prune_fallback)
@@ -1189,6 +1236,33 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, (kSmem
         __syncwarp();
         if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane, A.lengths + (long long)col * A.cs.ants));
         wfb += fb;
+    }
+    if constexpr (kCoop) {
+        if (coop) {
+            if (!helper) {
+                if (lane == 0) s_coop[pair].done = 1u;
+                pair_barrier(pair);   // release the helper
+            } else {
+                // the helper: serve the ant warp's fallbacks until it is done
+                SmemTabu tv;
+                tv.t = reinterpret_cast<uint32_t*>(g_smem + tab_off) + (warp - 1) * nwords;
+                while (true) {
+                    pair_barrier(pair);
+                    if (s_coop[pair].done) break;
+                    const uint32_t hcur = s_coop[pair].cur, hs = s_coop[pair].step, hant = s_coop[pair].ant;
+                    uint32_t fm = kNone, fc = kNone;
+                    scan_unvisited_staged(c_inv_w + (size_t)hcur * A.ld, tv, n, A.ld, A.fb_row_off, hs, hant, iter,
+                                          c_key, lane, warp, fm, fc, 1, 2);
+                    uint32_t hm, hc;
+                    warp_best(fm, fc, hm, hc);
+                    if (lane == 0) {
+                        s_coop[pair].mag = hm;
+                        s_coop[pair].city = hc;
+                    }
+                    pair_barrier(pair);
+                }
+            }
+        }
     }
     pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
     trace_mark(2);

@@ -125,6 +125,7 @@ struct mmas_ctx {
     bool rwm = false;           // MMAS_SELECT_RWM: construct_rwm_kernel (R28)
     int slots = 1;
     int cons_warps = 4, cons_grid = 1;
+    bool coop_fb = false;                   // L2-table kernel: paired fallback scans (2 ants + 2 helpers per block)
     size_t cons_smem = 0;
     uint32_t fb_row_off = 0;                // L2-table kernel: fallback row buffer in smem
     uint32_t tb_inv = 0, tb_id = 0;
@@ -299,6 +300,7 @@ ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = f
         A.l2_prefetch_bytes = (h->cl > 0 && !h->rwm && !h->lean && 2 * bytes * h->colonies <= (unsigned long long)h->l2_bytes &&
                                !(pf && pf[0] == '0')) ? bytes : 0ull;
     }
+    A.coop_fb = h->coop_fb ? 1 : 0;
     A.warps_per_block = h->cons_warps;
     A.table_bytes_inv = h->tb_inv;
     A.table_bytes_id = h->tb_id;
@@ -756,8 +758,24 @@ int setup(mmas_ctx* h) {
     }
 
     clk.mark("memsets + eta^beta", h->stream);
-    // candidate lists (host, parallel over rows)
-    if (h->cl > 0) {
+    // candidate lists: on the device (cand_lists_kernel) where a row's distances fit in shared
+    // memory, else on the host (parallel over rows)
+    const bool dev_cand = (size_t)n * 4 <= (size_t)h->smem_optin - 2048 && !std::getenv("MMAS_HOST_CAND");
+    if (h->cl > 0 && dev_cand) {
+        if (h->cl_ld != h->cl) {   // padding slots: the row's own city (always visited)
+            std::vector<uint16_t> padded((size_t)n * h->cl_ld);
+            for (int i = 0; i < n; ++i)
+                for (int k = 0; k < h->cl_ld; ++k) padded[(size_t)i * h->cl_ld + k] = (uint16_t)i;
+            CU(cudaMemcpyAsync(h->cand_id, padded.data(), sizeof(uint16_t) * padded.size(), cudaMemcpyHostToDevice,
+                               h->stream));
+            CU(cudaStreamSynchronize(h->stream));
+        }
+        cudaFuncSetAttribute(cand_lists_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin - 2048);
+        cand_lists_kernel<<<std::min(n, 8 * h->num_sms), 256, (size_t)n * 4, h->stream>>>(h->xy, n, h->cl, h->cand_id,
+                                                                                          h->cl_ld);
+        h->launches++;
+        CU(cudaGetLastError());
+    } else if (h->cl > 0) {
         std::vector<uint16_t> cand;
         candidate_lists(c.coords, n, h->cl, cand);
         if (h->cl_ld != h->cl) {   // pad every row to cl_ld slots with the row's own city
@@ -818,8 +836,9 @@ int setup(mmas_ctx* h) {
     // initial limits from the NN tour (Alg. 1); F from libm pow (R2)
     {
         // NN tour on the device (one block; the host loop was O(n^2) on one core)
+        // (scratch from the context's pool -- dalloc -- not the device's default pool)
         long long* d_len = nullptr;
-        CU(cudaMallocAsync(reinterpret_cast<void**>(&d_len), sizeof(long long), h->stream));
+        if ((st = dalloc(&d_len, 1))) return st;
         // integral coordinates within +-16383: the NN tour's distances in 32-bit arithmetic
         short2* d_xys = nullptr;
         {
@@ -833,19 +852,20 @@ int setup(mmas_ctx* h) {
                     xs[(size_t)i] = make_short2((short)x, (short)y);
             }
             if (integral) {
-                CU(cudaMallocAsync(reinterpret_cast<void**>(&d_xys), sizeof(short2) * n, h->stream));
+                if ((st = dalloc(&d_xys, (size_t)n))) return st;
                 CU(cudaMemcpyAsync(d_xys, xs.data(), sizeof(short2) * n, cudaMemcpyHostToDevice, h->stream));
                 CU(cudaStreamSynchronize(h->stream));
             }
         }
+        clk.mark("NN tour inputs", h->stream);
         nn_tour_kernel<<<1, nn_threads(n), 0, h->stream>>>(h->xy, d_xys, n, d_len);
-        if (d_xys) CU(cudaFreeAsync(d_xys, h->stream));
+        if (d_xys) CU(h->pooled ? cudaFreeAsync(d_xys, h->stream) : cudaFree(d_xys));
         h->launches++;
         CU(cudaGetLastError());
         long long len = 0;
         CU(cudaMemcpyAsync(&len, d_len, sizeof(len), cudaMemcpyDeviceToHost, h->stream));
-        CU(cudaFreeAsync(d_len, h->stream));
         CU(cudaStreamSynchronize(h->stream));
+        CU(h->pooled ? cudaFreeAsync(d_len, h->stream) : cudaFree(d_len));
         h->nn_len = len;
     }
     const double pn = std::pow(c.p_best, 1.0 / (double)n);
@@ -906,7 +926,7 @@ int setup(mmas_ctx* h) {
     }
     CU(cudaStreamSynchronize(h->stream));   // lim goes out of scope
 
-    clk.mark("NN tour + trails", h->stream);
+    clk.mark("NN tour kernel + trails", h->stream);
     // ---- construction launch plan ----
     // dynamic shared memory a construction kernel may take: the opt-in limit minus its
     // static shared memory (block_finish's slots; 128 B, reserve 1 KB)
@@ -968,6 +988,14 @@ int setup(mmas_ctx* h) {
             if (hbm_rows && 2 * (with_row + 1024) <= (size_t)h->smem_optin && !std::getenv("MMAS_NO_FB_ROW")) {
                 h->fb_row_off = (uint32_t)off;
                 h->cons_smem = with_row;
+                // paired fallback scans (construct.cuh CoopSlot): at fewer than 16 ant warps per SM
+                // (the uncapped-register instantiation), n > 1024, one slot per lane, WRS fallback:
+                // each block's four warps build two ants, each with a helper for its scans
+                const char* cf = std::getenv("MMAS_COOP_FB");
+                h->coop_fb = !(cf && cf[0] == '0') && !h->reg_tabu && h->slots == 1 &&
+                             (long long)h->m_local * h->colonies < 16ll * h->num_sms &&
+                             c.fallback == MMAS_FALLBACK_WRS && c.pheromone != MMAS_PHEROMONE_LEAN;
+                if (h->coop_fb) h->cons_grid = std::max(1, (h->m_local + 1) / 2);
             }
         }
     } else if (h->cfg.tabu == MMAS_TABU_COMPACT) {

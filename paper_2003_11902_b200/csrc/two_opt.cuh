@@ -259,7 +259,10 @@ namespace mmas {
 // so a round retires several pops for the latency of one evaluation; the
 // reversal of an applied move is spread over all kLsWarps * 32 lanes.
 // ---------------------------------------------------------------------------
-constexpr int kLsWarps = 8;
+#ifndef MMAS_LS_WARPS
+#define MMAS_LS_WARPS 8
+#endif
+constexpr int kLsWarps = MMAS_LS_WARPS;   // (MMAS_LS_WARPS: A/B builds)
 
 struct MoveEval {
     int found, dir, b, c, d;
