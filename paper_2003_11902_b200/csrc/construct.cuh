@@ -300,15 +300,11 @@ __device__ __forceinline__ void scan_unvisited(const float* __restrict__ row, co
 // the uniform of the dense scan (R13), so the argmax -- ties to the lowest id -- is the dense one.
 // (out of line and by value -- it leaves the tabu as it found it -- so the rarely taken lean
 // path adds no registers to the construction's step loop)
+// phase 1: hide the row's unvisited sparse cities (warp-collective marks, one city at a time);
+// bit r of the result: this lane's slot r * 32 + lane was hidden
 template <class Tabu>
-__device__ __noinline__ uint32_t lean_fallback(const LeanArgs Ln, const double2* __restrict__ xy, int cur,
-                                               Tabu tabu, int n, int alpha, uint32_t step,
-                                                  uint32_t ant, uint32_t iter, PhiloxKey key, int lane) {
-    const float b = __ldcg(Ln.bg + Ln.parity);   // the background trail after the last update
+__device__ __forceinline__ uint32_t lean_hide(const LeanArgs& Ln, int cur, Tabu& tabu, int n, int lane) {
     const uint16_t* ids = Ln.sp_id + (size_t)cur * Ln.cap;
-    const float* invs = Ln.sp_inv + (size_t)cur * Ln.cap;
-    // 1. hide the row's unvisited sparse cities (warp-collective marks, one city at a time);
-    //    bit r of `hid`: this lane's slot r * 32 + lane was hidden
     uint32_t hid = 0;
     tabu.prepare(lane);
     for (int r = 0; r * 32 < Ln.cap; ++r) {
@@ -324,13 +320,22 @@ __device__ __noinline__ uint32_t lean_fallback(const LeanArgs Ln, const double2*
         tabu.sync();
     }
     tabu.prepare(lane);
-    // 2. background scan: lane l takes the 4-city groups 128t + 4l (one Philox per group),
-    //    two groups per trip (independent chains); with integral coordinates the group's four
-    //    coordinates are one 16-byte load and 1 / choice_info comes from the table by distance
+    return hid;
+}
+
+// phase 2: the background scan over the trips part, part + nparts, ... (lane l: the 4-city
+// groups 128t + 4l, one Philox per group, two groups per trip); with integral coordinates the
+// group's four coordinates are one 16-byte load and 1 / choice_info comes from the table by
+// distance.  Per-lane minimum in (bm, bc), ascending cities.
+template <class Tabu>
+__device__ __forceinline__ void lean_scan(const LeanArgs& Ln, const double2* __restrict__ xy, int cur,
+                                          const Tabu& tabu, int n, int alpha, uint32_t step, uint32_t ant,
+                                          uint32_t iter, PhiloxKey key, int lane, int part, int nparts, uint32_t& bm,
+                                          uint32_t& bc) {
+    const float b = __ldcg(Ln.bg + Ln.parity);   // the background trail after the last update
     const double2 xc = __ldg(xy + cur);
     const short2 xcs = Ln.xys ? __ldg(Ln.xys + cur) : make_short2(0, 0);
     const float ba = pow_alpha(b, alpha);
-    uint32_t bm = kNone, bc = kNone;
     auto group = [&](int c0, uint32_t nib) {
         if (nib == 0xFu) return;
         const uint4 x = philox4x32_10(ctr_city((uint32_t)c0 >> 2, step, ant, iter), key);
@@ -357,14 +362,22 @@ __device__ __noinline__ uint32_t lean_fallback(const LeanArgs Ln, const double2*
             if (mag < bm) { bm = mag; bc = (uint32_t)(c0 + q); }   // ascending cities: ties keep the lower
         }
     };
-    for (int base = 0; base < n; base += 256) {
+    for (int base = 256 * part; base < n; base += 256 * nparts) {
         const int ca = base + 4 * lane, cb = ca + 128;
         const uint32_t na = chunk_nibble(tabu, ca, n), nb = chunk_nibble(tabu, cb, n);
         if (!__any_sync(kFull, (na & nb) != 0xFu)) continue;
         group(ca, na);
         group(cb, nb);
     }
-    // 3. unhide the hidden ones and evaluate them with their stored 1 / choice_info
+}
+
+// phase 3: unhide the hidden ones and evaluate them with their stored 1 / choice_info
+template <class Tabu>
+__device__ __forceinline__ void lean_unhide(const LeanArgs& Ln, int cur, Tabu& tabu, uint32_t hid, uint32_t step,
+                                            uint32_t ant, uint32_t iter, PhiloxKey key, int lane, uint32_t& bm,
+                                            uint32_t& bc) {
+    const uint16_t* ids = Ln.sp_id + (size_t)cur * Ln.cap;
+    const float* invs = Ln.sp_inv + (size_t)cur * Ln.cap;
     for (int r = 0; r * 32 < Ln.cap; ++r) {
         const uint32_t j = ids[r * 32 + lane];
         const bool h = (hid >> r) & 1u;
@@ -380,7 +393,27 @@ __device__ __noinline__ uint32_t lean_fallback(const LeanArgs Ln, const double2*
         }
         tabu.sync();
     }
+}
+
+template <class Tabu>
+__device__ __forceinline__ uint32_t lean_fallback(const LeanArgs& Ln, const double2* __restrict__ xy, int cur,
+                                                  Tabu& tabu, int n, int alpha, uint32_t step, uint32_t ant,
+                                                  uint32_t iter, PhiloxKey key, int lane) {
+    const uint32_t hid = lean_hide(Ln, cur, tabu, n, lane);
+    uint32_t bm = kNone, bc = kNone;
+    lean_scan(Ln, xy, cur, tabu, n, alpha, step, ant, iter, key, lane, 0, 1, bm, bc);
+    lean_unhide(Ln, cur, tabu, hid, step, ant, iter, key, lane, bm, bc);
     return warp_select(bm, bc);
+}
+// Out of line and by value (it leaves the tabu as it found it), for the kernels with a
+// 255-register budget (C1, C2), whose step loop's allocation it would otherwise perturb
+// (A/B: 0.2259 -> 0.2244 ms); under a 128-register cap the call's saved registers spill, so
+// those variants inline it.
+template <class Tabu>
+__device__ __noinline__ uint32_t lean_fallback_ool(const LeanArgs Ln, const double2* __restrict__ xy, int cur,
+                                                   Tabu tabu, int n, int alpha, uint32_t step, uint32_t ant,
+                                                   uint32_t iter, PhiloxKey key, int lane) {
+    return lean_fallback(Ln, xy, cur, tabu, n, alpha, step, ant, iter, key, lane);
 }
 
 template <bool kArgmax, class Tabu>
@@ -1094,10 +1127,42 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
                 tabu.prepare(lane);
                 const float* row = c_inv_w + (size_t)cur * A.ld;
                 uint32_t fm = kNone, fc = kNone;
+                if constexpr (kCoop) {
+                    if (coop && A.lean.cand_tau) {
+                        // the lean scan, paired (see CoopSlot): hidden sparse cities stay marked in
+                        // the ant's shared-memory tabu while both warps scan their trips
+                        const uint32_t hid = lean_hide(A.lean, (int)cur, tabu, n, lane);
+                        if (lane == 0) {
+                            s_coop[pair].cur = cur;
+                            s_coop[pair].step = (uint32_t)s;
+                            s_coop[pair].ant = ant;
+                            s_coop[pair].done = 0u;
+                        }
+                        pair_barrier(pair);
+                        uint32_t bm2 = kNone, bc2 = kNone;
+                        lean_scan(A.lean, A.xy, (int)cur, tabu, n, A.alpha, (uint32_t)s, ant, iter, c_key, lane, 0, 2,
+                                  bm2, bc2);
+                        pair_barrier(pair);   // the helper's partial result is posted
+                        const uint32_t m1 = s_coop[pair].mag, c1 = s_coop[pair].city;
+                        if (lane == 0 && (m1 < bm2 || (m1 == bm2 && c1 < bc2))) {
+                            bm2 = m1;
+                            bc2 = c1;
+                        }
+                        lean_unhide(A.lean, (int)cur, tabu, hid, (uint32_t)s, ant, iter, c_key, lane, bm2, bc2);
+                        commit(warp_select(bm2, bc2), s);
+                        return;
+                    }
+                }
                 if (A.lean.cand_tau) {
                     // memory-lean pheromone (R30): no inv_w row; the scan recomputes it
-                    commit(lean_fallback(A.lean, A.xy, (int)cur, tabu, n, A.alpha, (uint32_t)s, ant, iter, c_key, lane),
-                           s);
+                    if constexpr (kSmemTable && !kWide)
+                        commit(lean_fallback_ool(A.lean, A.xy, (int)cur, tabu, n, A.alpha, (uint32_t)s, ant, iter, c_key,
+                                                 lane),
+                               s);
+                    else
+                        commit(lean_fallback(A.lean, A.xy, (int)cur, tabu, n, A.alpha, (uint32_t)s, ant, iter, c_key,
+                                             lane),
+                               s);
                     return;
                 }
                 if (A.fallback_argmax)
@@ -1251,8 +1316,11 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
                     if (s_coop[pair].done) break;
                     const uint32_t hcur = s_coop[pair].cur, hs = s_coop[pair].step, hant = s_coop[pair].ant;
                     uint32_t fm = kNone, fc = kNone;
-                    scan_unvisited_staged(c_inv_w + (size_t)hcur * A.ld, tv, n, A.ld, A.fb_row_off, hs, hant, iter,
-                                          c_key, lane, warp, fm, fc, 1, 2);
+                    if (A.lean.cand_tau)
+                        lean_scan(A.lean, A.xy, (int)hcur, tv, n, A.alpha, hs, hant, iter, c_key, lane, 1, 2, fm, fc);
+                    else
+                        scan_unvisited_staged(c_inv_w + (size_t)hcur * A.ld, tv, n, A.ld, A.fb_row_off, hs, hant, iter,
+                                              c_key, lane, warp, fm, fc, 1, 2);
                     uint32_t hm, hc;
                     warp_best(fm, fc, hm, hc);
                     if (lane == 0) {

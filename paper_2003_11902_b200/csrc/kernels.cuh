@@ -105,7 +105,7 @@ __device__ __forceinline__ int32_t euc2d(double2 p, double2 q) {
 // (|error| << 1/2 except next to a half-integer) and one integer correction:
 // (2k-1)^2 <= 4S < (2k+1)^2  <=>  k^2 - k < S <= k^2 + k   (4S is even, (2k+-1)^2 odd).
 // No fp64 (DSQRT is a ~20-instruction subroutine with a long DFMA chain).  Pinned against
-// the double formula in tests/test_capi.py (exhaustive S <= 2^22, random S < 2^31, and the
+// the double formula in tests/test_int_distance.py (exhaustive S <= 2^22, random S < 2^31, and the
 // near-half-integer cases k^2 + k, k^2 + k + 1).
 __device__ __forceinline__ int32_t euc2d_int(short2 p, short2 q) {
     const int dx = (int)p.x - (int)q.x, dy = (int)p.y - (int)q.y;

@@ -994,7 +994,7 @@ int setup(mmas_ctx* h) {
                 const char* cf = std::getenv("MMAS_COOP_FB");
                 h->coop_fb = !(cf && cf[0] == '0') && !h->reg_tabu && h->slots == 1 &&
                              (long long)h->m_local * h->colonies < 16ll * h->num_sms &&
-                             c.fallback == MMAS_FALLBACK_WRS && c.pheromone != MMAS_PHEROMONE_LEAN;
+                             c.fallback == MMAS_FALLBACK_WRS;
                 if (h->coop_fb) h->cons_grid = std::max(1, (h->m_local + 1) / 2);
             }
         }

@@ -260,7 +260,7 @@ namespace mmas {
 // reversal of an applied move is spread over all kLsWarps * 32 lanes.
 // ---------------------------------------------------------------------------
 #ifndef MMAS_LS_WARPS
-#define MMAS_LS_WARPS 8
+#define MMAS_LS_WARPS 5   // warps per ant (sweep on C5: 2: 192, 3: 158, 4: 147, 5: 143, 6: 145, 8: 150, 12: 187, 16: 221 ms)
 #endif
 constexpr int kLsWarps = MMAS_LS_WARPS;   // (MMAS_LS_WARPS: A/B builds)
 

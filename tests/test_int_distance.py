@@ -1,4 +1,4 @@
-"""The 2-opt kernels' integer EUC_2D path (two_opt.cuh euc2d_int) against the R12 formula.
+"""The integer EUC_2D path (kernels.cuh euc2d_int: the 2-opt kernels, the NN tour, the lean fallback scans) against the R12 formula.
 
 For integral coordinates with |x|, |y| <= 16383 the kernels compute nint(sqrt(S)),
 S = dx^2 + dy^2 < 2^31, as an approximate fp32 sqrt rounded to the nearest integer k0 plus
