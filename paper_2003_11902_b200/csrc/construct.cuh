@@ -47,6 +47,8 @@ struct RegTabuX {
     __device__ __forceinline__ void init(uint32_t*, int, int) { w = 0u; wt = 0u; }
     // every lane of the warp must call word()/visited() (warp shuffle); kLazyW: after prepare()
     __device__ __forceinline__ uint32_t word(int idx) const { return __shfl_sync(kFull, w, idx); }
+    // the calling lane's own word (idx == lane; no shuffle)
+    __device__ __forceinline__ uint32_t own(int) const { return w; }
     __device__ __forceinline__ bool visited(uint32_t c) const { return (word((int)(c >> 5)) >> (c & 31)) & 1u; }
     // bit 31 = "c visited" (other bits garbage); lanes may pass any c < 1024
     __device__ __forceinline__ uint32_t top_bit(uint32_t c) const {
@@ -82,6 +84,7 @@ struct SmemTabu {
         __syncwarp();
     }
     __device__ __forceinline__ uint32_t word(int idx) const { return t[idx]; }
+    __device__ __forceinline__ uint32_t own(int idx) const { return t[idx]; }
     __device__ __forceinline__ bool visited(uint32_t c) const { return (t[c >> 5] >> (c & 31)) & 1u; }
     __device__ __forceinline__ uint32_t top_bit(uint32_t c) const { return t[c >> 5] << (~c & 31u); }
     __device__ __forceinline__ void mark(uint32_t c, int lane) {
@@ -414,6 +417,159 @@ __device__ __noinline__ uint32_t lean_fallback_ool(const LeanArgs Ln, const doub
                                                    Tabu tabu, int n, int alpha, uint32_t step, uint32_t ant,
                                                    uint32_t iter, PhiloxKey key, int lane) {
     return lean_fallback(Ln, xy, cur, tabu, n, alpha, step, ant, iter, key, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Lane-compacted fallback (row a3, R9) for the late steps of a tour.  A candidate list is
+// exhausted mostly near the end of a construction (C2's driver window: median step 941 of
+// 1002, ~6 % of the cities unvisited), where the trip scans above still draw a Philox and a
+// key for every 4-city group of the row (~2,900 cycles of the ant's chain at any U).  Here
+// each lane takes the unvisited cities of its own tabu bits -- no transpose, list or prefix
+// sum: with the register tabu lane l owns cities l, l + 32, l + 64, ... (the transposed word
+// wt the candidate test keeps anyway), with the shared-memory tabu the words l, l + 32, ... --
+// and evaluates them eight (or four) at a time: the scattered inv_w loads issued first, then
+// independent Philox / log chains (per city the Philox of its group, word c & 3: the uniform
+// the dense scan draws, R13).  The result is the same lexicographic (magnitude, city)
+// minimum, ties to the lowest id, so the argmax is the dense one bit for bit.  Returns kNone
+// (nothing evaluated) when some lane owns more than `cap` unvisited cities; the caller then
+// runs the trip scan.  Out of line: the step loops' register allocation stays as it is.
+// p ? a : b as one PTX selp (opaque to the compiler's select-to-branch conversion)
+__device__ __forceinline__ uint32_t selp_u32(uint32_t a, uint32_t b, bool p) {
+    uint32_t r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.b32 %0, %1, %2, q;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b), "r"((uint32_t)p));
+    return r;
+}
+// det_log2 (rng.cuh, R14) with its range reduction written as selects: the same operations
+// on the same values (bit-identical), but no branch, so ptxas interleaves several of them
+__device__ __forceinline__ float det_log2_sel(float u) {
+    const uint32_t b = __float_as_uint(u);
+    const uint32_t mant = b & 0x007FFFFFu;
+    const bool hi = mant > 0x003504F3u;
+    const int e = (int)(b >> 23) - 127 + (hi ? 1 : 0);
+    const uint32_t mb = mant | (hi ? 0x3F000000u : 0x3F800000u);
+    const float f = __fsub_rn(__uint_as_float(mb), 1.0f);
+    float p = 0.12583690881729126f;
+    p = __fmaf_rn(p, f, -0.20726971328258514f);
+    p = __fmaf_rn(p, f, 0.21571563184261322f);
+    p = __fmaf_rn(p, f, -0.23894482851028442f);
+    p = __fmaf_rn(p, f, 0.28791624307632446f);
+    p = __fmaf_rn(p, f, -0.3607036769390106f);
+    p = __fmaf_rn(p, f, 0.48091062903404236f);
+    p = __fmaf_rn(p, f, -0.7213473320007324f);
+    p = __fmaf_rn(p, f, 1.4426950216293335f);
+    const float ef = __fsub_rn(__int_as_float(0x4B400000 + e), 12582912.0f);
+    return __fmaf_rn(f, p, ef);
+}
+
+struct LaneCitiesReg {   // register tabu: bit k of ~wt = city 32 k + lane
+    uint32_t f;
+    int lane;
+    __device__ __forceinline__ LaneCitiesReg(uint32_t wt, int n, int l) : lane(l) {
+        const int cnt = (n - l + 31) >> 5;   // cities 32 k + l < n
+        f = ~wt & (cnt >= 32 ? 0xFFFFFFFFu : cnt <= 0 ? 0u : (1u << cnt) - 1u);
+    }
+    __device__ __forceinline__ int count() const { return __popc(f); }
+    __device__ __forceinline__ uint32_t next() {   // branch-free (kNone when exhausted)
+        const uint32_t c = f ? 32u * (uint32_t)(__ffs(f) - 1) + (uint32_t)lane : kNone;
+        f &= f - 1u;
+        return c;
+    }
+};
+struct LaneCitiesSmem {   // shared-memory tabu: the words lane, lane + 32, ...
+    const uint32_t* t;
+    int n, nw, wi;
+    uint32_t f;
+    __device__ __forceinline__ uint32_t free_word(int w) const {
+        uint32_t x = ~t[w];
+        const int rem = n - (w << 5);
+        if (rem < 32) x &= (1u << rem) - 1u;   // cities >= n do not exist
+        return x;
+    }
+    __device__ __forceinline__ LaneCitiesSmem(const SmemTabu& tb, int n_, int lane)
+        : t(tb.t), n(n_), nw((n_ + 31) >> 5), wi(lane) {
+        f = wi < nw ? free_word(wi) : 0u;
+    }
+    __device__ __forceinline__ int count() const {
+        int c = 0;
+        for (int w = wi; w < nw; w += 32) c += __popc(free_word(w));
+        return c;
+    }
+    __device__ __forceinline__ uint32_t next() {
+        while (!f) {
+            wi += 32;
+            if (wi >= nw) return kNone;
+            f = free_word(wi);
+        }
+        const uint32_t b = (uint32_t)(__ffs(f) - 1);
+        f &= f - 1u;
+        return 32u * (uint32_t)wi + b;
+    }
+};
+template <bool kLazyW>
+__device__ __forceinline__ LaneCitiesReg lane_cities(const RegTabuX<kLazyW>& t, int n, int lane) {
+    return LaneCitiesReg(t.wt, n, lane);
+}
+__device__ __forceinline__ LaneCitiesSmem lane_cities(const SmemTabu& t, int n, int lane) {
+    return LaneCitiesSmem(t, n, lane);
+}
+
+template <class Tabu>
+__device__ __noinline__ uint32_t fallback_compact(const float* __restrict__ row, const Tabu tabu, int n, int cap,
+                                                  uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
+                                                  int lane) {
+    const long long t0 = trace_clock();
+#ifdef MMAS_TRACE
+    // timing experiments only (tools/fb_cycles.py): cap bit 30 = no row loads, bit 29 = no Philox
+    const bool x_noload = (cap >> 30) & 1, x_nophilox = (cap >> 29) & 1;
+    cap &= (1 << 29) - 1;
+#else
+    constexpr bool x_noload = false, x_nophilox = false;
+#endif
+    auto it = lane_cities(tabu, n, lane);
+    const int most = __reduce_max_sync(kFull, (uint32_t)it.count());
+    if (most > cap) return kNone;   // warp-uniform
+    const long long t1 = trace_clock();
+    uint32_t bm = kNone, bc = kNone;
+    // K cities per lane at a time, branch-free (a lane with fewer carries kNone), so the K
+    // Philox / log chains interleave
+    auto eval = [&](auto K, const uint32_t* c, const float* iv) {
+        constexpr int k = decltype(K)::value;
+        uint32_t mag[k];
+#pragma unroll
+        for (int j = 0; j < k; ++j) {
+            const uint32_t cc = c[j] == kNone ? 0u : c[j];
+            const uint4 x = x_nophilox ? make_uint4(cc * 0x9E3779B9u, cc, cc ^ step, cc + ant)
+                                       : philox4x32_10(ctr_city(cc >> 2, step, ant, iter), key);
+            const uint32_t q = cc & 3u;
+            // selects in PTX (selp): the compiler would otherwise branch around the unused words
+            // and the idle lanes' logs, which serialises the chains
+            const uint32_t xw = selp_u32(selp_u32(x.x, x.y, q == 0u), selp_u32(x.z, x.w, q == 2u), q < 2u);
+            mag[j] = selp_u32(kNone, key_magnitude(__fmul_rn(det_log2_sel(uniform_open(xw)), iv[j])), c[j] == kNone);
+        }
+        // a lane's cities ascend (k, then the words, ascending), so a strict "<" keeps the
+        // lowest of equal keys (R16)
+#pragma unroll
+        for (int j = 0; j < k; ++j) {
+            const bool take = mag[j] < bm;
+            bm = selp_u32(mag[j], bm, take);
+            bc = selp_u32(c[j], bc, take);
+        }
+    };
+    for (int r = 0; r < most; r += 8) {
+        uint32_t c[8];
+        float iv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c[j] = it.next();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) iv[j] = c[j] != kNone ? (x_noload ? 1.5f : __ldg(row + c[j])) : 0.f;
+        if (r + 4 < most) eval(std::integral_constant<int, 8>{}, c, iv);   // warp-uniform
+        else eval(std::integral_constant<int, 4>{}, c, iv);
+    }
+    const long long t2 = trace_clock();
+    const uint32_t res = warp_select(bm, bc);
+    trace_compact(lane, t0, t1, t2, trace_clock());
+    return res;
 }
 
 template <bool kArgmax, class Tabu>
@@ -1124,7 +1280,6 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
             if (best >= 0x80000000u) {   // every candidate visited: R9 fallback
                 ++fb;
                 const long long t_fb = trace_clock();
-                tabu.prepare(lane);
                 const float* row = c_inv_w + (size_t)cur * A.ld;
                 uint32_t fm = kNone, fc = kNone;
                 if constexpr (kCoop) {
@@ -1155,6 +1310,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
                 }
                 if (A.lean.cand_tau) {
                     // memory-lean pheromone (R30): no inv_w row; the scan recomputes it
+                    tabu.prepare(lane);
                     if constexpr (kSmemTable && !kWide)
                         commit(lean_fallback_ool(A.lean, A.xy, (int)cur, tabu, n, A.alpha, (uint32_t)s, ant, iter, c_key,
                                                  lane),
@@ -1165,6 +1321,17 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
                                s);
                     return;
                 }
+                if (A.fb_lane_cap && !A.fallback_argmax) {
+                    // late in the tour: each lane evaluates only its own unvisited cities
+                    const uint32_t c = fallback_compact(row, tabu, n, A.fb_lane_cap, (uint32_t)s, ant, iter, c_key, lane);
+                    if (c != kNone) {
+                        trace_fallback(t_fb, lane, n - s);
+                        trace_compact_entry(lane, t_fb);
+                        commit(c, s);
+                        return;
+                    }
+                }
+                tabu.prepare(lane);
                 if (A.fallback_argmax)
                     scan_unvisited<true>(row, tabu, n, (uint32_t)s, ant, iter, c_key, lane, fm, fc);
                 else if (kCoop && coop) {
@@ -1198,7 +1365,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
                 else
                     scan_unvisited<false>(row, tabu, n, (uint32_t)s, ant, iter, c_key, lane, fm, fc);
                 nxt = warp_select(fm, fc);
-                trace_fallback(t_fb, lane);
+                trace_fallback(t_fb, lane, n - s);
             }
             commit(nxt, s);
         };

@@ -63,13 +63,35 @@ __device__ __forceinline__ void trace_mark(int k) {
 // fallback scans: [0] cycles summed over every fallback (lane 0's clock), [1] their count;
 // cooperative 2-opt: [2] rounds, [3] evaluations retired, [4] evaluations discarded behind a winner,
 // [5..14] applied reversals by length (log2 buckets: < 2, < 4, ... , >= 512), [15] total length
-__device__ unsigned long long g_fbcyc[16];
+// [16] compacted fallbacks, [17..19] their phase cycles (count | keys | select); from the
+// fallback's start to the compacted scan's entry: ([21] - [22]) / [16] (summed clocks);
+// [32 + b] cycles and [40 + b] count of the fallbacks with U unvisited cities, b = the bucket
+// U < 16, < 32, ..., < 1024, >= 1024 (U known to the caller: n - step)
+__device__ unsigned long long g_fbcyc[64];
 __device__ __forceinline__ long long trace_clock() { return clock64(); }
-__device__ __forceinline__ void trace_fallback(long long t0, int lane) {
+__device__ __forceinline__ void trace_fallback(long long t0, int lane, int unvisited = -1) {
     if (lane == 0) {
-        atomicAdd(&g_fbcyc[0], (unsigned long long)(clock64() - t0));
+        const unsigned long long dt = (unsigned long long)(clock64() - t0);
+        atomicAdd(&g_fbcyc[0], dt);
         atomicAdd(&g_fbcyc[1], 1ull);
+        if (unvisited > 0) {
+            const int b = min(7, max(0, 31 - __clz(unvisited) - 3));
+            atomicAdd(&g_fbcyc[32 + b], dt);
+            atomicAdd(&g_fbcyc[40 + b], 1ull);
+        }
     }
+}
+__device__ __forceinline__ void trace_compact(int lane, long long t0, long long t1, long long t2, long long t3) {
+    if (lane == 0) {
+        atomicAdd(&g_fbcyc[16], 1ull);
+        atomicAdd(&g_fbcyc[17], (unsigned long long)(t1 - t0));
+        atomicAdd(&g_fbcyc[18], (unsigned long long)(t2 - t1));
+        atomicAdd(&g_fbcyc[19], (unsigned long long)(t3 - t2));
+        atomicAdd(&g_fbcyc[21], (unsigned long long)t0);   // summed entry clocks
+    }
+}
+__device__ __forceinline__ void trace_compact_entry(int lane, long long t_fb) {
+    if (lane == 0) atomicAdd(&g_fbcyc[22], (unsigned long long)t_fb);   // summed fallback start clocks
 }
 __device__ __forceinline__ void trace_ls_len(int len) {
     const int b = min(9, max(0, 31 - __clz(max(len, 1)) ));
@@ -86,7 +108,9 @@ __device__ __forceinline__ void trace_ls_len(int) {}
 __device__ __forceinline__ void trace_ls_round(int, int) {}
 __device__ __forceinline__ void trace_mark(int) {}
 __device__ __forceinline__ long long trace_clock() { return 0; }
-__device__ __forceinline__ void trace_fallback(long long, int) {}
+__device__ __forceinline__ void trace_fallback(long long, int, int = -1) {}
+__device__ __forceinline__ void trace_compact(int, long long, long long, long long, long long) {}
+__device__ __forceinline__ void trace_compact_entry(int, long long) {}
 #endif
 
 // TSPLIB EUC_2D (R12): (int)(sqrt(dx*dx + dy*dy) + 0.5) in double.
@@ -461,6 +485,8 @@ struct ConstructArgs {
     int fallback_argmax;
     int prune_fallback;          // L2-table kernel: pruned (lagged-threshold) fallback scans
     uint32_t fb_row_off;         // L2-table kernel: shared-memory offset of the fallback row buffer (0 = none)
+    int fb_lane_cap;             // lane-compacted fallback (construct.cuh fallback_compact): taken when no lane owns
+                                 // more than this many unvisited cities (0 = the trip scans only)
     int warps_per_block;
     uint32_t table_bytes_inv, table_bytes_id;  // smem-table variant: padded table sizes
     // > 0: every block asks L2 for its share of the inv_w matrix (n x ld f32, this many bytes)

@@ -128,6 +128,7 @@ struct mmas_ctx {
     bool coop_fb = false;                   // L2-table kernel: paired fallback scans (2 ants + 2 helpers per block)
     size_t cons_smem = 0;
     uint32_t fb_row_off = 0;                // L2-table kernel: fallback row buffer in smem
+    int fb_lane_cap = 0;                    // lane-compacted fallback: max unvisited cities per lane (0 = off)
     uint32_t tb_inv = 0, tb_id = 0;
 
     // memory-lean pheromone (R30): no n x n matrices; candidate trails + sparse rows
@@ -291,6 +292,7 @@ ConstructArgs construct_args(mmas_ctx* h, bool fuse_select, bool skip_finish = f
     // 5.78 -> 5.34 ms); the branch-free scan at fewer (C5: 29.4 vs 33.0 ms pruned)
     A.prune_fallback = (long long)h->m_local * h->colonies >= 16ll * h->num_sms;
     A.fb_row_off = h->fb_row_off;
+    A.fb_lane_cap = h->fb_lane_cap;
     // candidate-list colonies whose inv_w matrix takes at most half the L2: its fallback rows
     // are prefetched into L2 at launch start (4 MB at pr1002: < 1 us of HBM time); MMAS_L2_PF=0
     // turns it off (A/B)
@@ -1014,6 +1016,19 @@ int setup(mmas_ctx* h) {
     }
     if (h->cons_smem > cons_dyn_max)
         return fail(MMAS_EINVAL, "n too large for the shared-memory tabu of one block");
+    // lane-compacted fallback scans (construct.cuh fallback_compact): taken when no lane of the
+    // ant's warp owns more than cap unvisited cities.  Measured (A/B): with
+    // the register tabu and a row of more than two 256-city trips (C2) cap 12 cuts the driver
+    // window's construction 0.2227 -> 0.2077 ms (8 and 16 within 0.5 %, 24 slower); a one- or
+    // two-trip row (C1) is cheaper to scan whole, the shared-memory tabu's word counts cost
+    // more than they save (C3 +2 %), and HBM-resident rows (C5) pay a 32-byte sector per city.
+    // MMAS_FB_COMPACT=<cap> overrides (0 = off; the parity tests force every variant).
+    if (h->cl > 0 && !h->rwm && !h->lean) {
+        const bool hbm_rows = 4.0 * (double)n * h->ld > 0.75 * (double)h->l2_bytes;
+        int cap = (h->reg_tabu && n > 512 && !hbm_rows) ? 12 : 0;
+        if (const char* e = std::getenv("MMAS_FB_COMPACT")) cap = std::max(0, std::atoi(e));
+        h->fb_lane_cap = cap;
+    }
     allow_max_smem(construct_rwm_kernel<false>, h->smem_optin);
     allow_max_smem(construct_rwm_kernel<true>, h->smem_optin);
     if (h->cl > 0) {
@@ -1584,6 +1599,7 @@ int mmas_get_stats(mmas_ctx* h, mmas_stats* out) {
     out->first_ant = h->ant_lo;
     out->local_search_moves = 0;
     out->update_fused = (h->fuse_update || h->fuse_peers) ? 1 : 0;
+    out->fallback_lane_cap = h->fb_lane_cap;
     if (h->ls_moves) {
         unsigned long long mv = 0;
         CU(cudaMemcpy(&mv, h->ls_moves, sizeof(mv), cudaMemcpyDeviceToHost));
@@ -1806,8 +1822,8 @@ int mmas_load_state(mmas_ctx* h, const void* host_buf, int64_t bytes) {
 // Debug: fallback-scan cycles (sum, count) since load (a -DMMAS_TRACE build), and reset.
 extern "C" int mmas_debug_fb_cycles(unsigned long long* out) {
 #ifdef MMAS_TRACE
-    if (cudaMemcpyFromSymbol(out, mmas::g_fbcyc, 16 * sizeof(unsigned long long)) != cudaSuccess) return MMAS_ECUDA;
-    const unsigned long long z[16] = {};
+    if (cudaMemcpyFromSymbol(out, mmas::g_fbcyc, 64 * sizeof(unsigned long long)) != cudaSuccess) return MMAS_ECUDA;
+    const unsigned long long z[64] = {};
     if (cudaMemcpyToSymbol(mmas::g_fbcyc, z, sizeof(z)) != cudaSuccess) return MMAS_ECUDA;
     return MMAS_OK;
 #else

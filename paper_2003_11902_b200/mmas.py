@@ -62,7 +62,7 @@ class Stats(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int64), ("fallback_steps", ctypes.c_int64),
                 ("ant_steps", ctypes.c_int64), ("ants_local", ctypes.c_int32), ("first_ant", ctypes.c_int32),
                 ("local_search_moves", ctypes.c_int64), ("update_fused", ctypes.c_int32),
-                ("reserved_", ctypes.c_int32)]
+                ("fallback_lane_cap", ctypes.c_int32)]
 
 
 class PhaseTimes(ctypes.Structure):

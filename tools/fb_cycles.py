@@ -6,8 +6,8 @@
                                                     # first .. first+count-1 (default 5, 20),
                                                     # L2 flushed before each like bench.py
 
-Variants (environment of a child process each): MMAS_L2_PF 1 / 0 (inv_w prefetched into L2 at
-launch start or not)."""
+Variants (environment of a child process each): MMAS_FB_COMPACT caps from $CAPS (default
+0,200,1008; 0 = the trip scans only); per-U buckets of cycles, phases of the compacted path."""
 import ctypes
 import json
 import os
@@ -28,7 +28,7 @@ def child(cfg, first, count):
     col = mmas.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed, device=0)
     L = mmas.lib()
     L.mmas_debug_fb_cycles.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
-    buf = (ctypes.c_ulonglong * 16)()
+    buf = (ctypes.c_ulonglong * 64)()
     if first:
         col.iterate(first)
     col.sync()
@@ -46,7 +46,13 @@ def child(cfg, first, count):
         ms += ev[0].elapsed_time(ev[1])
     L.mmas_debug_fb_cycles(buf)
     cyc, cnt = buf[0], buf[1]
-    print(json.dumps({"fallbacks": cnt, "cycles_per_fallback": cyc / max(cnt, 1),
+    buckets = {f"U<{16 << b}" if b < 7 else "U>=1024": [int(buf[40 + b]), round(buf[32 + b] / max(buf[40 + b], 1))]
+               for b in range(8) if buf[40 + b]}
+    nc = buf[16]
+    compact = {"count": nc, "phases_count_keys_select": [round(buf[17 + k] / max(nc, 1)) for k in range(3)],
+               "start_to_entry": round((buf[21] - buf[22]) / max(nc, 1))} if nc else None
+    print(json.dumps({"fallbacks": cnt, "cycles_per_fallback": cyc / max(cnt, 1), "by_unvisited": buckets,
+                      "compact": compact,
                       "fallbacks_per_tour": cnt / (count * w.n_ants), "ms_per_iteration": ms / count}))
 
 
@@ -63,12 +69,13 @@ def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
     first = int(sys.argv[2]) if len(sys.argv) > 2 else 5
     count = int(sys.argv[3]) if len(sys.argv) > 3 else 20
-    for pf in ("1", "0"):
+    for cap in os.environ.get("CAPS", "0,200,1008").split(","):
         if True:
-            env = dict(os.environ, MMAS_L2_PF=pf)
+            env = dict(os.environ, MMAS_FB_COMPACT=cap)
+            pf = cap
             out = subprocess.run([sys.executable, __file__, "child", cfg, str(first), str(count)], env=env,
                                  capture_output=True, text=True)
-            print(f"{cfg} it {first}-{first + count - 1} l2_prefetch={pf}:",
+            print(f"{cfg} it {first}-{first + count - 1} MMAS_FB_COMPACT={pf}:",
                   out.stdout.strip() or out.stderr[-400:])
 
 
