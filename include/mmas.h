@@ -115,10 +115,9 @@ typedef struct mmas_stats {
     int64_t local_search_moves; /* improving 2-opt moves applied (row a8), this shard */
     int32_t update_fused;     /* 1: mmas_iterate runs construction + selection + update as ONE
                                  launch (see mmas_config.separate_update) */
-    int32_t fallback_lane_cap; /* lane-compacted fallback scans (row a3): a fallback where no lane
-                                  owns more than this many unvisited cities draws keys for the
-                                  unvisited cities only (0 = off; DESIGN.md Sec. 5 "Lane-compacted
-                                  fallback"); env MMAS_FB_COMPACT */
+    int32_t fallback_lane_cap; /* lane-compacted fallback scans (row a3): a fallback with at most
+                                  this many unvisited cities draws keys for the unvisited cities
+                                  only (0 = off, a3); env MMAS_FB_COMPACT */
 } mmas_stats;
 
 /* Last error message of this thread ("" if none). */

@@ -515,21 +515,12 @@ __device__ __forceinline__ LaneCitiesSmem lane_cities(const SmemTabu& t, int n, 
 }
 
 template <class Tabu>
-__device__ __noinline__ uint32_t fallback_compact(const float* __restrict__ row, const Tabu tabu, int n, int cap,
+__device__ __noinline__ uint32_t fallback_compact(const float* __restrict__ row, const Tabu tabu, int n,
                                                   uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
                                                   int lane) {
     const long long t0 = trace_clock();
-#ifdef MMAS_TRACE
-    // timing experiments only (tools/fb_cycles.py): cap bit 30 = no row loads, bit 29 = no Philox
-    const bool x_noload = (cap >> 30) & 1, x_nophilox = (cap >> 29) & 1;
-    cap &= (1 << 29) - 1;
-#else
-    constexpr bool x_noload = false, x_nophilox = false;
-#endif
     auto it = lane_cities(tabu, n, lane);
-    const int most = __reduce_max_sync(kFull, (uint32_t)it.count());
-    if (most > cap) return kNone;   // warp-uniform
-    const long long t1 = trace_clock();
+    const uint32_t cnt = (uint32_t)it.count();
     uint32_t bm = kNone, bc = kNone;
     // K cities per lane at a time, branch-free (a lane with fewer carries kNone), so the K
     // Philox / log chains interleave
@@ -539,8 +530,7 @@ __device__ __noinline__ uint32_t fallback_compact(const float* __restrict__ row,
 #pragma unroll
         for (int j = 0; j < k; ++j) {
             const uint32_t cc = c[j] == kNone ? 0u : c[j];
-            const uint4 x = x_nophilox ? make_uint4(cc * 0x9E3779B9u, cc, cc ^ step, cc + ant)
-                                       : philox4x32_10(ctr_city(cc >> 2, step, ant, iter), key);
+            const uint4 x = philox4x32_10(ctr_city(cc >> 2, step, ant, iter), key);
             const uint32_t q = cc & 3u;
             // selects in PTX (selp): the compiler would otherwise branch around the unused words
             // and the idle lanes' logs, which serialises the chains
@@ -556,15 +546,25 @@ __device__ __noinline__ uint32_t fallback_compact(const float* __restrict__ row,
             bc = selp_u32(c[j], bc, take);
         }
     };
-    for (int r = 0; r < most; r += 8) {
-        uint32_t c[8];
-        float iv[8];
+    // the first round's cities and row loads go out before the warp learns how many rounds
+    // it needs (the reduction's latency hides behind the loads)
+    uint32_t c[8];
+    float iv[8];
+    auto fetch = [&]() {
 #pragma unroll
         for (int j = 0; j < 8; ++j) c[j] = it.next();
 #pragma unroll
-        for (int j = 0; j < 8; ++j) iv[j] = c[j] != kNone ? (x_noload ? 1.5f : __ldg(row + c[j])) : 0.f;
+        for (int j = 0; j < 8; ++j) iv[j] = c[j] != kNone ? __ldg(row + c[j]) : 0.f;
+    };
+    fetch();
+    const int most = (int)__reduce_max_sync(kFull, cnt);
+    const long long t1 = trace_clock();
+    for (int r = 0;;) {
         if (r + 4 < most) eval(std::integral_constant<int, 8>{}, c, iv);   // warp-uniform
         else eval(std::integral_constant<int, 4>{}, c, iv);
+        r += 8;
+        if (r >= most) break;
+        fetch();
     }
     const long long t2 = trace_clock();
     const uint32_t res = warp_select(bm, bc);
@@ -1268,15 +1268,20 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
             return best >= 0x80000000u;
         };
         // GENERIC step (runtime j): guards, and the R9 fallback (row a3) inlined ONCE
-        auto generic_step = [&](int j, int s) {
-            float Lv[kSlots];
+        // known_fb: the speculative / fast attempt of this step already found every candidate
+        // visited (from the same state), so the evaluation is not repeated
+        auto generic_step = [&](int j, int s, bool known_fb) {
+            uint32_t best = 0x80000000u, nxt = 0u;
+            if (!known_fb) {
+                float Lv[kSlots];
 #pragma unroll
-            for (int q = 0; q < kSlots; ++q)
-                Lv[q] = j == 0 ? L[q][0] : j == 1 ? L[q][1] : j == 2 ? L[q][2] : L[q][3];
-            uint32_t bm, bc;
-            evaluate(Lv, [] {}, [] {}, bm, bc);
-            const uint32_t best = __reduce_min_sync(kFull, bm);
-            uint32_t nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
+                for (int q = 0; q < kSlots; ++q)
+                    Lv[q] = j == 0 ? L[q][0] : j == 1 ? L[q][1] : j == 2 ? L[q][2] : L[q][3];
+                uint32_t bm, bc;
+                evaluate(Lv, [] {}, [] {}, bm, bc);
+                best = __reduce_min_sync(kFull, bm);
+                nxt = __reduce_min_sync(kFull, bm == best ? bc : kNone);
+            }
             if (best >= 0x80000000u) {   // every candidate visited: R9 fallback
                 ++fb;
                 const long long t_fb = trace_clock();
@@ -1321,15 +1326,13 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
                                s);
                     return;
                 }
-                if (A.fb_lane_cap && !A.fallback_argmax) {
-                    // late in the tour: each lane evaluates only its own unvisited cities
-                    const uint32_t c = fallback_compact(row, tabu, n, A.fb_lane_cap, (uint32_t)s, ant, iter, c_key, lane);
-                    if (c != kNone) {
-                        trace_fallback(t_fb, lane, n - s);
-                        trace_compact_entry(lane, t_fb);
-                        commit(c, s);
-                        return;
-                    }
+                if (n - s <= A.fb_lane_cap && !A.fallback_argmax) {
+                    // late in the tour (n - s unvisited cities): each lane evaluates only its own
+                    const uint32_t c = fallback_compact(row, tabu, n, (uint32_t)s, ant, iter, c_key, lane);
+                    trace_fallback(t_fb, lane, n - s);
+                    trace_compact_entry(lane, t_fb);
+                    commit(c, s);
+                    return;
                 }
                 tabu.prepare(lane);
                 if (A.fallback_argmax)
@@ -1459,7 +1462,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
             for (int j = j0; j < 4; ++j) {
                 if (pipeline && !sliced_all && !(j == j0 && sliced_j0)) slice_rt(j);
                 const int s = 4 * g + j;
-                if (s > 0 && s < n) generic_step(j, s);
+                if (s > 0 && s < n) generic_step(j, s, j == j0 && (sliced_all || sliced_j0));
             }
             if (pipeline) rotate();
             ++g;

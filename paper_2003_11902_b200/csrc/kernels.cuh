@@ -485,8 +485,8 @@ struct ConstructArgs {
     int fallback_argmax;
     int prune_fallback;          // L2-table kernel: pruned (lagged-threshold) fallback scans
     uint32_t fb_row_off;         // L2-table kernel: shared-memory offset of the fallback row buffer (0 = none)
-    int fb_lane_cap;             // lane-compacted fallback (construct.cuh fallback_compact): taken when no lane owns
-                                 // more than this many unvisited cities (0 = the trip scans only)
+    int fb_lane_cap;             // lane-compacted fallback (construct.cuh fallback_compact): taken at steps with at
+                                 // most this many unvisited cities (0 = the trip scans only)
     int warps_per_block;
     uint32_t table_bytes_inv, table_bytes_id;  // smem-table variant: padded table sizes
     // > 0: every block asks L2 for its share of the inv_w matrix (n x ld f32, this many bytes)

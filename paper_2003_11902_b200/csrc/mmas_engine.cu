@@ -1016,16 +1016,15 @@ int setup(mmas_ctx* h) {
     }
     if (h->cons_smem > cons_dyn_max)
         return fail(MMAS_EINVAL, "n too large for the shared-memory tabu of one block");
-    // lane-compacted fallback scans (construct.cuh fallback_compact): taken when no lane of the
-    // ant's warp owns more than cap unvisited cities.  Measured (A/B): with
-    // the register tabu and a row of more than two 256-city trips (C2) cap 12 cuts the driver
-    // window's construction 0.2227 -> 0.2077 ms (8 and 16 within 0.5 %, 24 slower); a one- or
+    // lane-compacted fallback scans (construct.cuh fallback_compact): taken at steps with at
+    // most cap unvisited cities.  Measured (A/B): with the register tabu and
+    // a row of more than two 256-city trips (C2) the compacted scan wins up to ~cap; a one- or
     // two-trip row (C1) is cheaper to scan whole, the shared-memory tabu's word counts cost
     // more than they save (C3 +2 %), and HBM-resident rows (C5) pay a 32-byte sector per city.
     // MMAS_FB_COMPACT=<cap> overrides (0 = off; the parity tests force every variant).
     if (h->cl > 0 && !h->rwm && !h->lean) {
         const bool hbm_rows = 4.0 * (double)n * h->ld > 0.75 * (double)h->l2_bytes;
-        int cap = (h->reg_tabu && n > 512 && !hbm_rows) ? 12 : 0;
+        int cap = (h->reg_tabu && n > 512 && !hbm_rows) ? 224 : 0;
         if (const char* e = std::getenv("MMAS_FB_COMPACT")) cap = std::max(0, std::atoi(e));
         h->fb_lane_cap = cap;
     }

@@ -3,7 +3,7 @@
 When every candidate of the current city is visited, Alg. 3 draws a key for
 every unvisited city and takes the largest.  Late in a tour each lane of the ant's warp
 evaluates only the unvisited cities of its own tabu bits; the trip scans over the whole row
-remain for fallbacks where some lane owns more than `cap` unvisited cities.  Both must give
+remain for fallbacks with more than `cap` unvisited cities.  Both must give
 the oracle's choice bit for bit on every kernel variant: MMAS_FB_COMPACT forces the cap
 (0: trip scans only; >= n: the compacted scan for every fallback; small: a mix within one
 tour)."""
@@ -23,7 +23,7 @@ KERNELS = [
     ("l2-table", "fl3795", 1500, 40, 32, 2, {}),                # table beyond shared memory
     ("l2-table-staged-coop", "fl3795", 1300, 40, 4, 2, {"MMAS_FB_ROW": "1"}),   # C5's paired path
 ]
-CAPS = [("trip-only", lambda n: 0), ("compact-always", lambda n: n), ("mixed", lambda n: 2)]
+CAPS = [("trip-only", lambda n: 0), ("compact-always", lambda n: n), ("mixed", lambda n: n // 3)]
 
 
 @pytest.mark.parametrize("cap_name,cap", CAPS, ids=[c[0] for c in CAPS])
@@ -41,12 +41,12 @@ def test_compacted_fallback_bit_exact(label, recipe, n, m, cl, iters, env, cap_n
 
 def test_compacted_fallback_pruned_l2_kernel(monkeypatch):
     """The 16-warps-per-SM L2-table kernel (pruned trip scans otherwise): 2400 ants, cl = 4,
-    most steps fall back; the compacted scan wherever no lane owns more than 12 cities."""
-    monkeypatch.setenv("MMAS_FB_COMPACT", "12")
+    most steps fall back; the compacted scan at the steps with at most 400 unvisited cities."""
+    monkeypatch.setenv("MMAS_FB_COMPACT", "400")
     c = make_coords("fl3795", 1300, 21)
     g, o = lockstep(c, 2400, 4, 1, seed=13)
     assert g.stats()["fallback_steps"] > 100000
-    assert g.stats()["fallback_lane_cap"] == 12
+    assert g.stats()["fallback_lane_cap"] == 400
 
 
 def test_compacted_fallback_colonies(monkeypatch):
@@ -54,7 +54,7 @@ def test_compacted_fallback_colonies(monkeypatch):
     import oracle
     from paper_2003_11902_b200 import mmas
     from test_parity_gpu import compare_iteration
-    monkeypatch.setenv("MMAS_FB_COMPACT", "5")
+    monkeypatch.setenv("MMAS_FB_COMPACT", "40")
     c = make_coords("uniform", 130, 77)
     g = mmas.Colony(c, 40, 6, seed=5, colonies=3)
     os_ = [oracle.Colony(c, 40, 6, seed=5 + k) for k in range(3)]
@@ -64,17 +64,17 @@ def test_compacted_fallback_colonies(monkeypatch):
             o.iterate(1)
             g.select_colony(k)
             compare_iteration(g, o, f"{it} (colony {k})")
-    assert g.stats()["fallback_lane_cap"] == 5
+    assert g.stats()["fallback_lane_cap"] == 40
 
 
 def test_default_cap_is_set_for_c2():
     """bench.py's C2 launch (pr1002-shaped, cl 32): the compacted scan is on with the default
-    cap (12 cities per lane: register tabu, L2-resident rows); off for C1 (one-trip rows)."""
+    cap (224 unvisited cities: register tabu, L2-resident rows); off for C1 (one-trip rows)."""
     from paper_2003_11902_b200 import mmas
     from paper_2003_11902_b200.instances import CONFIGS
     w = CONFIGS["C2"]
     g = mmas.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed)
-    assert g.stats()["fallback_lane_cap"] == 12
+    assert g.stats()["fallback_lane_cap"] == 224
     w = CONFIGS["C1"]
     g = mmas.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed)
     assert g.stats()["fallback_lane_cap"] == 0
