@@ -427,12 +427,11 @@ __device__ __noinline__ uint32_t lean_fallback_ool(const LeanArgs Ln, const doub
 // each lane takes the unvisited cities of its own tabu bits -- no transpose, list or prefix
 // sum: with the register tabu lane l owns cities l, l + 32, l + 64, ... (the transposed word
 // wt the candidate test keeps anyway), with the shared-memory tabu the words l, l + 32, ... --
-// and evaluates them eight (or four) at a time: the scattered inv_w loads issued first, then
+// and evaluates them eight (four, two) at a time: the scattered inv_w loads issued first, then
 // independent Philox / log chains (per city the Philox of its group, word c & 3: the uniform
 // the dense scan draws, R13).  The result is the same lexicographic (magnitude, city)
-// minimum, ties to the lowest id, so the argmax is the dense one bit for bit.  Returns kNone
-// (nothing evaluated) when some lane owns more than `cap` unvisited cities; the caller then
-// runs the trip scan.  Out of line: the step loops' register allocation stays as it is.
+// minimum, ties to the lowest id, so the argmax is the dense one bit for bit.  The caller
+// takes it at steps with at most `fb_lane_cap` unvisited cities, the trip scan otherwise.
 // p ? a : b as one PTX selp (opaque to the compiler's select-to-branch conversion)
 __device__ __forceinline__ uint32_t selp_u32(uint32_t a, uint32_t b, bool p) {
     uint32_t r;
@@ -514,8 +513,9 @@ __device__ __forceinline__ LaneCitiesSmem lane_cities(const SmemTabu& t, int n, 
     return LaneCitiesSmem(t, n, lane);
 }
 
+// (inlined: out of line measured 1 % slower on C2, the call's ~200-cycle entry)
 template <class Tabu>
-__device__ __noinline__ uint32_t fallback_compact(const float* __restrict__ row, const Tabu tabu, int n,
+__device__ __forceinline__ uint32_t fallback_compact(const float* __restrict__ row, const Tabu tabu, int n,
                                                   uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
                                                   int lane) {
     const long long t0 = trace_clock();
@@ -560,8 +560,10 @@ __device__ __noinline__ uint32_t fallback_compact(const float* __restrict__ row,
     const int most = (int)__reduce_max_sync(kFull, cnt);
     const long long t1 = trace_clock();
     for (int r = 0;;) {
-        if (r + 4 < most) eval(std::integral_constant<int, 8>{}, c, iv);   // warp-uniform
-        else eval(std::integral_constant<int, 4>{}, c, iv);
+        // (warp-uniform) 8, 4 or 2 chains: the short tail rounds issue only what they use
+        if (r + 4 < most) eval(std::integral_constant<int, 8>{}, c, iv);
+        else if (r + 2 < most) eval(std::integral_constant<int, 4>{}, c, iv);
+        else eval(std::integral_constant<int, 2>{}, c, iv);
         r += 8;
         if (r >= most) break;
         fetch();
