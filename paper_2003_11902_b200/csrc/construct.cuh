@@ -1398,6 +1398,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
         // run the GENERIC path, which appears once in the loop body.
         int g = 0;
         while (g < n_groups) {
+            const long long t_g0 = trace_clock();
             const bool pipeline = g + 1 < n_groups;
             int j0 = 0;
             bool sliced_j0 = false;
@@ -1423,6 +1424,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
                     if (__builtin_expect(!(h0 | h1 | h2 | h3), 1)) {
                         rotate();
                         ++g;
+                        trace_group(t_g0, lane, false);
                         continue;
                     }
                     tabu.w = w0;
@@ -1468,6 +1470,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
             }
             if (pipeline) rotate();
             ++g;
+            if (sliced_all || sliced_j0) trace_group(t_g0, lane, true);
         }
         flush_route(route, n, lane, stage);
         __syncwarp();

@@ -90,6 +90,14 @@ __device__ __forceinline__ void trace_compact(int lane, long long t0, long long 
         atomicAdd(&g_fbcyc[21], (unsigned long long)t0);   // summed entry clocks
     }
 }
+// [48], [49]: cycles and count of the speculative groups that hit a fallback (the whole group:
+// speculation, rollback, fallback scan, generic redo); [50], [51]: the same for clean groups
+__device__ __forceinline__ void trace_group(long long t0, int lane, bool hit) {
+    if (lane == 0) {
+        atomicAdd(&g_fbcyc[hit ? 48 : 50], (unsigned long long)(clock64() - t0));
+        atomicAdd(&g_fbcyc[hit ? 49 : 51], 1ull);
+    }
+}
 __device__ __forceinline__ void trace_compact_entry(int lane, long long t_fb) {
     if (lane == 0) atomicAdd(&g_fbcyc[22], (unsigned long long)t_fb);   // summed fallback start clocks
 }
@@ -111,6 +119,7 @@ __device__ __forceinline__ long long trace_clock() { return 0; }
 __device__ __forceinline__ void trace_fallback(long long, int, int = -1) {}
 __device__ __forceinline__ void trace_compact(int, long long, long long, long long, long long) {}
 __device__ __forceinline__ void trace_compact_entry(int, long long) {}
+__device__ __forceinline__ void trace_group(long long, int, bool) {}
 #endif
 
 // TSPLIB EUC_2D (R12): (int)(sqrt(dx*dx + dy*dy) + 0.5) in double.
@@ -837,30 +846,55 @@ __global__ void heur_kernel(const double2* __restrict__ xy, int n, int ld, int b
 // j = tid, tid + 1024, ... as a (d, j) key, the block reduces the key to its minimum (ties
 // -> lowest id) and thread 0 moves there.  Visited bits in shared memory (n <= 65535).
 constexpr int kNnThreads = 1024;   // upper bound; launched with nn_threads(n)
-// Nearest-neighbour tour from city 0, ties -> lowest id (R3; Alg. 1): one block,
-// each step a block-wide argmin of (d, id) over the unvisited cities by two 32-bit warp
-// reductions (redux.sync) per level.  Setup only, but inside bench.py's end-to-end timing.
+// Nearest-neighbour tour from city 0, ties -> lowest id (R3; Alg. 1).  Setup
+// only, but inside bench.py's end-to-end timing (it was ~1 ms of C2's mmas_create and
+// ~170 ms of C5's as a block-wide scan per step).
+// Candidate fast path (cl > 0): a candidate row holds the row's cl smallest keys (d, id) in
+// ascending order (R10, cand_lists_kernel), and every city off the row has a larger key, so
+// when the row of the current city has an unvisited entry the FIRST such entry is the exact
+// argmin over all unvisited cities.  Warp 0 alone runs those steps (one row read, a tabu test
+// per lane, a ballot); only when the whole row is visited does it wake the block (named
+// barrier 1) for the full scan: each thread its cities j = tid, tid + T, ... (ascending, so
+// ties keep the lower id), 32-bit warp reductions of (d, id) per warp, named barrier 2, warp 0
+// combines.  Without candidate lists every step is a full scan.  The tour length is summed
+// over the recorded route at the end (exact int64; the order does not matter).
+// Dynamic shared memory: route (n u16, rounded to 16 B), then the candidate table when
+// `stage_cand` (n x cl_ld u16), else the rows are read from global memory.
 __host__ __device__ constexpr int nn_threads(int n) { return n <= 2048 ? 256 : n <= 8192 ? 512 : 1024; }
+__device__ __forceinline__ void nn_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 __global__ void __launch_bounds__(kNnThreads) nn_tour_kernel(const double2* __restrict__ xy,
                                                              const short2* __restrict__ xys, int n,
-                                                             long long* len_out) {
+                                                             const uint16_t* __restrict__ cand, int cl, int cl_ld,
+                                                             int stage_cand, long long* len_out) {
+    extern __shared__ __align__(16) uint16_t nn_smem[];
     __shared__ uint32_t vis[2048];
     __shared__ uint32_t s_d[kNnThreads / 32], s_j[kNnThreads / 32];
-    __shared__ int s_cur;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    for (int w = tid; w < 2048; w += blockDim.x) vis[w] = 0u;
+    __shared__ int s_cur, s_done;
+    __shared__ unsigned long long s_len;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5, T = blockDim.x;
+    uint16_t* route = nn_smem;
+    uint16_t* s_cand = nn_smem + ((n + 7) & ~7);
+    const uint16_t* rows = stage_cand ? s_cand : cand;
+    for (int w = tid; w < 2048; w += T) vis[w] = 0u;
+    if (stage_cand)
+        for (int i = tid; i < n * cl_ld; i += T) s_cand[i] = cand[i];
     if (tid == 0) {
         vis[0] = 1u;
         s_cur = 0;
+        s_done = 0;
+        s_len = 0ull;
+        route[0] = 0;
     }
     __syncthreads();
-    long long len = 0;
-    for (int s = 1; s < n; ++s) {
+    // one full-scan step from s_cur (every thread; returns the argmin to warp 0)
+    auto full_scan = [&]() -> uint32_t {
         const int cur = s_cur;
         const double2 pc = xy[cur];
         const short2 pcs = xys ? xys[cur] : make_short2(0, 0);
         uint32_t bd = kNone, bj = kNone;
-        for (int j = tid; j < n; j += blockDim.x) {   // ascending j: ties keep the lower id
+        for (int j = tid; j < n; j += T) {   // ascending j: ties keep the lower id
             if ((vis[j >> 5] >> (j & 31)) & 1u) continue;
             // integral coordinates: the exact 32-bit path (euc2d_int == R12), else fp64
             const uint32_t d = (uint32_t)(xys ? euc2d_int(pcs, xys[j]) : euc2d(pc, xy[j]));
@@ -875,20 +909,56 @@ __global__ void __launch_bounds__(kNnThreads) nn_tour_kernel(const double2* __re
             s_d[warp] = wd;
             s_j[warp] = wj;
         }
-        __syncthreads();
-        if (warp == 0) {
-            const uint32_t d = lane < nw ? s_d[lane] : kNone, jj = lane < nw ? s_j[lane] : kNone;
-            wd = __reduce_min_sync(kFull, d);
-            wj = __reduce_min_sync(kFull, d == wd ? jj : kNone);
-            if (lane == 0) {
-                len += (long long)wd;
-                vis[wj >> 5] |= 1u << (wj & 31);
-                s_cur = (int)wj;
+        nn_bar(2, T);
+        if (warp != 0) return kNone;
+        const uint32_t d = lane < nw ? s_d[lane] : kNone, jj = lane < nw ? s_j[lane] : kNone;
+        wd = __reduce_min_sync(kFull, d);
+        return __reduce_min_sync(kFull, d == wd ? jj : kNone);
+    };
+    if (warp == 0) {
+        int cur = 0;
+        for (int s = 1; s < n; ++s) {
+            uint32_t nxt = kNone;
+            for (int k0 = 0; k0 < cl && nxt == kNone; k0 += 32) {   // 32 row entries at a time
+                const int k = k0 + lane;
+                const uint32_t c = k < cl ? (uint32_t)rows[(size_t)cur * cl_ld + k] : 0u;
+                const bool fresh = k < cl && !((vis[c >> 5] >> (c & 31)) & 1u);
+                const uint32_t m = __ballot_sync(kFull, fresh);
+                if (m) nxt = __shfl_sync(kFull, c, __ffs(m) - 1);
             }
+            if (nxt == kNone) {   // the whole row is visited (or no lists): the block scans
+                if (lane == 0) s_cur = cur;
+                nn_bar(1, T);
+                nxt = full_scan();
+            }
+            if (lane == 0) {
+                vis[nxt >> 5] |= 1u << (nxt & 31);
+                route[s] = (uint16_t)nxt;
+            }
+            __syncwarp();
+            cur = (int)nxt;
         }
-        __syncthreads();
+        if (lane == 0) s_done = 1;
+        nn_bar(1, T);   // release the helpers
+    } else {
+        while (true) {
+            nn_bar(1, T);
+            if (s_done) break;
+            full_scan();
+        }
     }
-    if (tid == 0) *len_out = len + euc2d(xy[s_cur], xy[0]);
+    __syncthreads();
+    // length over the recorded route (R12 distances, exact in int64)
+    long long len = 0;
+    for (int s = tid; s < n; s += T) {
+        const int a = route[s], b = route[s + 1 < n ? s + 1 : 0];
+        len += xys ? (long long)euc2d_int(xys[a], xys[b]) : (long long)euc2d(xy[a], xy[b]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) len += __shfl_down_sync(kFull, len, o);
+    if (lane == 0) atomicAdd(&s_len, (unsigned long long)len);
+    __syncthreads();
+    if (tid == 0) *len_out = (long long)s_len;
 }
 
 // tau = tau_max (Alg. 1) and inv_w = 1/choice_info.
@@ -928,6 +998,21 @@ __global__ void __launch_bounds__(256) cand_lists_kernel(const double2* __restri
             first = false;
             __syncthreads();   // s_red reused next round
         }
+    }
+}
+
+// 2-opt neighbour distances d(i, nn[i][q]) (R12) and, for integral coordinates, the packed
+// entries nn | d << 16 the 2-opt kernels read (row a8 setup; was a host pass)
+__global__ void ls_dist_kernel(const double2* __restrict__ xy, int n, int k, const uint16_t* __restrict__ nn,
+                               int32_t* __restrict__ nnd, uint32_t* __restrict__ nnp) {
+    const long long total = (long long)n * k;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / k);
+        const uint32_t j = nn[e];
+        const int32_t d = euc2d(xy[i], xy[j]);
+        nnd[e] = d;
+        if (nnp) nnp[e] = j | ((uint32_t)d << 16);
     }
 }
 

@@ -150,7 +150,7 @@ struct mmas_ctx {
     int64_t launches = 0;
 
     // row a8: 2-opt local search (local_search != 0)
-    int ls_k = 0, ls_nwords = 0, ls_coop_smem_max = 0;
+    int ls_k = 0, ls_nwords = 0, ls_coop_smem_max = 0, ls_group_smem_max = 0;
     uint16_t* ls_nn = nullptr;         // n x ls_k neighbour lists
     int32_t* ls_nnd = nullptr;         // n x ls_k: d(a, nn[a][k])
     short2* ls_xys = nullptr;          // integral coordinates (ls_int_xy), else null
@@ -493,7 +493,18 @@ int launch_two_opt(mmas_ctx* h, bool fuse_select) {
     T.moves = h->ls_moves;
     // route + pos (u16) and the queued bits in shared memory
     const size_t per_ant = (size_t)4 * h->ldr + (size_t)4 * h->ls_nwords;
-    if (per_ant <= (size_t)h->ls_coop_smem_max) {
+    // grouped kernel (two_opt.cuh two_opt_group_kernel): coordinates in shared memory, two ants
+    // per block.  Opt-in (MMAS_LS_GROUP=1): on C5 its rounds are ~20 % shorter, but two ants per
+    // SM instead of three make the local search slower overall (125 -> 151 ms)
+    const size_t group_smem = (((size_t)h->n * 4 + 15) & ~(size_t)15) + kLsGroupsMax * per_ant;
+    const char* ge = std::getenv("MMAS_LS_GROUP");
+    const bool group = h->ls_int_xy && group_smem <= (size_t)h->ls_group_smem_max && ge && ge[0] == '1';
+    if (group) {
+        T.warps_per_block = kLsGroupsMax * kLsWarps;
+        const int grid = std::max(1, (h->m_local + kLsGroupsMax - 1) / kLsGroupsMax);
+        launch_pdl(two_opt_group_kernel<kLsGroupsMax>, dim3(grid, h->colonies), dim3(kLsGroupsMax * kLsWarps * 32),
+                   group_smem, h->stream, T, construct_args(h, fuse_select));
+    } else if (per_ant <= (size_t)h->ls_coop_smem_max) {
         // one block of kLsWarps warps per ant (speculative parallel FIFO, two_opt_coop_kernel)
         T.warps_per_block = kLsWarps;
         if (h->ls_int_xy)
@@ -797,11 +808,16 @@ int setup(mmas_ctx* h) {
         h->ls_k = std::min(32, n - 1);
         h->ls_nwords = (n + 31) / 32;
         std::vector<uint16_t> nnl;
-        candidate_lists(c.coords, n, h->ls_k, nnl);
+        // the lists and their distances on the device (cand_lists_kernel, ls_dist_kernel) where
+        // a row's distances fit in shared memory (C5: was ~80-190 ms on the host), else the host
+        const bool dev_ls = dev_cand;
+        if (!dev_ls) candidate_lists(c.coords, n, h->ls_k, nnl);
+        const size_t nent = (size_t)n * h->ls_k;
         // neighbour distances (exact R12 values; the 2-opt evaluation reads d(a, c) from here)
-        std::vector<int32_t> nnd(nnl.size());
-        for (int i = 0; i < n; ++i)
-            for (int k = 0; k < h->ls_k; ++k) nnd[(size_t)i * h->ls_k + k] = host_dist(c.coords, i, nnl[(size_t)i * h->ls_k + k]);
+        std::vector<int32_t> nnd(dev_ls ? 0 : nent);
+        if (!dev_ls)
+            for (int i = 0; i < n; ++i)
+                for (int k = 0; k < h->ls_k; ++k) nnd[(size_t)i * h->ls_k + k] = host_dist(c.coords, i, nnl[(size_t)i * h->ls_k + k]);
         // integral coordinates with |x|, |y| <= 16383: the 2-opt kernels compute distances in
         // 32-bit integer arithmetic (two_opt.cuh euc2d_int; identical results)
         h->ls_int_xy = true;
@@ -814,22 +830,40 @@ int setup(mmas_ctx* h) {
                 xys[(size_t)i] = make_short2((short)x, (short)y);
         }
         h->cs.inq = (int)(ma * h->ls_nwords);
-        if ((st = dalloc(&h->ls_nn, nnl.size())) || (st = dalloc(&h->ls_nnd, nnd.size())) ||
+        if ((st = dalloc(&h->ls_nn, nent)) || (st = dalloc(&h->ls_nnd, nent)) ||
             (st = dalloc(&h->ls_pos, ma * h->ldr * K)) ||
             (st = dalloc(&h->ls_queue, ma * h->ldr * K)) || (st = dalloc(&h->ls_inq, ma * h->ls_nwords * K)) ||
             (st = dalloc(&h->ls_moves, 1)))
             return st;
         if (h->ls_int_xy) {
-            std::vector<uint32_t> nnp(nnl.size());
-            for (size_t e = 0; e < nnl.size(); ++e) nnp[e] = (uint32_t)nnl[e] | ((uint32_t)nnd[e] << 16);
-            if ((st = dalloc(&h->ls_xys, (size_t)n)) || (st = dalloc(&h->ls_nnp, nnp.size()))) return st;
+            if ((st = dalloc(&h->ls_xys, (size_t)n)) || (st = dalloc(&h->ls_nnp, nent))) return st;
             CU(cudaMemcpyAsync(h->ls_xys, xys.data(), sizeof(short2) * n, cudaMemcpyHostToDevice, h->stream));
-            CU(cudaMemcpyAsync(h->ls_nnp, nnp.data(), sizeof(uint32_t) * nnp.size(), cudaMemcpyHostToDevice,
-                               h->stream));
-            CU(cudaStreamSynchronize(h->stream));   // the host vectors go out of scope
         }
-        CU(cudaMemcpyAsync(h->ls_nnd, nnd.data(), sizeof(int32_t) * nnd.size(), cudaMemcpyHostToDevice, h->stream));
-        CU(cudaMemcpyAsync(h->ls_nn, nnl.data(), sizeof(uint16_t) * nnl.size(), cudaMemcpyHostToDevice, h->stream));
+        if (dev_ls) {
+            if (h->cl == h->ls_k && h->cl_ld == h->cl) {   // the same lists (R10): copy them
+                CU(cudaMemcpyAsync(h->ls_nn, h->cand_id, sizeof(uint16_t) * nent, cudaMemcpyDeviceToDevice, h->stream));
+            } else {
+                cudaFuncSetAttribute(cand_lists_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin - 2048);
+                cand_lists_kernel<<<std::min(n, 8 * h->num_sms), 256, (size_t)n * 4, h->stream>>>(h->xy, n, h->ls_k,
+                                                                                                  h->ls_nn, h->ls_k);
+                h->launches++;
+            }
+            ls_dist_kernel<<<4 * h->num_sms, 256, 0, h->stream>>>(h->xy, n, h->ls_k, h->ls_nn, h->ls_nnd,
+                                                                  h->ls_int_xy ? h->ls_nnp : nullptr);
+            h->launches++;
+            CU(cudaGetLastError());
+            CU(cudaStreamSynchronize(h->stream));   // xys goes out of scope
+        } else {
+            if (h->ls_int_xy) {
+                std::vector<uint32_t> nnp(nent);
+                for (size_t e = 0; e < nent; ++e) nnp[e] = (uint32_t)nnl[e] | ((uint32_t)nnd[e] << 16);
+                CU(cudaMemcpyAsync(h->ls_nnp, nnp.data(), sizeof(uint32_t) * nnp.size(), cudaMemcpyHostToDevice,
+                                   h->stream));
+                CU(cudaStreamSynchronize(h->stream));   // the host vectors go out of scope
+            }
+            CU(cudaMemcpyAsync(h->ls_nnd, nnd.data(), sizeof(int32_t) * nnd.size(), cudaMemcpyHostToDevice, h->stream));
+            CU(cudaMemcpyAsync(h->ls_nn, nnl.data(), sizeof(uint16_t) * nnl.size(), cudaMemcpyHostToDevice, h->stream));
+        }
         CU(cudaMemsetAsync(h->ls_moves, 0, sizeof(unsigned long long), h->stream));
         CU(cudaStreamSynchronize(h->stream));
     }
@@ -860,7 +894,18 @@ int setup(mmas_ctx* h) {
             }
         }
         clk.mark("NN tour inputs", h->stream);
-        nn_tour_kernel<<<1, nn_threads(n), 0, h->stream>>>(h->xy, d_xys, n, d_len);
+        {
+            // the candidate rows (padded to cl_ld slots with the row's own city, always visited)
+            // staged into shared memory next to the route when they fit
+            const size_t route_b = (size_t)((n + 7) & ~7) * 2;
+            const size_t cand_b = (size_t)n * h->cl_ld * 2;
+            const size_t budget = (size_t)h->smem_optin - 16384;   // static: tabu words + partials
+            const int stage = h->cl > 0 && route_b + cand_b <= budget;
+            const size_t dyn = route_b + (stage ? cand_b : 0);
+            cudaFuncSetAttribute(nn_tour_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            nn_tour_kernel<<<1, nn_threads(n), dyn, h->stream>>>(h->xy, d_xys, n, h->cl > 0 ? h->cand_id : nullptr,
+                                                                 h->cl, h->cl_ld, stage, d_len);
+        }
         if (d_xys) CU(h->pooled ? cudaFreeAsync(d_xys, h->stream) : cudaFree(d_xys));
         h->launches++;
         CU(cudaGetLastError());
@@ -1048,6 +1093,11 @@ int setup(mmas_ctx* h) {
                              h->ls_coop_smem_max);
         cudaFuncSetAttribute(two_opt_coop_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              h->ls_coop_smem_max);
+        cudaFuncAttributes fg{};
+        cudaFuncGetAttributes(&fg, two_opt_group_kernel<kLsGroupsMax>);
+        h->ls_group_smem_max = h->smem_optin - (int)fg.sharedSizeBytes;
+        cudaFuncSetAttribute(two_opt_group_kernel<kLsGroupsMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             h->ls_group_smem_max);
         // experiment (MMAS_LS_CARVEOUT = percent of the unified L1/shared memory given to shared
         // memory): fewer resident 2-opt blocks per SM, but an L1 large enough for the coordinates
         if (const char* co = std::getenv("MMAS_LS_CARVEOUT")) {

@@ -55,6 +55,18 @@ struct Pts<true> {
     __device__ __forceinline__ static int64_t dist(P a, P b) { return euc2d_int(a, b); }
 };
 
+// integral coordinates staged in shared memory (two_opt_group_kernel): one LDS per point
+struct PtsSmem {
+    using P = short2;
+    uint32_t base;   // shared-window address of the n short2
+    __device__ __forceinline__ P at(int i) const {
+        uint32_t v;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + 4u * (uint32_t)i));
+        return make_short2((short)(v & 0xFFFFu), (short)(v >> 16));
+    }
+    __device__ __forceinline__ static int64_t dist(P a, P b) { return euc2d_int(a, b); }
+};
+
 // neighbour k of a and d(a, it): one 4-byte load of the packed table (integer path), else two
 template <bool kInt>
 __device__ __forceinline__ void load_nbr(const TwoOptArgs& T, int a, int k, int& c, int64_t& d) {
@@ -278,12 +290,11 @@ __device__ __forceinline__ uint4 pack_eval(const MoveEval& m) {
 
 // Evaluate node a on the current route (one warp).  Lane k: the k-th neighbour.
 // d(a, c) comes from the setup's neighbour-distance table (loaded with the neighbour id).
-template <bool kInt>
-__device__ __forceinline__ MoveEval eval_node(const TwoOptArgs& T, const uint16_t* route, const uint16_t* pos,
-                                              int a, int lane) {
+template <bool kInt, class Xs>
+__device__ __forceinline__ MoveEval eval_node(const TwoOptArgs& T, const Xs& X, const uint16_t* route,
+                                              const uint16_t* pos, int a, int lane) {
     const int n = T.n, K = T.K;
-    const Pts<kInt> X(T);
-    using P = typename Pts<kInt>::P;
+    using P = typename Xs::P;
     int c = a, sc = 0, pc = 0;
     int64_t d_ac = 0;
     if (lane < K) load_nbr<kInt>(T, a, lane, c, d_ac);
@@ -326,6 +337,124 @@ __device__ __forceinline__ MoveEval eval_node(const TwoOptArgs& T, const uint16_
     return m;
 }
 
+// One ant's cooperative 2-opt by a group of kLsWarps warps (tid, warp: within the group),
+// synchronised by `sync` (the block barrier, or the group's named barrier).
+template <bool kInt, class Xs, class Sync>
+__device__ __forceinline__ long long coop_route(const TwoOptArgs& T, const Xs& X, uint16_t* route, uint16_t* queue,
+                                                uint16_t* s_route, uint16_t* s_pos, uint32_t* inq, uint4* s_eval,
+                                                int* s_ctl, int tid, int nthr, int lane, int warp, Sync sync) {
+    const int n = T.n;
+    long long moves = 0;
+    for (int i = 2 * tid; i < T.ldr; i += 2 * nthr)
+        *reinterpret_cast<uint32_t*>(s_route + i) = *reinterpret_cast<const uint32_t*>(route + i);
+    sync();
+    for (int i = tid; i < n; i += nthr) s_pos[s_route[i]] = (uint16_t)i;
+    int sweep_moves;
+    do {
+        // (re-)seed the queue with every node in route order
+        for (int i = tid; i < n; i += nthr) queue[i] = s_route[i];
+        for (int w = tid; w < T.nwords; w += nthr) inq[w] = 0xFFFFFFFFu;
+        if (tid == 0) {
+            s_ctl[0] = 0;
+            s_ctl[1] = n;
+            s_ctl[2] = 0;
+        }
+        sync();
+        while (true) {
+            const int head = s_ctl[0], count = s_ctl[1];
+            if (count == 0) break;
+            // warp w evaluates the w-th queued node (all on the same route)
+            if (warp < count) {
+                int q = head + warp;
+                if (q >= n) q -= n;
+                const MoveEval m = eval_node<kInt>(T, X, s_route, s_pos, (int)queue[q], lane);
+                if (lane == 0) s_eval[warp] = pack_eval(m);
+            }
+            sync();
+            // take the results in queue order up to the first improving one
+            const int avail = min(count, kLsWarps);
+            uint32_t fmask = 0;
+#pragma unroll
+            for (int w = 0; w < kLsWarps; ++w) fmask |= (w < avail && s_eval[w].x) ? 1u << w : 0u;
+            const int win = fmask ? __ffs(fmask) - 1 : -1;
+            const int retired = win >= 0 ? win + 1 : avail;
+            if (warp == 0 && lane < retired) {
+                int q = head + lane;
+                if (q >= n) q -= n;
+                const int a = queue[q];
+                atomicAnd(inq + (a >> 5), ~(1u << (a & 31)));
+            }
+            int nhead = head + retired;
+            if (nhead >= n) nhead -= n;
+            int ncount = count - retired;
+            if (tid == 0) trace_ls_round(retired, avail - retired);
+            if (win >= 0) {
+                const uint4 pe = s_eval[win];
+                const int mb = (int)(pe.y & 0xFFFFu), mc = (int)(pe.y >> 16), md = (int)pe.z;
+                int q = head + win;
+                if (q >= n) q -= n;
+                const int a = queue[q];
+                // reverse (all lanes of all warps; disjoint pairs); the segment's positions
+                // come with the evaluation, so no thread reads pos before it changes
+                int i = (int)(pe.w & 0xFFFFu);
+                int j = (int)(pe.w >> 16);
+                int len = j - i;
+                if (len < 0) len += n;
+                len += 1;
+                if (2 * len > n) {
+                    const int ni = wrap_inc(j, n), nj = wrap_dec(i, n);
+                    i = ni;
+                    j = nj;
+                    len = n - len;
+                }
+                if (tid == 0) trace_ls_len(len);
+                for (int k = tid; k < len / 2; k += nthr) {
+                    int p = i + k;
+                    if (p >= n) p -= n;
+                    int qq = j - k;
+                    if (qq < 0) qq += n;
+                    const uint16_t vp = s_route[p], vq = s_route[qq];
+                    s_route[p] = vq;
+                    s_route[qq] = vp;
+                    s_pos[vq] = (uint16_t)p;
+                    s_pos[vp] = (uint16_t)qq;
+                }
+                // enqueue a, b, c, d in that order (thread 0; the bits of a .. d)
+                if (tid == 0) {
+                    const int ends[4] = {a, mb, mc, md};
+                    __threadfence_block();
+                    for (int e = 0; e < 4; ++e) {
+                        const int v = ends[e];
+                        const uint32_t bit = 1u << (v & 31);
+                        if (!(atomicOr(inq + (v >> 5), bit) & bit)) {
+                            int t = nhead + ncount;
+                            if (t >= n) t -= n;
+                            queue[t] = (uint16_t)v;
+                            ++ncount;
+                        }
+                    }
+                    s_ctl[2] += 1;
+                }
+            }
+            // every thread read head / count before the first barrier of this round, so
+            // thread 0 may publish the next round's values now; one barrier covers both
+            // the reversal and the queue state
+            if (tid == 0) {
+                s_ctl[0] = nhead;
+                s_ctl[1] = ncount;
+            }
+            sync();
+        }
+        sweep_moves = s_ctl[2];
+        moves += sweep_moves;
+        sync();
+    } while (sweep_moves > 0);
+    for (int i = 2 * tid; i < T.ldr; i += 2 * nthr)
+        *reinterpret_cast<uint32_t*>(route + i) = *reinterpret_cast<const uint32_t*>(s_route + i);
+    sync();
+    return moves;
+}
+
 template <bool kInt>
 __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs T, ConstructArgs A) {
     if (blockIdx.y) colony_offset(T, A, (int)blockIdx.y);
@@ -336,128 +465,74 @@ __global__ void __launch_bounds__(kLsWarps * 32) two_opt_coop_kernel(TwoOptArgs 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const int n = T.n;
     uint16_t* s_route = ls_smem;
     uint16_t* s_pos = ls_smem + T.ldr;
     uint32_t* inq = reinterpret_cast<uint32_t*>(ls_smem + 2 * T.ldr);   // queued bits (smem atomics)
+    const Pts<kInt> X(T);
     unsigned long long wbest = ~0ull;
     long long moves = 0;
     for (int al = blockIdx.x; al < T.m_local; al += gridDim.x) {
         uint16_t* route = T.routes + (size_t)al * T.ldr;
-        uint16_t* queue = T.queue + (size_t)al * T.ldr;
-        for (int i = 2 * tid; i < T.ldr; i += 2 * blockDim.x)
-            *reinterpret_cast<uint32_t*>(s_route + i) = *reinterpret_cast<const uint32_t*>(route + i);
-        __syncthreads();
-        for (int i = tid; i < n; i += blockDim.x) s_pos[s_route[i]] = (uint16_t)i;
-        int sweep_moves;
-        do {
-            // (re-)seed the queue with every node in route order
-            for (int i = tid; i < n; i += blockDim.x) queue[i] = s_route[i];
-            for (int w = tid; w < T.nwords; w += blockDim.x) inq[w] = 0xFFFFFFFFu;
-            if (tid == 0) {
-                s_ctl[0] = 0;
-                s_ctl[1] = n;
-                s_ctl[2] = 0;
-            }
-            __syncthreads();
-            while (true) {
-                const int head = s_ctl[0], count = s_ctl[1];
-                if (count == 0) break;
-                // warp w evaluates the w-th queued node (all on the same route)
-                if (warp < count) {
-                    int q = head + warp;
-                    if (q >= n) q -= n;
-                    const MoveEval m = eval_node<kInt>(T, s_route, s_pos, (int)queue[q], lane);
-                    if (lane == 0) s_eval[warp] = pack_eval(m);
-                }
-                __syncthreads();
-                // take the results in queue order up to the first improving one
-                const int avail = min(count, kLsWarps);
-                uint32_t fmask = 0;
-#pragma unroll
-                for (int w = 0; w < kLsWarps; ++w) fmask |= (w < avail && s_eval[w].x) ? 1u << w : 0u;
-                const int win = fmask ? __ffs(fmask) - 1 : -1;
-                const int retired = win >= 0 ? win + 1 : avail;
-                if (warp == 0 && lane < retired) {
-                    int q = head + lane;
-                    if (q >= n) q -= n;
-                    const int a = queue[q];
-                    atomicAnd(inq + (a >> 5), ~(1u << (a & 31)));
-                }
-                int nhead = head + retired;
-                if (nhead >= n) nhead -= n;
-                int ncount = count - retired;
-                if (tid == 0) trace_ls_round(retired, avail - retired);
-                if (win >= 0) {
-                    const uint4 pe = s_eval[win];
-                    const int mb = (int)(pe.y & 0xFFFFu), mc = (int)(pe.y >> 16), md = (int)pe.z;
-                    int q = head + win;
-                    if (q >= n) q -= n;
-                    const int a = queue[q];
-                    // reverse (all lanes of all warps; disjoint pairs); the segment's positions
-                    // come with the evaluation, so no thread reads pos before it changes
-                    int i = (int)(pe.w & 0xFFFFu);
-                    int j = (int)(pe.w >> 16);
-                    int len = j - i;
-                    if (len < 0) len += n;
-                    len += 1;
-                    if (2 * len > n) {
-                        const int ni = wrap_inc(j, n), nj = wrap_dec(i, n);
-                        i = ni;
-                        j = nj;
-                        len = n - len;
-                    }
-                    if (tid == 0) trace_ls_len(len);
-                    for (int k = tid; k < len / 2; k += blockDim.x) {
-                        int p = i + k;
-                        if (p >= n) p -= n;
-                        int qq = j - k;
-                        if (qq < 0) qq += n;
-                        const uint16_t vp = s_route[p], vq = s_route[qq];
-                        s_route[p] = vq;
-                        s_route[qq] = vp;
-                        s_pos[vq] = (uint16_t)p;
-                        s_pos[vp] = (uint16_t)qq;
-                    }
-                    // enqueue a, b, c, d in that order (thread 0; the bits of a .. d)
-                    if (tid == 0) {
-                        const int ends[4] = {a, mb, mc, md};
-                        __threadfence_block();
-                        for (int e = 0; e < 4; ++e) {
-                            const int v = ends[e];
-                            const uint32_t bit = 1u << (v & 31);
-                            if (!(atomicOr(inq + (v >> 5), bit) & bit)) {
-                                int t = nhead + ncount;
-                                if (t >= n) t -= n;
-                                queue[t] = (uint16_t)v;
-                                ++ncount;
-                            }
-                        }
-                        s_ctl[2] += 1;
-                    }
-                }
-                // every thread read head / count before the first barrier of this round, so
-                // thread 0 may publish the next round's values now; one barrier covers both
-                // the reversal and the queue state
-                if (tid == 0) {
-                    s_ctl[0] = nhead;
-                    s_ctl[1] = ncount;
-                }
-                __syncthreads();
-            }
-            sweep_moves = s_ctl[2];
-            moves += sweep_moves;
-            __syncthreads();
-        } while (sweep_moves > 0);
-        for (int i = 2 * tid; i < T.ldr; i += 2 * blockDim.x)
-            *reinterpret_cast<uint32_t*>(route + i) = *reinterpret_cast<const uint32_t*>(s_route + i);
-        __syncthreads();
+        moves += coop_route<kInt>(T, X, route, T.queue + (size_t)al * T.ldr, s_route, s_pos, inq, s_eval, s_ctl, tid,
+                                  (int)blockDim.x, lane, warp, [] { __syncthreads(); });
         if (warp == 0) wbest = min(wbest, finish_ant(A, route, al, (uint32_t)(A.ant_lo + al), lane));
         __syncthreads();
     }
     if (tid == 0 && moves) atomicAdd(T.moves, (unsigned long long)moves);
     pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
     block_finish(A, wbest, 0, lane, warp);
+}
+
+// ---------------------------------------------------------------------------
+// Grouped cooperative 2-opt (integral coordinates, large n: C5).  The coordinate loads of an
+// evaluation (the popped node's two tour neighbours, each neighbour's successor or
+// predecessor) were L2 round trips on its chain: three 76 KB one-ant blocks per SM leave no
+// L1 for 74 KB of coordinates.  Here one block holds the coordinates once in shared memory
+// and runs kGroups ants side by side (kLsWarps warps each, the group's own named barrier
+// 1 + g), each with its own route / pos / queued bits.  Same rounds, same moves.  Measured on
+// C5: rounds ~20 % shorter, but two ants per SM instead of three: 125 -> 151 ms; opt-in only.
+// Shared memory: coordinates (n short2, 16 B aligned), then per group route, pos, inq.
+// ---------------------------------------------------------------------------
+constexpr int kLsGroupsMax = 2;
+template <int kGroups>
+__global__ void __launch_bounds__(kGroups * kLsWarps * 32) two_opt_group_kernel(TwoOptArgs T, ConstructArgs A) {
+    if (blockIdx.y) colony_offset(T, A, (int)blockIdx.y);
+    pdl_wait();
+    extern __shared__ __align__(16) uint16_t ls_smem[];
+    __shared__ uint4 s_eval[kGroups][kLsWarps];
+    __shared__ int s_ctl[kGroups][4];
+    const int n = T.n;
+    const int lane = threadIdx.x & 31;
+    const int g = (int)(threadIdx.x >> 5) / kLsWarps;
+    const int tid = (int)threadIdx.x - g * kLsWarps * 32;
+    const int warp = tid >> 5;
+    const uint32_t xy_bytes = ((uint32_t)n * 4u + 15u) & ~15u;
+    {   // the coordinates, once per block
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(T.xys);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(ls_smem);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    const uint32_t per_ant = (uint32_t)(4 * T.ldr + 4 * T.nwords);
+    uint16_t* s_route = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(ls_smem) + xy_bytes + g * per_ant);
+    uint16_t* s_pos = s_route + T.ldr;
+    uint32_t* inq = reinterpret_cast<uint32_t*>(s_pos + T.ldr);
+    PtsSmem X;
+    X.base = (uint32_t)__cvta_generic_to_shared(ls_smem);
+    const int bar = 1 + g;
+    auto sync = [bar] { asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(kLsWarps * 32) : "memory"); };
+    unsigned long long wbest = ~0ull;
+    long long moves = 0;
+    for (int al = blockIdx.x * kGroups + g; al < T.m_local; al += gridDim.x * kGroups) {
+        uint16_t* route = T.routes + (size_t)al * T.ldr;
+        moves += coop_route<true>(T, X, route, T.queue + (size_t)al * T.ldr, s_route, s_pos, inq, s_eval[g], s_ctl[g],
+                                  tid, kLsWarps * 32, lane, warp, sync);
+        if (warp == 0) wbest = min(wbest, finish_ant(A, route, al, (uint32_t)(A.ant_lo + al), lane));
+        sync();
+    }
+    if (tid == 0 && moves) atomicAdd(T.moves, (unsigned long long)moves);
+    pdl_trigger();   // this block is done with its ants: let the next kernel's blocks in
+    block_finish(A, wbest, 0, lane, (int)(threadIdx.x >> 5));
 }
 
 }  // namespace mmas

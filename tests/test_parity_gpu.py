@@ -320,6 +320,25 @@ def test_two_opt_bit_exact(n, m, cl, iters):
     lockstep(make_coords("uniform", n, 3000 + n), m, cl, iters, seed=11 + n, local_search=True, rho=0.7)
 
 
+@pytest.mark.parametrize("n,m,cl,iters", [(300, 21, 32, 2), (1100, 9, 32, 2), (60, 5, 8, 3)],
+                         ids=["n300-odd-ants", "n1100", "n60"])
+def test_two_opt_grouped_kernel_bit_exact(n, m, cl, iters, monkeypatch):
+    """The grouped 2-opt kernel (coordinates in shared memory, two ants per block, one named
+    barrier per ant; opt-in with MMAS_LS_GROUP=1): lockstep with the oracle, including an odd
+    ant count (one group of the last block idle)."""
+    monkeypatch.setenv("MMAS_LS_GROUP", "1")
+    lockstep(make_coords("uniform", n, 5000 + n), m, cl, iters, seed=9 + n, local_search=True, rho=0.7)
+
+
+@pytest.mark.parametrize("n,m,cl", [(300, 20, 32), (150, 20, 16)], ids=["cl32", "cl16"])
+def test_two_opt_host_built_lists_bit_exact(n, m, cl, monkeypatch):
+    """The candidate and 2-opt neighbour lists (and the neighbour distances) built on the host
+    (the path for rows whose distances exceed shared memory, n > ~57k; forced here with
+    MMAS_HOST_CAND) equal the device-built ones: lockstep with the oracle."""
+    monkeypatch.setenv("MMAS_HOST_CAND", "1")
+    lockstep(make_coords("uniform", n, 4000 + n), m, cl, 2, seed=3 + n, local_search=True, rho=0.7)
+
+
 @pytest.mark.parametrize("shift,scale", [(0.25, 1.0), (0.0, 3.0)], ids=["fractional", "beyond-16383"])
 def test_two_opt_bit_exact_double_distance_path(shift, scale):
     """Coordinates that are not integers, or exceed |x| <= 16383, take the 2-opt kernels'

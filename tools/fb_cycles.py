@@ -51,7 +51,8 @@ def child(cfg, first, count):
     nc = buf[16]
     compact = {"count": nc, "phases_count_keys_select": [round(buf[17 + k] / max(nc, 1)) for k in range(3)],
                "start_to_entry": round((buf[21] - buf[22]) / max(nc, 1))} if nc else None
-    print(json.dumps({"fallbacks": cnt, "cycles_per_fallback": cyc / max(cnt, 1), "by_unvisited": buckets,
+    groups = {"hit": [int(buf[49]), round(buf[48] / max(buf[49], 1))], "clean": [int(buf[51]), round(buf[50] / max(buf[51], 1))]}
+    print(json.dumps({"fallbacks": cnt, "cycles_per_fallback": cyc / max(cnt, 1), "by_unvisited": buckets, "groups": groups,
                       "compact": compact,
                       "fallbacks_per_tour": cnt / (count * w.n_ants), "ms_per_iteration": ms / count}))
 
