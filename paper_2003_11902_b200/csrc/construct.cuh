@@ -461,6 +461,14 @@ __device__ __forceinline__ float det_log2_sel(float u) {
     return __fmaf_rn(f, p, ef);
 }
 
+// (checked builds) is city c -- one of this lane's own -- marked in the tabu?
+template <bool kLazyW>
+__device__ __forceinline__ bool tabu_own_visited(const RegTabuX<kLazyW>& t, uint32_t c, int lane) {
+    return (c & 31u) == (uint32_t)lane && ((t.wt >> (c >> 5)) & 1u);
+}
+__device__ __forceinline__ bool tabu_own_visited(const SmemTabu& t, uint32_t c, int) {
+    return (t.t[c >> 5] >> (c & 31)) & 1u;
+}
 struct LaneCitiesReg {   // register tabu: bit k of ~wt = city 32 k + lane
     uint32_t f;
     int lane;
@@ -513,15 +521,15 @@ __device__ __forceinline__ LaneCitiesSmem lane_cities(const SmemTabu& t, int n, 
     return LaneCitiesSmem(t, n, lane);
 }
 
+// The per-lane part: (bm, bc) = this lane's minimum over its unvisited cities, 1 / choice_info
+// of city c from ivf(c) (a row of inv_w, or the lean pheromone's recomputed background).
 // (inlined: out of line measured 1 % slower on C2, the call's ~200-cycle entry)
-template <class Tabu>
-__device__ __forceinline__ uint32_t fallback_compact(const float* __restrict__ row, const Tabu tabu, int n,
-                                                  uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
-                                                  int lane) {
+template <class Tabu, class IvF>
+__device__ __forceinline__ void compact_scan(IvF ivf, const Tabu& tabu, int n, uint32_t step, uint32_t ant,
+                                             uint32_t iter, PhiloxKey key, int lane, uint32_t& bm, uint32_t& bc) {
     const long long t0 = trace_clock();
     auto it = lane_cities(tabu, n, lane);
     const uint32_t cnt = (uint32_t)it.count();
-    uint32_t bm = kNone, bc = kNone;
     // K cities per lane at a time, branch-free (a lane with fewer carries kNone), so the K
     // Philox / log chains interleave
     auto eval = [&](auto K, const uint32_t* c, const float* iv) {
@@ -554,7 +562,10 @@ __device__ __forceinline__ uint32_t fallback_compact(const float* __restrict__ r
 #pragma unroll
         for (int j = 0; j < 8; ++j) c[j] = it.next();
 #pragma unroll
-        for (int j = 0; j < 8; ++j) iv[j] = c[j] != kNone ? __ldg(row + c[j]) : 0.f;
+        for (int j = 0; j < 8; ++j) {
+            MMAS_CHECK(c[j] == kNone || (c[j] < (uint32_t)n && !tabu_own_visited(tabu, c[j], lane)));
+            iv[j] = c[j] != kNone ? ivf(c[j]) : 0.f;
+        }
     };
     fetch();
     const int most = (int)__reduce_max_sync(kFull, cnt);
@@ -568,9 +579,44 @@ __device__ __forceinline__ uint32_t fallback_compact(const float* __restrict__ r
         if (r >= most) break;
         fetch();
     }
-    const long long t2 = trace_clock();
+    trace_compact(lane, t0, t1, trace_clock(), trace_clock());
+}
+template <class Tabu>
+__device__ __forceinline__ uint32_t fallback_compact(const float* __restrict__ row, const Tabu& tabu, int n,
+                                                  uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
+                                                  int lane) {
+    uint32_t bm = kNone, bc = kNone;
+    compact_scan([row](uint32_t c) { return __ldg(row + c); }, tabu, n, step, ant, iter, key, lane, bm, bc);
     const uint32_t res = warp_select(bm, bc);
-    trace_compact(lane, t0, t1, t2, trace_clock());
+    MMAS_CHECK(res < (uint32_t)n);
+    return res;
+}
+// The memory-lean pheromone's fallback (R30) compacted: the row's sparse cities hidden in the
+// tabu, every other unvisited city evaluated with the background's 1 / choice_info recomputed
+// from the coordinates (the dense value, lean_scan's formula), the sparse ones unhidden and
+// evaluated with their stored values -- the same argmax as the dense scan.
+template <class Tabu>
+__device__ __forceinline__ uint32_t lean_fallback_compact(const LeanArgs& Ln, const double2* __restrict__ xy, int cur,
+                                                       Tabu& tabu, int n, int alpha, uint32_t step, uint32_t ant,
+                                                       uint32_t iter, PhiloxKey key, int lane) {
+    const uint32_t hid = lean_hide(Ln, cur, tabu, n, lane);
+    uint32_t bm = kNone, bc = kNone;
+    if (Ln.xys) {
+        const short2 xcs = __ldg(Ln.xys + cur);
+        const short2* __restrict__ xys = Ln.xys;
+        const float* __restrict__ tab = Ln.inv_tab;
+        compact_scan([=](uint32_t c) { return __ldg(tab + euc2d_int(xcs, __ldg(xys + c))); }, tabu, n, step, ant,
+                     iter, key, lane, bm, bc);
+    } else {
+        const float ba = pow_alpha(__ldcg(Ln.bg + Ln.parity), alpha);
+        const double2 xc = __ldg(xy + cur);
+        const int beta = Ln.beta;
+        compact_scan([=](uint32_t c) { return __fdiv_rn(1.0f, __fmul_rn(ba, heur_edge(xc, __ldg(xy + c), beta))); },
+                     tabu, n, step, ant, iter, key, lane, bm, bc);
+    }
+    lean_unhide(Ln, cur, tabu, hid, step, ant, iter, key, lane, bm, bc);
+    const uint32_t res = warp_select(bm, bc);
+    MMAS_CHECK(res < (uint32_t)n);
     return res;
 }
 
@@ -1289,6 +1335,14 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
                 const long long t_fb = trace_clock();
                 const float* row = c_inv_w + (size_t)cur * A.ld;
                 uint32_t fm = kNone, fc = kNone;
+                if (A.lean.cand_tau && n - s <= A.fb_lane_cap) {
+                    // memory-lean pheromone late in the tour: the ant warp alone, compacted
+                    const uint32_t c = lean_fallback_compact(A.lean, A.xy, (int)cur, tabu, n, A.alpha, (uint32_t)s,
+                                                             ant, iter, c_key, lane);
+                    trace_fallback(t_fb, lane, n - s);
+                    commit(c, s);
+                    return;
+                }
                 if constexpr (kCoop) {
                     if (coop && A.lean.cand_tau) {
                         // the lean scan, paired (see CoopSlot): hidden sparse cities stay marked in
@@ -1328,7 +1382,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
                                s);
                     return;
                 }
-                if (n - s <= A.fb_lane_cap && !A.fallback_argmax) {
+                if (n - s <= A.fb_lane_cap && !A.fallback_argmax) {   // (lean: above)
                     // late in the tour (n - s unvisited cities): each lane evaluates only its own
                     const uint32_t c = fallback_compact(row, tabu, n, (uint32_t)s, ant, iter, c_key, lane);
                     trace_fallback(t_fb, lane, n - s);

@@ -19,6 +19,25 @@ namespace mmas {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
+// Device-side bounds checks (-DMMAS_CHECKED builds: tools/checked_runs.py; compute-sanitizer is
+// not available on the GPU pool).  A failed check records its line in g_check_line and traps,
+// so the launch fails with an error instead of reading or writing out of bounds.
+#ifdef MMAS_CHECKED
+__device__ int g_check_line;
+#define MMAS_CHECK(cond)                                   \
+    do {                                                   \
+        if (!(cond)) {                                     \
+            atomicExch(&::mmas::g_check_line, __LINE__);   \
+            __threadfence_system();                        \
+            __trap();                                      \
+        }                                                  \
+    } while (0)
+#else
+#define MMAS_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 // Programmatic dependent launch: the iteration's kernels are launched with
 // programmatic stream serialisation, so a kernel's blocks are resident before its
 // predecessor finishes; each waits here before touching the predecessor's output
@@ -931,6 +950,8 @@ __global__ void __launch_bounds__(kNnThreads) nn_tour_kernel(const double2* __re
                 nn_bar(1, T);
                 nxt = full_scan();
             }
+            MMAS_CHECK(nxt < (uint32_t)n && !((vis[nxt >> 5] >> (nxt & 31)) & 1u));
+            __syncwarp();
             if (lane == 0) {
                 vis[nxt >> 5] |= 1u << (nxt & 31);
                 route[s] = (uint16_t)nxt;
@@ -1010,6 +1031,7 @@ __global__ void ls_dist_kernel(const double2* __restrict__ xy, int n, int k, con
          e += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(e / k);
         const uint32_t j = nn[e];
+        MMAS_CHECK(j < (uint32_t)n && j != (uint32_t)i);
         const int32_t d = euc2d(xy[i], xy[j]);
         nnd[e] = d;
         if (nnp) nnp[e] = j | ((uint32_t)d << 16);

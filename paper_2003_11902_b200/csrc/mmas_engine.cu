@@ -1038,10 +1038,23 @@ int setup(mmas_ctx* h) {
                 // paired fallback scans (construct.cuh CoopSlot): at fewer than 16 ant warps per SM
                 // (the uncapped-register instantiation), n > 1024, one slot per lane, WRS fallback:
                 // each block's four warps build two ants, each with a helper for its scans
+                // -- only while the paired grid (twice the blocks) is still resident in one wave:
+                // C65KL's 32 KB tabus make ~100 KB blocks, 2 per SM, and 400 paired blocks
+                // measured 1504 ms against 1256 ms for 200 unpaired ones
                 const char* cf = std::getenv("MMAS_COOP_FB");
                 h->coop_fb = !(cf && cf[0] == '0') && !h->reg_tabu && h->slots == 1 &&
                              (long long)h->m_local * h->colonies < 16ll * h->num_sms &&
                              c.fallback == MMAS_FALLBACK_WRS;
+                if (h->coop_fb && !(cf && cf[0] == '1')) {
+                    int per_sm = 0;
+                    set_smem_attr<1, false, false, true, true>(h->smem_optin);
+                    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, construct_cl_kernel<1, false, false, true, true>,
+                                                                      h->cons_warps * 32, with_row) != cudaSuccess) {
+                        cudaGetLastError();
+                        per_sm = 0;
+                    }
+                    h->coop_fb = (long long)std::max(1, (h->m_local + 1) / 2) * h->colonies <= (long long)per_sm * h->num_sms;
+                }
                 if (h->coop_fb) h->cons_grid = std::max(1, (h->m_local + 1) / 2);
             }
         }
@@ -1061,15 +1074,19 @@ int setup(mmas_ctx* h) {
     }
     if (h->cons_smem > cons_dyn_max)
         return fail(MMAS_EINVAL, "n too large for the shared-memory tabu of one block");
-    // lane-compacted fallback scans (construct.cuh fallback_compact): taken at steps with at
-    // most cap unvisited cities.  Measured (A/B): with the register tabu and
-    // a row of more than two 256-city trips (C2) the compacted scan wins up to ~cap; a one- or
-    // two-trip row (C1) is cheaper to scan whole, the shared-memory tabu's word counts cost
-    // more than they save (C3 +2 %), and HBM-resident rows (C5) pay a 32-byte sector per city.
+    // lane-compacted fallback scans (construct.cuh fallback_compact / lean_fallback_compact):
+    // taken at steps with at most cap unvisited cities.  Measured (A/B):
+    // register tabu with rows of more than two 256-city trips (C2) 224 (driver window 0.2286
+    // -> 0.2038 ms with the rest of the round's fallback work); one- or two-trip rows (C1) are
+    // cheaper to scan whole; the shared-memory tabu with L2-resident rows (C3) 64 (5.13 ->
+    // 5.06 ms; 128+ slower: the per-lane word counts); HBM-resident rows (C5, paired scans)
+    // n / 8 (construction 18.6 -> 14.7 ms at 2048; 4096: 15.0, 9256: 16.9); the memory-lean
+    // pheromone, whose trip scans recompute every background value from the coordinates, n / 2
+    // (C65KL 1256 -> ~300 ms per iteration, C5L construction 44 -> 25 ms).
     // MMAS_FB_COMPACT=<cap> overrides (0 = off; the parity tests force every variant).
-    if (h->cl > 0 && !h->rwm && !h->lean) {
+    if (h->cl > 0 && !h->rwm) {
         const bool hbm_rows = 4.0 * (double)n * h->ld > 0.75 * (double)h->l2_bytes;
-        int cap = (h->reg_tabu && n > 512 && !hbm_rows) ? 224 : 0;
+        int cap = h->lean ? n / 2 : h->reg_tabu ? (n > 512 && !hbm_rows ? 224 : 0) : (hbm_rows ? n / 8 : 64);
         if (const char* e = std::getenv("MMAS_FB_COMPACT")) cap = std::max(0, std::atoi(e));
         h->fb_lane_cap = cap;
     }

@@ -1,7 +1,14 @@
-set -x
-mkdir -p gpurun_out/r02m
-timeout 1200 python -m pytest tests -m gpu -q -x --durations=5 > gpurun_out/r02m/pytest.log 2>&1; echo rc=$? >> gpurun_out/r02m/pytest.log; tail -3 gpurun_out/r02m/pytest.log
-for cfg in C5L C65KL; do timeout 900 python bench.py --config $cfg --steps 4 --warmup 5 --no-cpu-baseline > gpurun_out/r02m/bench_$cfg.json 2>gpurun_out/r02m/bench_$cfg.err; head -c 250 gpurun_out/r02m/bench_$cfg.json; echo; done
-MMAS_CREATE_PROFILE=1 timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r02m/bench_driver.json 2> gpurun_out/r02m/bench_driver.err; head -c 300 gpurun_out/r02m/bench_driver.json; echo
-bash scripts/gpu_session.sh r02m ncu ncuC1 ncuC3 ncuC4 ncuC4CT ncuC5 ncuC5L ncuC2x8
-timeout 2400 bash scripts/sanitize.sh r02m_sanitize
+#!/bin/bash
+# round-2 session m: compacted fallback caps on C3 (shared-memory tabu, L2 rows) and C5 (HBM rows)
+OUT=gpurun_out/r02m; mkdir -p $OUT
+export PYTHONUNBUFFERED=1
+for r in 1 2; do
+ for cap in 0 64 128 256 512; do
+  MMAS_FB_COMPACT=$cap timeout 900 python bench.py --config C3 --steps 20 --warmup 5 --no-cpu-baseline > $OUT/c3.json 2>>$OUT/b.err
+  python -c "import json; d=json.loads(open('$OUT/c3.json').readline()); print('C3 cap=$cap', round(d['ms_per_step'],4), round(d['phases_ms_per_step']['construct'],4))"
+ done
+ for cap in 0 32 64 128; do
+  MMAS_FB_COMPACT=$cap timeout 900 python bench.py --config C5 --steps 3 --warmup 3 --no-cpu-baseline > $OUT/c5.json 2>>$OUT/b.err
+  python -c "import json; d=json.loads(open('$OUT/c5.json').readline()); print('C5 cap=$cap', round(d['ms_per_step'],3), round(d['phases_ms_per_step']['construct'],3))"
+ done
+done

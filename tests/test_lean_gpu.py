@@ -111,3 +111,37 @@ def test_lean_maximum_n():
     assert gl <= L.min()
     assert g.stats()["fallback_steps"] > 0
     g.status()
+
+
+# ---- the lean fallback compacted (construct.cuh lean_fallback_compact) -----------------------
+LEAN_COMPACT = [
+    # (shape, n, m, cl, iterations, kwargs, env)
+    ("fl3795", 600, 60, 8, 3, {}, {}),                                   # register tabu, smem table
+    ("fl3795", 1100, 24, 6, 2, {}, {}),                                  # shared-memory tabu
+    ("fl3795", 1500, 24, 32, 2, {}, {}),                                 # L2-table kernel
+    ("fl3795", 1300, 20, 4, 2, {}, {"MMAS_FB_ROW": "1"}),                # paired (C5-style) kernel
+    ("uniform", 300, 30, 8, 3, {"beta": 3.0}, {}),                       # beta 3
+]
+
+
+@pytest.mark.parametrize("cap", ["all", "mixed"])
+@pytest.mark.parametrize("shape,n,m,cl,iters,kw,env", LEAN_COMPACT,
+                         ids=[f"{c[0]}-n{c[1]}-cl{c[3]}{'-row' if c[6] else ''}" for c in LEAN_COMPACT])
+def test_lean_compacted_fallback_equals_dense_oracle(shape, n, m, cl, iters, kw, env, cap, monkeypatch):
+    """The lean pheromone's compacted fallback (sparse cities hidden, every other unvisited city
+    with the recomputed background value, the sparse ones unhidden) against the dense oracle:
+    for every fallback ("all") and from a third of the tour on ("mixed")."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    monkeypatch.setenv("MMAS_FB_COMPACT", str(n if cap == "all" else n // 3))
+    g, o = lockstep_lean(make_coords(shape, n, 70 + n), m, cl, iters, **kw)
+    assert g.stats()["fallback_steps"] > 0
+
+
+def test_lean_compacted_fallback_fractional_coordinates(monkeypatch):
+    """Non-integral coordinates: the compacted lean scan recomputes 1 / (b^alpha eta^beta) in
+    double (heur_edge) instead of the table by distance."""
+    monkeypatch.setenv("MMAS_FB_COMPACT", "400")
+    c = make_coords("fl3795", 400, 11) + 0.25
+    g, o = lockstep_lean(c, 40, 6, 3)
+    assert g.stats()["fallback_steps"] > 0

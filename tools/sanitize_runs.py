@@ -5,7 +5,8 @@
 MODE: fused (one launch per iteration: construction + grid barrier + update), separate (the
 two-kernel path), exchange (two shards in one process on their own streams, the fused
 peer-exchange launch), split (two shards, construct_publish / update_exchange), full (cl = 0
-bitmask + compact tabu), ls (2-opt), rwm (roulette wheel).  d198-shaped C1 colony (smaller
+bitmask + compact tabu), ls (2-opt), rwm (roulette wheel), compact (the lane-compacted fallback
+scan on three kernel variants).  d198-shaped C1 colony (smaller
 for the slow tools), 2 iterations; results compared with the oracle, so a run that the tool
 perturbs still has to be right."""
 import os
@@ -83,6 +84,20 @@ def main(mode):
             g.iterate(1)
             o.iterate(1)
             check([g], o, f"2-opt iteration {it}")
+    elif mode == "compact":
+        # the lane-compacted fallback scan on the register-tabu, shared-memory-tabu and
+        # L2-table kernels (forced for every fallback); the NN tour and list kernels run in
+        # every mode's setup
+        os.environ["MMAS_FB_COMPACT"] = "4096"
+        for n, mm, cl in ((700, 24, 6), (1100, 16, 6), (1500, 16, 32)):
+            cc = make_coords("fl3795", n, 7)
+            g = mmas.Colony(cc, mm, cl, seed=3)
+            o = oracle.Colony(cc, mm, cl, seed=3)
+            assert g.stats()["fallback_lane_cap"] == 4096
+            for it in range(2):
+                g.iterate(1)
+                o.iterate(1)
+                check([g], o, f"compact n={n} iteration {it}")
     elif mode == "rwm":
         g = mmas.Colony(c, 32, cl, seed=3, selection=mmas.SELECT_RWM)
         o = oracle.Colony(c, 32, cl, seed=3, selection=1)
