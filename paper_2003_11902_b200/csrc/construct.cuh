@@ -525,7 +525,7 @@ __device__ __forceinline__ LaneCitiesSmem lane_cities(const SmemTabu& t, int n, 
 // of city c from ivf(c) (a row of inv_w, or the lean pheromone's recomputed background).
 // (inlined: out of line measured 1 % slower on C2, the call's ~200-cycle entry)
 template <class Tabu, class IvF>
-__device__ __forceinline__ void compact_scan(IvF ivf, const Tabu& tabu, int n, uint32_t step, uint32_t ant,
+__device__ __forceinline__ void compact_scan(IvF ivf, const Tabu tabu, int n, uint32_t step, uint32_t ant,
                                              uint32_t iter, PhiloxKey key, int lane, uint32_t& bm, uint32_t& bc) {
     const long long t0 = trace_clock();
     auto it = lane_cities(tabu, n, lane);
@@ -582,7 +582,7 @@ __device__ __forceinline__ void compact_scan(IvF ivf, const Tabu& tabu, int n, u
     trace_compact(lane, t0, t1, trace_clock(), trace_clock());
 }
 template <class Tabu>
-__device__ __forceinline__ uint32_t fallback_compact(const float* __restrict__ row, const Tabu& tabu, int n,
+__device__ __forceinline__ uint32_t fallback_compact(const float* __restrict__ row, const Tabu tabu, int n,
                                                   uint32_t step, uint32_t ant, uint32_t iter, PhiloxKey key,
                                                   int lane) {
     uint32_t bm = kNone, bc = kNone;
@@ -1335,16 +1335,8 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
                 const long long t_fb = trace_clock();
                 const float* row = c_inv_w + (size_t)cur * A.ld;
                 uint32_t fm = kNone, fc = kNone;
-                if (A.lean.cand_tau && n - s <= A.fb_lane_cap) {
-                    // memory-lean pheromone late in the tour: the ant warp alone, compacted
-                    const uint32_t c = lean_fallback_compact(A.lean, A.xy, (int)cur, tabu, n, A.alpha, (uint32_t)s,
-                                                             ant, iter, c_key, lane);
-                    trace_fallback(t_fb, lane, n - s);
-                    commit(c, s);
-                    return;
-                }
                 if constexpr (kCoop) {
-                    if (coop && A.lean.cand_tau) {
+                    if (coop && A.lean.cand_tau && n - s > A.fb_lane_cap) {
                         // the lean scan, paired (see CoopSlot): hidden sparse cities stay marked in
                         // the ant's shared-memory tabu while both warps scan their trips
                         const uint32_t hid = lean_hide(A.lean, (int)cur, tabu, n, lane);
@@ -1371,6 +1363,18 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
                 }
                 if (A.lean.cand_tau) {
                     // memory-lean pheromone (R30): no inv_w row; the scan recomputes it
+                    // late in the tour: compacted, the ant warp alone -- in the L2-table kernels
+                    // (C5L, C65KL), not in the 255-register shared-memory-table ones, whose step
+                    // loops move by ~1 % with any added code (C2 A/B; their lean rows are short)
+                    if constexpr (!(kSmemTable && !kWide)) {
+                        if (n - s <= A.fb_lane_cap) {
+                            const uint32_t c = lean_fallback_compact(A.lean, A.xy, (int)cur, tabu, n, A.alpha,
+                                                                     (uint32_t)s, ant, iter, c_key, lane);
+                            trace_fallback(t_fb, lane, n - s);
+                            commit(c, s);
+                            return;
+                        }
+                    }
                     tabu.prepare(lane);
                     if constexpr (kSmemTable && !kWide)
                         commit(lean_fallback_ool(A.lean, A.xy, (int)cur, tabu, n, A.alpha, (uint32_t)s, ant, iter, c_key,
