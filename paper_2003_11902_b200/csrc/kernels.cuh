@@ -1022,6 +1022,83 @@ __global__ void __launch_bounds__(256) cand_lists_kernel(const double2* __restri
     }
 }
 
+// The same NN tour for n <= 1024 by one warp (C1, C2): the tabu in registers (lane l holds
+// cities l, l + 32, ... as bit k of its word, the layout of the construction kernels' candidate
+// test), the candidate rows and the coordinates staged in shared memory.  A candidate step is
+// a row read, a shuffle per lane and a ballot; an exhausted row is scanned by the warp alone
+// (each lane its own unvisited cities, ascending, then (d, id) by two reductions) instead of
+// waking a block.  Dynamic shared memory: route (1024 u16), coordinates (n short2 or double2),
+// candidate table (n x cl_ld u16).
+__global__ void __launch_bounds__(32) nn_tour_warp_kernel(const double2* __restrict__ xy,
+                                                          const short2* __restrict__ xys, int n,
+                                                          const uint16_t* __restrict__ cand, int cl, int cl_ld,
+                                                          long long* len_out) {
+    extern __shared__ __align__(16) unsigned char nnw_smem[];
+    uint16_t* route = reinterpret_cast<uint16_t*>(nnw_smem);
+    const size_t xy_b = xys ? (size_t)n * 4 : (size_t)n * 16;
+    short2* s_xys = reinterpret_cast<short2*>(nnw_smem + 2048);
+    double2* s_xy = reinterpret_cast<double2*>(nnw_smem + 2048);
+    uint16_t* s_cand = reinterpret_cast<uint16_t*>(nnw_smem + 2048 + ((xy_b + 15) & ~(size_t)15));
+    const int lane = threadIdx.x;
+    for (int i = lane; i < n; i += 32) {
+        if (xys) s_xys[i] = xys[i];
+        else s_xy[i] = xy[i];
+    }
+    for (int i = lane; i < n * cl_ld; i += 32) s_cand[i] = cand[i];
+    uint32_t wt = lane == 0 ? 1u : 0u;   // city 0 visited
+    const int cnt = (n - lane + 31) >> 5;   // this lane's cities l + 32 k < n
+    const uint32_t mine = cnt >= 32 ? 0xFFFFFFFFu : cnt <= 0 ? 0u : (1u << cnt) - 1u;
+    if (lane == 0) route[0] = 0;
+    __syncwarp();
+    int cur = 0;
+    for (int s = 1; s < n; ++s) {
+        uint32_t nxt = kNone;
+        for (int k0 = 0; k0 < cl && nxt == kNone; k0 += 32) {
+            const int k = k0 + lane;
+            const uint32_t c = k < cl ? (uint32_t)s_cand[cur * cl_ld + k] : 0u;
+            const bool vis = (__shfl_sync(kFull, wt, (int)(c & 31u)) >> (c >> 5)) & 1u;
+            const uint32_t m = __ballot_sync(kFull, k < cl && !vis);
+            if (m) nxt = __shfl_sync(kFull, c, __ffs(m) - 1);
+        }
+        if (nxt == kNone) {   // the row is exhausted (or no lists): the warp scans
+            uint32_t bd = kNone, bj = kNone;
+            uint32_t f = ~wt & mine;
+            if (xys) {
+                const short2 pc = s_xys[cur];
+                while (f) {
+                    const uint32_t j = 32u * (uint32_t)(__ffs(f) - 1) + (uint32_t)lane;
+                    f &= f - 1u;
+                    const uint32_t d = (uint32_t)euc2d_int(pc, s_xys[j]);
+                    if (d < bd) { bd = d; bj = j; }   // ascending j: ties keep the lower id
+                }
+            } else {
+                const double2 pc = s_xy[cur];
+                while (f) {
+                    const uint32_t j = 32u * (uint32_t)(__ffs(f) - 1) + (uint32_t)lane;
+                    f &= f - 1u;
+                    const uint32_t d = (uint32_t)euc2d(pc, s_xy[j]);
+                    if (d < bd) { bd = d; bj = j; }
+                }
+            }
+            const uint32_t wd = __reduce_min_sync(kFull, bd);
+            nxt = __reduce_min_sync(kFull, bd == wd ? bj : kNone);
+        }
+        MMAS_CHECK(nxt < (uint32_t)n);
+        if (lane == (int)(nxt & 31u)) wt |= 1u << (nxt >> 5);
+        if (lane == 0) route[s] = (uint16_t)nxt;
+        cur = (int)nxt;
+    }
+    __syncwarp();
+    long long len = 0;
+    for (int s = lane; s < n; s += 32) {
+        const int a = route[s], b = route[s + 1 < n ? s + 1 : 0];
+        len += xys ? (long long)euc2d_int(s_xys[a], s_xys[b]) : (long long)euc2d(s_xy[a], s_xy[b]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) len += __shfl_down_sync(kFull, len, o);
+    if (lane == 0) *len_out = len;
+}
+
 // 2-opt neighbour distances d(i, nn[i][q]) (R12) and, for integral coordinates, the packed
 // entries nn | d << 16 the 2-opt kernels read (row a8 setup; was a host pass)
 __global__ void ls_dist_kernel(const double2* __restrict__ xy, int n, int k, const uint16_t* __restrict__ nn,

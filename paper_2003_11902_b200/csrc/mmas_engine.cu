@@ -902,9 +902,18 @@ int setup(mmas_ctx* h) {
             const size_t budget = (size_t)h->smem_optin - 16384;   // static: tabu words + partials
             const int stage = h->cl > 0 && route_b + cand_b <= budget;
             const size_t dyn = route_b + (stage ? cand_b : 0);
-            cudaFuncSetAttribute(nn_tour_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-            nn_tour_kernel<<<1, nn_threads(n), dyn, h->stream>>>(h->xy, d_xys, n, h->cl > 0 ? h->cand_id : nullptr,
-                                                                 h->cl, h->cl_ld, stage, d_len);
+            // n <= 1024: one warp with the register tabu (nn_tour_warp_kernel), when the route,
+            // coordinates and candidate table fit in its shared memory
+            const size_t warp_dyn = 2048 + (((size_t)n * (d_xys ? 4 : 16) + 15) & ~(size_t)15) + cand_b;
+            if (n <= 1024 && warp_dyn <= budget && !std::getenv("MMAS_NN_BLOCK")) {
+                cudaFuncSetAttribute(nn_tour_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_dyn);
+                nn_tour_warp_kernel<<<1, 32, warp_dyn, h->stream>>>(h->xy, d_xys, n, h->cl > 0 ? h->cand_id : nullptr,
+                                                                    h->cl, h->cl_ld, d_len);
+            } else {
+                cudaFuncSetAttribute(nn_tour_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+                nn_tour_kernel<<<1, nn_threads(n), dyn, h->stream>>>(h->xy, d_xys, n, h->cl > 0 ? h->cand_id : nullptr,
+                                                                     h->cl, h->cl_ld, stage, d_len);
+            }
         }
         if (d_xys) CU(h->pooled ? cudaFreeAsync(d_xys, h->stream) : cudaFree(d_xys));
         h->launches++;

@@ -386,3 +386,20 @@ def test_best_length_async_matches_sync_reads():
     assert vals[0] == -1
     assert vals[-1] == g.best_length() == g.best_tour()[1]
     assert all(a >= b for a, b in zip(vals[1:], vals[2:]))
+
+
+# ---- setup: the NN tour (Alg. 1, R3) behind the limits ---------------------------
+@pytest.mark.parametrize("block", [False, True], ids=["warp-kernel", "block-kernel"])
+@pytest.mark.parametrize("n,cl,frac", [(198, 16, False), (1002, 32, False), (300, 0, False), (257, 8, True)],
+                         ids=["d198", "pr1002", "no-lists", "fractional"])
+def test_nn_tour_limits_equal_oracle(n, cl, frac, block, monkeypatch):
+    """tau_max = 1 / ((1 - rho) L_nn): the NN tour length of the one-warp kernel (n <= 1024,
+    register tabu) and of the block kernel (MMAS_NN_BLOCK=1) equal the oracle's, with the
+    candidate fast path (cl > 0), without lists, and with fractional coordinates (fp64 path)."""
+    if block:
+        monkeypatch.setenv("MMAS_NN_BLOCK", "1")
+    c = make_coords("uniform", n, 600 + n) + (0.375 if frac else 0.0)
+    g = mmas.Colony(c, 8, cl, seed=1)
+    o = oracle.Colony(c, 8, cl, seed=1)
+    assert g.limits() == o.limits()
+    assert o.nn_length == oracle.nn_tour(c)[1]
