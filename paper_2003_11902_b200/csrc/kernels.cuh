@@ -112,6 +112,9 @@ __device__ __forceinline__ void trace_compact(int lane, long long t0, long long 
 // [48], [49]: cycles and count of the speculative groups that hit a fallback (the whole group:
 // speculation, rollback, fallback scan, generic redo); [50], [51]: the same for clean groups
 __device__ __forceinline__ void trace_group(long long t0, int lane, bool hit) {
+#ifndef MMAS_TRACE_GROUPS   // (two atomics per group: only in builds that ask for them)
+    return;
+#endif
     if (lane == 0) {
         atomicAdd(&g_fbcyc[hit ? 48 : 50], (unsigned long long)(clock64() - t0));
         atomicAdd(&g_fbcyc[hit ? 49 : 51], 1ull);

@@ -60,7 +60,7 @@ def child(cfg, first, count):
 def main():
     if sys.argv[1:2] == ["build"]:
         from paper_2003_11902_b200 import build as b
-        cmd = [b.NVCC, *b.NVCC_FLAGS, "-DMMAS_TRACE", "-I", os.path.join(ROOT, "include"), "-o", SO, *b.SOURCES]
+        cmd = [b.NVCC, *b.NVCC_FLAGS, "-DMMAS_TRACE", "-DMMAS_TRACE_GROUPS", "-I", os.path.join(ROOT, "include"), "-o", SO, *b.SOURCES]
         subprocess.run(cmd, check=True, capture_output=True)
         print(SO)
         return
