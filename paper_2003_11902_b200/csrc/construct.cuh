@@ -1610,10 +1610,17 @@ __global__ void __launch_bounds__(128) construct_full_kernel(const ConstructArgs
         uint32_t stage = (lane == 0) ? start : 0u;
         uint32_t cur = start;
         for (int s = 1; s < n; ++s) {
-            uint32_t bm = kNone, bc = kNone;
-            scan_unvisited<false, true>(c_inv_w + (size_t)cur * A.ld, tabu, n, (uint32_t)s, ant, iter, c_key, lane, bm,
-                                  bc);
-            const uint32_t nxt = warp_select(bm, bc);
+            uint32_t nxt;
+            if (n - s <= A.fb_lane_cap) {
+                // late in the tour: each lane evaluates only its own unvisited cities (the
+                // candidate-list fallback's compacted scan, same keys, same argmax)
+                nxt = fallback_compact(c_inv_w + (size_t)cur * A.ld, tabu, n, (uint32_t)s, ant, iter, c_key, lane);
+            } else {
+                uint32_t bm = kNone, bc = kNone;
+                scan_unvisited<false, true>(c_inv_w + (size_t)cur * A.ld, tabu, n, (uint32_t)s, ant, iter, c_key, lane,
+                                            bm, bc);
+                nxt = warp_select(bm, bc);
+            }
             tabu.mark(nxt, lane);
             stage_route(route, s, nxt, lane, stage);
             tabu.sync();

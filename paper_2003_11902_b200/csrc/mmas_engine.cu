@@ -1098,6 +1098,13 @@ int setup(mmas_ctx* h) {
         int cap = h->lean ? n / 2 : h->reg_tabu ? (n > 512 && !hbm_rows ? 224 : 0) : (hbm_rows ? n / 8 : 64);
         if (const char* e = std::getenv("MMAS_FB_COMPACT")) cap = std::max(0, std::atoi(e));
         h->fb_lane_cap = cap;
+    } else if (h->cl == 0 && !h->rwm && !h->compact_tabu) {
+        // full-row construction (construct_full_kernel, C4): the same compacted scan for the
+        // last steps of a tour, where the pruned trip scan still draws a Philox per live group
+        // (C4 A/B: 27.78 ms at 0, 26.72 at 250 ~ n / 10, 26.83 at 398, 27.77 at 600, 31.9 at 1000)
+        int cap = n / 10;
+        if (const char* e = std::getenv("MMAS_FB_COMPACT")) cap = std::max(0, std::atoi(e));
+        h->fb_lane_cap = cap;
     }
     allow_max_smem(construct_rwm_kernel<false>, h->smem_optin);
     allow_max_smem(construct_rwm_kernel<true>, h->smem_optin);

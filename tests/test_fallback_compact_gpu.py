@@ -78,3 +78,14 @@ def test_default_cap_is_set_for_c2():
     w = CONFIGS["C1"]
     g = mmas.Colony(w.coords(), w.n_ants, w.cand_len, rho=w.rho, seed=w.mmas_seed)
     assert g.stats()["fallback_lane_cap"] == 0
+
+
+@pytest.mark.parametrize("cap_name,cap", CAPS, ids=[c[0] for c in CAPS])
+@pytest.mark.parametrize("n,m", [(300, 40), (1100, 16)], ids=["regtabu", "smemtabu"])
+def test_full_row_compacted_steps_bit_exact(n, m, cap_name, cap, monkeypatch):
+    """Full-row construction (cl = 0, construct_full_kernel): the last steps of a tour take the
+    compacted scan (default n / 10 unvisited cities); every variant against the oracle."""
+    monkeypatch.setenv("MMAS_FB_COMPACT", str(cap(n)))
+    c = make_coords("uniform", n, 1300 + n)
+    g, o = lockstep(c, m, 0, 2, seed=5 + n)
+    assert g.stats()["fallback_lane_cap"] == cap(n)
