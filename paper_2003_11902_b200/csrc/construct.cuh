@@ -1534,6 +1534,7 @@ __global__ void __launch_bounds__(kSmemTable ? (kWide ? 512 : 256) : 128, kSmemT
         __syncwarp();
         if (!A.skip_finish) wbest = min(wbest, finish_ant(A, route, al, ant, lane, A.lengths + (long long)col * A.cs.ants));
         wfb += fb;
+        trace_warp_done(warp, lane);
     }
     if constexpr (kCoop) {
         if (coop) {

@@ -72,6 +72,15 @@ __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) { return 
 // + selection), barrier released, end], %globaltimer ns, thread 0.  No code otherwise.
 #ifdef MMAS_TRACE
 __device__ unsigned long long g_trace[1024 * 8];
+// per (block, warp): %globaltimer when the warp finished its last ant (tools/trace_warps.py)
+__device__ unsigned long long g_trace_w[1024 * 16];
+__device__ __forceinline__ void trace_warp_done(int warp, int lane) {
+    if (lane == 0 && blockIdx.x < 1024 && warp < 16) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+        g_trace_w[blockIdx.x * 16 + warp] = t;
+    }
+}
 __device__ __forceinline__ void trace_mark(int k) {
     if (threadIdx.x == 0 && blockIdx.x < 1024) {
         unsigned long long t;
@@ -137,6 +146,7 @@ __device__ __forceinline__ void trace_ls_round(int retired, int discarded) {
 __device__ __forceinline__ void trace_ls_len(int) {}
 __device__ __forceinline__ void trace_ls_round(int, int) {}
 __device__ __forceinline__ void trace_mark(int) {}
+__device__ __forceinline__ void trace_warp_done(int, int) {}
 __device__ __forceinline__ long long trace_clock() { return 0; }
 __device__ __forceinline__ void trace_fallback(long long, int, int = -1) {}
 __device__ __forceinline__ void trace_compact(int, long long, long long, long long, long long) {}

@@ -1914,6 +1914,18 @@ extern "C" int mmas_debug_fb_cycles(unsigned long long* out) {
 #endif
 }
 
+extern "C" int mmas_debug_trace_warps(unsigned long long* out, int count) {
+#ifdef MMAS_TRACE
+    if (!out || count < 0 || count > 1024 * 16) return MMAS_EINVAL;
+    if (cudaMemcpyFromSymbol(out, mmas::g_trace_w, sizeof(unsigned long long) * count) != cudaSuccess) return MMAS_ECUDA;
+    return MMAS_OK;
+#else
+    (void)out;
+    (void)count;
+    return MMAS_ESTATE;
+#endif
+}
+
 extern "C" int mmas_debug_trace(unsigned long long* out, int count) {
 #ifdef MMAS_TRACE
     if (!out || count < 0 || count > 1024 * 8) return MMAS_EINVAL;
