@@ -1078,11 +1078,19 @@ __global__ void __launch_bounds__(32) nn_tour_warp_kernel(const double2* __restr
             uint32_t f = ~wt & mine;
             if (xys) {
                 const short2 pc = s_xys[cur];
-                while (f) {
-                    const uint32_t j = 32u * (uint32_t)(__ffs(f) - 1) + (uint32_t)lane;
-                    f &= f - 1u;
-                    const uint32_t d = (uint32_t)euc2d_int(pc, s_xys[j]);
-                    if (d < bd) { bd = d; bj = j; }   // ascending j: ties keep the lower id
+                while (__any_sync(kFull, f != 0u)) {   // four cities per lane per trip (ILP)
+                    uint32_t j[4], d[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        j[q] = f ? 32u * (uint32_t)(__ffs(f) - 1) + (uint32_t)lane : kNone;
+                        f &= f - 1u;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        d[q] = j[q] != kNone ? (uint32_t)euc2d_int(pc, s_xys[j[q]]) : kNone;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (d[q] < bd) { bd = d[q]; bj = j[q]; }   // ascending j: ties keep the lower id
                 }
             } else {
                 const double2 pc = s_xy[cur];
@@ -1125,6 +1133,36 @@ __global__ void ls_dist_kernel(const double2* __restrict__ xy, int n, int k, con
         const int32_t d = euc2d(xy[i], xy[j]);
         nnd[e] = d;
         if (nnp) nnp[e] = j | ((uint32_t)d << 16);
+    }
+}
+
+// The same lists for n <= 1024 by one warp per row: lane l keeps the keys d << 10 | j of its
+// cities j = l, l + 32, ... in registers (d < 2^22 for |coordinates| < 2^20 -- else the block
+// kernel), and each of the cl rounds takes the warp minimum above the previous one (keys are
+// unique, so the (d, id) order is the key order).
+constexpr int kCandWarpMaxN = 1024;
+__global__ void __launch_bounds__(256) cand_lists_warp_kernel(const double2* __restrict__ xy, int n, int cl,
+                                                             uint16_t* __restrict__ out, int out_ld) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int i = gw; i < n; i += nwarps) {
+        const double2 pi = xy[i];
+        uint32_t key[kCandWarpMaxN / 32];
+#pragma unroll
+        for (int t = 0; t < kCandWarpMaxN / 32; ++t) {
+            const int j = lane + 32 * t;
+            key[t] = (j < n && j != i) ? ((uint32_t)euc2d(pi, xy[j]) << 10) | (uint32_t)j : kNone;
+        }
+        uint32_t prev = 0u;
+        for (int k = 0; k < cl; ++k) {
+            uint32_t best = kNone;
+#pragma unroll
+            for (int t = 0; t < kCandWarpMaxN / 32; ++t)
+                if ((k == 0 || key[t] > prev) && key[t] < best) best = key[t];
+            best = __reduce_min_sync(kFull, best);
+            if (lane == 0) out[(size_t)i * out_ld + k] = (uint16_t)(best & 0x3FFu);
+            prev = best;
+        }
     }
 }
 

@@ -783,9 +783,16 @@ int setup(mmas_ctx* h) {
                                h->stream));
             CU(cudaStreamSynchronize(h->stream));
         }
-        cudaFuncSetAttribute(cand_lists_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin - 2048);
-        cand_lists_kernel<<<std::min(n, 8 * h->num_sms), 256, (size_t)n * 4, h->stream>>>(h->xy, n, h->cl, h->cand_id,
-                                                                                          h->cl_ld);
+        // n <= 1024 with distances < 2^22 (|coordinates| < 2^20): one warp per row, keys in registers
+        double cmax = 0.0;
+        for (int i = 0; i < 2 * n; ++i) cmax = std::max(cmax, std::fabs(c.coords[i]));
+        if (n <= kCandWarpMaxN && cmax < 1048576.0 && !std::getenv("MMAS_CAND_BLOCK")) {
+            cand_lists_warp_kernel<<<std::max(1, (n + 7) / 8), 256, 0, h->stream>>>(h->xy, n, h->cl, h->cand_id, h->cl_ld);
+        } else {
+            cudaFuncSetAttribute(cand_lists_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin - 2048);
+            cand_lists_kernel<<<std::min(n, 8 * h->num_sms), 256, (size_t)n * 4, h->stream>>>(h->xy, n, h->cl,
+                                                                                              h->cand_id, h->cl_ld);
+        }
         h->launches++;
         CU(cudaGetLastError());
     } else if (h->cl > 0) {

@@ -389,6 +389,17 @@ def test_best_length_async_matches_sync_reads():
 
 
 # ---- setup: the NN tour (Alg. 1, R3) behind the limits ---------------------------
+@pytest.mark.parametrize("n,cl", [(300, 16), (1024, 32), (1025, 8)], ids=["n300", "n1024", "n1025"])
+def test_candidate_lists_block_and_warp_kernels(n, cl, monkeypatch):
+    """The candidate lists (R10: the cl nearest by (d, id)) of the warp-per-row kernel (n <= 1024,
+    the default) and of the block kernel (MMAS_CAND_BLOCK=1) equal the oracle's."""
+    c = make_coords("uniform", n, 700 + n)
+    o = oracle.Colony(c, 4, cl, seed=1)
+    assert np.array_equal(mmas.Colony(c, 4, cl, seed=1).cand(), o.cand())
+    monkeypatch.setenv("MMAS_CAND_BLOCK", "1")
+    assert np.array_equal(mmas.Colony(c, 4, cl, seed=1).cand(), o.cand())
+
+
 @pytest.mark.parametrize("block", [False, True], ids=["warp-kernel", "block-kernel"])
 @pytest.mark.parametrize("n,cl,frac", [(198, 16, False), (1002, 32, False), (300, 0, False), (257, 8, True)],
                          ids=["d198", "pr1002", "no-lists", "fractional"])
