@@ -267,6 +267,14 @@ int64_t mmas_kernel_launches(const mmas_ctx *h);
  * mmas_debug_log2: out[i] = device det_log2(u[i]) for normal u[i] > 0 (host arrays). */
 int mmas_debug_philox(const uint32_t *ctr_key, int64_t count, uint32_t *out_words, float *out_log2);
 int mmas_debug_log2(const float *u, int64_t count, float *out);
+/* Measurement tooling of -DMMAS_TRACE builds (tools/trace_phases.py, tools/trace_warps.py,
+ * tools/fb_cycles.py); every other build returns MMAS_ESTATE and writes nothing.
+ * mmas_debug_trace: %globaltimer stamps, 8 per block (u64, count <= 8192);
+ * mmas_debug_trace_warps: the time each ant warp finished its last ant, 16 per block (count <= 16384);
+ * mmas_debug_fb_cycles: 64 u64 counters of the fallback scans (kernels.cuh g_fbcyc), then zeroed. */
+int mmas_debug_trace(unsigned long long *out, int count);
+int mmas_debug_trace_warps(unsigned long long *out, int count);
+int mmas_debug_fb_cycles(unsigned long long *out);
 
 /* ---- checkpoint / resume (synchronous; caller-owned host buffer) ----
  * The random numbers are counter-based (keyed by seed, iteration, ant, step, city; R13), so a

@@ -36,6 +36,7 @@ EXPORTED = (
     "mmas_get_inv_w", "mmas_get_heuristic", "mmas_get_candidates", "mmas_get_limits",
     "mmas_get_stats", "mmas_profile", "mmas_get_phase_times", "mmas_kernel_launches",
     "mmas_stream", "mmas_sync", "mmas_debug_philox", "mmas_debug_log2",
+    "mmas_debug_trace", "mmas_debug_trace_warps", "mmas_debug_fb_cycles",
 )
 
 
