@@ -1053,11 +1053,28 @@ __global__ void __launch_bounds__(32) nn_tour_warp_kernel(const double2* __restr
     double2* s_xy = reinterpret_cast<double2*>(nnw_smem + 2048);
     uint16_t* s_cand = reinterpret_cast<uint16_t*>(nnw_smem + 2048 + ((xy_b + 15) & ~(size_t)15));
     const int lane = threadIdx.x;
-    for (int i = lane; i < n; i += 32) {
-        if (xys) s_xys[i] = xys[i];
-        else s_xy[i] = xy[i];
-    }
-    for (int i = lane; i < n * cl_ld; i += 32) s_cand[i] = cand[i];
+    // staging in 16-byte pieces, several in flight per lane (one warp moves ~70 KB for C2: u16
+    // element copies took most of the kernel)
+    auto stage16 = [&](void* dst, const void* src, size_t bytes) {
+        const size_t n16 = bytes / 16;
+        uint4* d = reinterpret_cast<uint4*>(dst);
+        const uint4* g = reinterpret_cast<const uint4*>(src);
+        size_t i = lane;
+        for (; i + 96 < n16; i += 128) {
+            const uint4 a = __ldg(g + i), b = __ldg(g + i + 32), c = __ldg(g + i + 64), e = __ldg(g + i + 96);
+            d[i] = a;
+            d[i + 32] = b;
+            d[i + 64] = c;
+            d[i + 96] = e;
+        }
+        for (; i < n16; i += 32) d[i] = __ldg(g + i);
+        const unsigned char* gs = reinterpret_cast<const unsigned char*>(src);
+        unsigned char* ds = reinterpret_cast<unsigned char*>(dst);
+        for (size_t b = n16 * 16 + lane; b < bytes; b += 32) ds[b] = gs[b];   // (tail bytes)
+    };
+    if (xys) stage16(s_xys, xys, (size_t)n * 4);
+    else stage16(s_xy, xy, (size_t)n * 16);
+    if (cl_ld > 0) stage16(s_cand, cand, (size_t)n * cl_ld * 2);
     uint32_t wt = lane == 0 ? 1u : 0u;   // city 0 visited
     const int cnt = (n - lane + 31) >> 5;   // this lane's cities l + 32 k < n
     const uint32_t mine = cnt >= 32 ? 0xFFFFFFFFu : cnt <= 0 ? 0u : (1u << cnt) - 1u;
