@@ -529,7 +529,10 @@ __device__ __forceinline__ void compact_scan(IvF ivf, const Tabu tabu, int n, ui
                                              uint32_t iter, PhiloxKey key, int lane, uint32_t& bm, uint32_t& bc) {
     const long long t0 = trace_clock();
     auto it = lane_cities(tabu, n, lane);
-    const uint32_t cnt = (uint32_t)it.count();
+    // the register tabu counts a lane's cities with one popc; the shared-memory tabu would read
+    // every word twice, so its rounds are sized by ballots over the fetched cities instead
+    constexpr bool kCount = std::is_same<decltype(it), LaneCitiesReg>::value;
+    const uint32_t cnt = kCount ? (uint32_t)it.count() : 0u;
     // K cities per lane at a time, branch-free (a lane with fewer carries kNone), so the K
     // Philox / log chains interleave
     auto eval = [&](auto K, const uint32_t* c, const float* iv) {
@@ -568,17 +571,28 @@ __device__ __forceinline__ void compact_scan(IvF ivf, const Tabu tabu, int n, ui
         }
     };
     fetch();
-    const int most = (int)__reduce_max_sync(kFull, cnt);
-    const long long t1 = trace_clock();
-    for (int r = 0;;) {
-        // (warp-uniform) 8, 4 or 2 chains: the short tail rounds issue only what they use
-        if (r + 4 < most) eval(std::integral_constant<int, 8>{}, c, iv);
-        else if (r + 2 < most) eval(std::integral_constant<int, 4>{}, c, iv);
-        else eval(std::integral_constant<int, 2>{}, c, iv);
-        r += 8;
-        if (r >= most) break;
-        fetch();
+    if constexpr (kCount) {
+        const int most = (int)__reduce_max_sync(kFull, cnt);
+        for (int r = 0;;) {
+            // (warp-uniform) 8, 4 or 2 chains: the short tail rounds issue only what they use
+            if (r + 4 < most) eval(std::integral_constant<int, 8>{}, c, iv);
+            else if (r + 2 < most) eval(std::integral_constant<int, 4>{}, c, iv);
+            else eval(std::integral_constant<int, 2>{}, c, iv);
+            r += 8;
+            if (r >= most) break;
+            fetch();
+        }
+    } else {
+        // a lane's fetched cities fill c[0], c[1], ... before kNone
+        while (__any_sync(kFull, c[0] != kNone)) {
+            if (__any_sync(kFull, c[4] != kNone)) eval(std::integral_constant<int, 8>{}, c, iv);
+            else if (__any_sync(kFull, c[2] != kNone)) eval(std::integral_constant<int, 4>{}, c, iv);
+            else eval(std::integral_constant<int, 2>{}, c, iv);
+            if (!__any_sync(kFull, c[7] != kNone)) break;   // every lane ran out in this round
+            fetch();
+        }
     }
+    const long long t1 = t0;
     trace_compact(lane, t0, t1, trace_clock(), trace_clock());
 }
 template <class Tabu>
