@@ -1080,15 +1080,28 @@ __global__ void __launch_bounds__(32) nn_tour_warp_kernel(const double2* __restr
     const uint32_t mine = cnt >= 32 ? 0xFFFFFFFFu : cnt <= 0 ? 0u : (1u << cnt) - 1u;
     if (lane == 0) route[0] = 0;
     __syncwarp();
+    // the row stride and this lane's slot in registers (ptxas otherwise reloads them from the
+    // constant bank inside the step chain)
+    uint32_t row_ld = (uint32_t)cl_ld, slot_ok = lane < cl ? 1u : 0u;
+    uint32_t s_base = (uint32_t)__cvta_generic_to_shared(s_cand) + 2u * (uint32_t)lane;
+    asm volatile("" : "+r"(row_ld), "+r"(slot_ok), "+r"(s_base));
     int cur = 0;
     for (int s = 1; s < n; ++s) {
         uint32_t nxt = kNone;
-        for (int k0 = 0; k0 < cl && nxt == kNone; k0 += 32) {
-            const int k = k0 + lane;
-            const uint32_t c = k < cl ? (uint32_t)s_cand[cur * cl_ld + k] : 0u;
+        if (cl <= 32) {   // one row read per step (C1, C2)
+            uint32_t c = 0u;
+            if (slot_ok) asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c) : "r"(s_base + 2u * (uint32_t)cur * row_ld));
             const bool vis = (__shfl_sync(kFull, wt, (int)(c & 31u)) >> (c >> 5)) & 1u;
-            const uint32_t m = __ballot_sync(kFull, k < cl && !vis);
+            const uint32_t m = __ballot_sync(kFull, slot_ok && !vis);
             if (m) nxt = __shfl_sync(kFull, c, __ffs(m) - 1);
+        } else {
+            for (int k0 = 0; k0 < cl && nxt == kNone; k0 += 32) {
+                const int k = k0 + lane;
+                const uint32_t c = k < cl ? (uint32_t)s_cand[cur * cl_ld + k] : 0u;
+                const bool vis = (__shfl_sync(kFull, wt, (int)(c & 31u)) >> (c >> 5)) & 1u;
+                const uint32_t m = __ballot_sync(kFull, k < cl && !vis);
+                if (m) nxt = __shfl_sync(kFull, c, __ffs(m) - 1);
+            }
         }
         if (nxt == kNone) {   // the row is exhausted (or no lists): the warp scans
             uint32_t bd = kNone, bj = kNone;
