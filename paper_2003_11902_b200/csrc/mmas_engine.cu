@@ -1018,6 +1018,7 @@ int setup(mmas_ctx* h) {
         // the SMs are shared out between the colonies (one persistent block per SM each)
         const int sms = std::max(1, h->num_sms / h->colonies);
         int w = std::max(1, std::min(wmax, (h->m_local + sms - 1) / sms));
+        if (const char* e = std::getenv("MMAS_CONS_WARPS")) w = std::max(1, std::min(wmax, std::atoi(e)));   // (A/B)
         size_t need = 128 + (size_t)h->tb_inv + h->tb_id + 16 + (size_t)w * per_warp;
         h->smem_table = need <= cons_dyn_max;
         if (h->smem_table) {
