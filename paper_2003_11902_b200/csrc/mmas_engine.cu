@@ -1040,6 +1040,7 @@ int setup(mmas_ctx* h) {
         } else {
             h->cons_warps = 4;
             h->cons_grid = std::max(1, (h->m_local + 3) / 4);
+            if (const char* e = std::getenv("MMAS_CONS_GRID")) h->cons_grid = std::max(1, std::atoi(e));   // (A/B)
             h->cons_smem = 128 + 16 + 4 * per_warp;
             // per warp kFbBufs 8 KB chunk buffers for the R9 fallback scans over HBM-resident rows
             // (construct.cuh scan_unvisited_staged), when they leave room for two blocks per SM
