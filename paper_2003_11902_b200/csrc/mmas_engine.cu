@@ -1099,12 +1099,14 @@ int setup(mmas_ctx* h) {
     // cheaper to scan whole; the shared-memory tabu with L2-resident rows (C3) 64 (5.13 ->
     // 5.06 ms; 128+ slower: the per-lane word counts); HBM-resident rows (C5, paired scans)
     // n / 8 (construction 18.6 -> 14.7 ms at 2048; 4096: 15.0, 9256: 16.9); the memory-lean
-    // pheromone, whose trip scans recompute every background value from the coordinates, n / 2
-    // (C65KL 1256 -> ~300 ms per iteration, C5L construction 44 -> 25 ms).
+    // pheromone, whose trip scans recompute every background value from the coordinates, n / 2,
+    // and every fallback beyond 32768 cities (C5L construction 44 -> 25 ms at 9256, 27.3 at n;
+    // C65KL 1256 -> 293 ms per iteration at n, 318 at n / 2, 384 at n / 4).
     // MMAS_FB_COMPACT=<cap> overrides (0 = off; the parity tests force every variant).
     if (h->cl > 0 && !h->rwm) {
         const bool hbm_rows = 4.0 * (double)n * h->ld > 0.75 * (double)h->l2_bytes;
-        int cap = h->lean ? n / 2 : h->reg_tabu ? (n > 512 && !hbm_rows ? 224 : 0) : (hbm_rows ? n / 8 : 64);
+        int cap = h->lean ? (n > 32768 ? n : n / 2)
+                          : h->reg_tabu ? (n > 512 && !hbm_rows ? 224 : 0) : (hbm_rows ? n / 8 : 64);
         if (const char* e = std::getenv("MMAS_FB_COMPACT")) cap = std::max(0, std::atoi(e));
         h->fb_lane_cap = cap;
     } else if (h->cl == 0 && !h->rwm && !h->compact_tabu) {
